@@ -1,0 +1,180 @@
+"""CPU oracle for the ASK Mandelbrot path — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg
+may import this package.  The product package (paper_2206_02255_b200) never imports it
+and shares no code with it; the only shared module is the input definitions in
+workloads.py, which hold none of the method's arithmetic.
+
+Contents:
+  * mandel_oracle.c  -- plain single-threaded C: dwell, Ex,
+                        recursive Mariani-Silver / ASK, ASK-by-lookup.
+  * montecarlo.py    -- Bernoulli subdivision-tree simulation of the cost model's work
+                        (P:120-182), the oracle for costmodel.W_S / W_SSD.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+from typing import Optional, Sequence, Tuple
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "mandel_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared"]
+
+MAX_LEVELS = 32
+
+_lock = threading.Lock()
+_lib: Optional[ctypes.CDLL] = None
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with contraction off (R4)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+class Region(ctypes.Structure):
+    _fields_ = [("re_min", ctypes.c_double), ("re_max", ctypes.c_double),
+                ("im_min", ctypes.c_double), ("im_max", ctypes.c_double)]
+
+
+class LevelStats(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_int64) for k in (
+        "regions_in", "filled", "subdivided", "leaves",
+        "border_px", "border_iters", "leaf_px", "leaf_iters")]
+
+
+class RegionRec(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_int32) for k in ("x", "y", "d", "kind", "value", "level")]
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    with _lock:
+        if _lib is None:
+            L = ctypes.CDLL(build())
+            P = ctypes.POINTER
+            i32p, i64p = P(ctypes.c_int32), P(ctypes.c_int64)
+            L.oracle_dwell.restype = ctypes.c_int32
+            L.oracle_dwell.argtypes = [ctypes.c_float, ctypes.c_float, ctypes.c_int32]
+            L.oracle_pixel_c.restype = None
+            L.oracle_pixel_c.argtypes = [Region, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                         P(ctypes.c_float), P(ctypes.c_float)]
+            L.oracle_exhaustive_rows.restype = None
+            L.oracle_exhaustive_rows.argtypes = [Region, ctypes.c_int64, ctypes.c_int32,
+                                                 ctypes.c_int64, ctypes.c_int64, i32p]
+            L.oracle_dwell_pixels.restype = None
+            L.oracle_dwell_pixels.argtypes = [Region, ctypes.c_int64, ctypes.c_int32, i64p, i64p,
+                                              ctypes.c_int64, i32p]
+            L.oracle_ask.restype = ctypes.c_int
+            L.oracle_ask.argtypes = [Region, ctypes.c_int64, ctypes.c_int32, ctypes.c_int,
+                                     ctypes.c_int, ctypes.c_int, i32p, ctypes.c_int64, i32p,
+                                     P(LevelStats), ctypes.c_int, P(RegionRec), ctypes.c_int64,
+                                     i64p]
+            L.oracle_ask_by_lookup.restype = ctypes.c_int
+            L.oracle_ask_by_lookup.argtypes = [i32p, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                               ctypes.c_int, i32p, ctypes.c_int64, i32p,
+                                               P(LevelStats), ctypes.c_int]
+            _lib = L
+    return _lib
+
+
+def _i32(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+
+
+def _i64(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+
+
+def dwell(cr: float, ci: float, maxdwell: int) -> int:
+    """Dwell of c = cr + i ci (both rounded to float32 first)."""
+    return int(lib().oracle_dwell(cr, ci, maxdwell))
+
+
+def pixel_c(region, n: int, i: int, j: int) -> Tuple[float, float]:
+    cr, ci = ctypes.c_float(), ctypes.c_float()
+    lib().oracle_pixel_c(Region(*region), n, i, j, ctypes.byref(cr), ctypes.byref(ci))
+    return cr.value, ci.value
+
+
+def exhaustive(region, n: int, maxdwell: int, row0: int = 0, rows: Optional[int] = None) -> np.ndarray:
+    """Ex image rows [row0, row0+rows) as int32 (rows x n)."""
+    rows = n - row0 if rows is None else rows
+    out = np.empty((rows, n), dtype=np.int32)
+    lib().oracle_exhaustive_rows(Region(*region), n, maxdwell, row0, rows, _i32(out))
+    return out
+
+
+def dwell_pixels(region, n: int, maxdwell: int, ii, jj) -> np.ndarray:
+    ii = np.ascontiguousarray(ii, dtype=np.int64)
+    jj = np.ascontiguousarray(jj, dtype=np.int64)
+    out = np.empty(ii.shape, dtype=np.int32)
+    lib().oracle_dwell_pixels(Region(*region), n, maxdwell, _i64(ii), _i64(jj), ii.size, _i32(out))
+    return out
+
+
+def _stats_list(st, levels: int) -> list:
+    out = []
+    for lv in range(levels):
+        s = st[lv]
+        d = {k: int(getattr(s, k)) for k, _ in LevelStats._fields_}
+        if d["regions_in"] == 0:
+            break
+        d["level"] = lv
+        out.append(d)
+    return out
+
+
+def ask(region, n: int, maxdwell: int, g: int, r: int, B: int,
+        tiles: Optional[Sequence[int]] = None, out: Optional[np.ndarray] = None,
+        want_regions: bool = False):
+    """Recursive ASK (Mariani-Silver) image.  Returns (image, level_stats[, region_recs]).
+
+    With `tiles`, only those level-0 tiles (canonical k = gy*g + gx) are computed; pixels
+    outside them keep the value they have in `out` (default: -1)."""
+    L = lib()
+    if out is None:
+        out = np.full((n, n), -1, dtype=np.int32)
+    st = (LevelStats * MAX_LEVELS)()
+    t_arr = None if tiles is None else np.ascontiguousarray(tiles, dtype=np.int32)
+    recs = None
+    cap = 0
+    cnt = ctypes.c_int64(0)
+    if want_regions:
+        cap = 4 * n * n // max(1, B * B) + 16
+        recs = (RegionRec * cap)()
+    rc = L.oracle_ask(Region(*region), n, maxdwell, g, r, B,
+                      None if t_arr is None else _i32(t_arr), 0 if t_arr is None else t_arr.size,
+                      _i32(out), st, MAX_LEVELS, recs, cap, ctypes.byref(cnt))
+    if rc != 0:
+        raise ValueError(f"oracle_ask failed rc={rc}")
+    stats = _stats_list(st, MAX_LEVELS)
+    if want_regions:
+        arr = np.ctypeslib.as_array(recs)[: cnt.value]
+        recs_np = np.array([tuple(x) for x in arr], dtype=np.int64).reshape(-1, 6)
+        return out, stats, recs_np
+    return out, stats
+
+
+def ask_by_lookup(E: np.ndarray, g: int, r: int, B: int, tiles: Optional[Sequence[int]] = None):
+    """ASK decisions replayed over an exhaustive image E."""
+    E = np.ascontiguousarray(E, dtype=np.int32)
+    n = E.shape[0]
+    out = np.full((n, n), -1, dtype=np.int32)
+    st = (LevelStats * MAX_LEVELS)()
+    t_arr = None if tiles is None else np.ascontiguousarray(tiles, dtype=np.int32)
+    rc = lib().oracle_ask_by_lookup(_i32(E), n, g, r, B,
+                                    None if t_arr is None else _i32(t_arr),
+                                    0 if t_arr is None else t_arr.size, _i32(out), st, MAX_LEVELS)
+    if rc != 0:
+        raise ValueError(f"oracle_ask_by_lookup failed rc={rc}")
+    return out, _stats_list(st, MAX_LEVELS)
