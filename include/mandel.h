@@ -1,0 +1,146 @@
+/*
+ * mandel.h -- C ABI of the B200 ASK Mandelbrot library (libmandel_b200.so).
+ *
+ * The operations are the paper's (P:NNN = /root/reference/PAPER.md line NNN):
+ *   mandel_exhaustive   the exhaustive approach Ex: one flat kernel, one thread per pixel
+ *                       (P:111-117 eq:exhaustive-general; "Ex: Exhaustive approach in
+ *                       one flat kernel execution").
+ *   mandel_ask          Adaptive Serial Kernels (Sec. 5) applied to the
+ *                       Mariani-Silver subdivision of the Mandelbrot set:
+ *                       initial g x g regions, border dwell per region, fill if the border is
+ *                       uniform, else split r x r while the child side stays >= B, else
+ *                       per-pixel dwell (leaf).  "Generating the Mandelbrot set in the complex
+ *                       plane [region] using a dwell of d ... problem size n x n".
+ *   mandel_ask_tiles    mandel_ask restricted to a subset of the level-0 regions (the
+ *                       multi-GPU partition: each rank runs its own tiles).
+ *
+ * Arithmetic (R2-R4): dwell = first i >= 1 with |z_i|^2 > 4 (z_0 = 0), else
+ * maxdwell; IEEE binary32, round-to-nearest, no FMA contraction, no FTZ, operation order
+ * x2=x*x, y2=y*y, xy=x*y, x=(x2-y2)+cr, y=(xy+xy)+ci.  Pixel (row i, column j) samples
+ * its centre c = cr + i ci with cr = (float)re_min + ((float)j+0.5f)*dx and
+ * ci = (float)im_min + ((float)i+0.5f)*dy, dx = (float)((re_max-re_min)/n), dy likewise
+ * (each a single RN float operation); row i = 0 is the im_min side.
+ *
+ * Memory and ownership:
+ *   - d_out: caller-owned DEVICE buffer of int32, row-major, row i at d_out + i*out_pitch
+ *     (out_pitch >= n elements).  mandel_exhaustive and mandel_ask write every pixel;
+ *     mandel_ask_tiles writes only the pixels of its tiles.  The vectorised fill needs
+ *     d_out 16-byte aligned and out_pitch % 4 == 0; other layouts fall back to 4-byte stores.
+ *   - d_ws: caller-owned DEVICE workspace of >= mandel_ask_workspace_bytes(...) bytes
+ *     (offset lists, fill/leaf lists, counters).  One in-flight call per workspace.
+ *   - The library never allocates device memory.  It caches one captured CUDA graph per
+ *     distinct call (key: device, all arguments, pointers); mandel_shutdown() frees them.
+ *   - Calls are asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream),
+ *     except mandel_ask_last_stats, which synchronises it.
+ *
+ * Errors: every function returns MANDEL_OK or an error code and never throws.
+ *   MANDEL_EINVAL      invalid argument (checked synchronously, nothing launched):
+ *                      n, g, r, B powers of two; r >= 2; B >= 2; g*B <= n; n <= 65536;
+ *                      1 <= maxdwell; re_min < re_max, im_min < im_max (finite);
+ *                      out_pitch >= n; non-null pointers; tile ids in [0, g*g), unique.
+ *   MANDEL_EWORKSPACE  ws_bytes < mandel_ask_workspace_bytes(...).
+ *   MANDEL_ECUDA       a CUDA runtime call or launch failed (see mandel_last_cuda_error()).
+ */
+#ifndef MANDEL_B200_H
+#define MANDEL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Complex-plane window, SPEC.md S:173-176 Viewport.  */
+typedef struct {
+    double re_min, re_max, im_min, im_max;
+} mandel_region;
+
+/* Per-level statistics (SPEC.md S:274-277 LevelStats, extended with pixel counts). */
+typedef struct {
+    int32_t level;        /* 0 = the initial g x g split                                    */
+    int32_t side;         /* region side d at this level: n/(g r^level)                     */
+    int64_t regions_in;   /* regions examined (= |G_level|)                          */
+    int64_t filled;       /* uniform border -> filled (terminal work T)              */
+    int64_t subdivided;   /* non-uniform, d/r >= B -> r*r children              */
+    int64_t leaves;       /* non-uniform, d/r <  B -> per-pixel dwell (L)        */
+    int64_t border_px;    /* border pixels whose dwell this level computed                  */
+    int64_t border_iters; /* iterations counted for them (= sum of their dwells)            */
+    int64_t leaf_px;      /* leaf interior pixels computed at this level                    */
+    int64_t leaf_iters;   /* sum of their dwells                                           */
+} mandel_level_stats;
+
+enum {
+    MANDEL_OK = 0,
+    MANDEL_EINVAL = 1,
+    MANDEL_EWORKSPACE = 2,
+    MANDEL_ECUDA = 3
+};
+
+/* Scheme of the subdivision kernels.  Both produce bit-identical images.
+ *   MANDEL_SCHEME_SBR   the paper's ASK-SBR: per level one CUDA
+ *                       block per region computes the region's whole border (split across
+ *                       its warps, reduced with warp reductions), then appends to the fill
+ *                       list / next-level offset list / leaf list; leaves: one block each.
+ *   MANDEL_SCHEME_B200  B200 re-design: border dwells are written to the
+ *                       image and reused -- a child only computes the new internal division
+ *                       lines of its parent -- by a flat, load-balanced kernel over all new
+ *                       border pixels of the level; a warp per region then decides
+ *                       uniformity from the image with warp reductions; leaf interiors run
+ *                       as one flat pixel-parallel kernel.                                */
+enum {
+    MANDEL_SCHEME_SBR = 0,
+    MANDEL_SCHEME_B200 = 1
+};
+
+/* flags */
+#define MANDEL_FLAG_STATS 1u /* also accumulate border/leaf pixel + iteration counters */
+
+/* Bytes of workspace mandel_ask / mandel_ask_tiles need for these parameters (worst case
+ * over all images: every region at every level may subdivide).  0 if invalid. */
+size_t mandel_ask_workspace_bytes(int64_t n, int32_t g, int32_t r, int32_t B);
+
+/* Number of subdivision levels ASK runs: 1 + floor(log_r((n/g)/B)).  0 if invalid. */
+int32_t mandel_ask_levels(int64_t n, int32_t g, int32_t r, int32_t B);
+
+/* Exhaustive dwell image Ex. */
+int mandel_exhaustive(mandel_region reg, int64_t n, int32_t maxdwell, int32_t *d_out,
+                      int64_t out_pitch, void *stream);
+
+/* Full ASK image over all g*g level-0 regions. */
+int mandel_ask(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, int32_t r, int32_t B,
+               int32_t *d_out, int64_t out_pitch, void *d_ws, size_t ws_bytes, void *stream);
+
+/* ASK over the level-0 regions h_tile_ids[0..n_tiles) (HOST array; canonical id
+ * k = gy*g + gx), with an explicit scheme and flags.  n_tiles == 0 with h_tile_ids == NULL
+ * means all g*g tiles in canonical order. */
+int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, int32_t r,
+                     int32_t B, const int32_t *h_tile_ids, int32_t n_tiles, int32_t scheme,
+                     uint32_t flags, int32_t *d_out, int64_t out_pitch, void *d_ws,
+                     size_t ws_bytes, void *stream);
+
+/* End-to-end variant over HOST memory: runs mandel_ask_tiles into the device buffer d_out
+ * and copies the n x n image (rows of n elements) into h_out (host; pinned for full
+ * bandwidth), then synchronises `stream`.  For tile runs only the tiles' pixels are
+ * meaningful.  h_out is written with row pitch n. */
+int mandel_ask_to_host(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, int32_t r,
+                       int32_t B, const int32_t *h_tile_ids, int32_t n_tiles, int32_t scheme,
+                       int32_t *d_out, int64_t out_pitch, void *d_ws, size_t ws_bytes,
+                       int32_t *h_out, void *stream);
+
+/* Per-level statistics of the last call that used d_ws (synchronises `stream`).
+ * Writes min(levels, max_levels) entries; returns the number of levels (>= 0) or -code. */
+int mandel_ask_last_stats(const void *d_ws, mandel_level_stats *h_out, int32_t max_levels,
+                          void *stream);
+
+/* Number of kernel launches one mandel_ask_tiles call issues for these parameters. */
+int32_t mandel_ask_kernel_count(int64_t n, int32_t g, int32_t r, int32_t B, int32_t scheme);
+
+const char *mandel_strerror(int code);
+const char *mandel_last_cuda_error(void);
+void mandel_shutdown(void); /* frees cached graphs/events/streams; owns no device buffers */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MANDEL_B200_H */

@@ -79,6 +79,12 @@ def lib() -> ctypes.CDLL:
                                      ctypes.c_int, ctypes.c_int, i32p, ctypes.c_int64, i32p,
                                      P(LevelStats), ctypes.c_int, P(RegionRec), ctypes.c_int64,
                                      i64p]
+            L.oracle_ask_window.restype = ctypes.c_int
+            L.oracle_ask_window.argtypes = [Region, ctypes.c_int64, ctypes.c_int32, ctypes.c_int,
+                                            ctypes.c_int, ctypes.c_int, i32p, ctypes.c_int64, i32p,
+                                            ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                            P(LevelStats), ctypes.c_int, P(RegionRec),
+                                            ctypes.c_int64, i64p]
             L.oracle_ask_by_lookup.restype = ctypes.c_int
             L.oracle_ask_by_lookup.argtypes = [i32p, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                                ctypes.c_int, i32p, ctypes.c_int64, i32p,
@@ -163,6 +169,22 @@ def ask(region, n: int, maxdwell: int, g: int, r: int, B: int,
         recs_np = np.array([tuple(x) for x in arr], dtype=np.int64).reshape(-1, 6)
         return out, stats, recs_np
     return out, stats
+
+
+def ask_tile(region, n: int, maxdwell: int, g: int, r: int, B: int, tile: int):
+    """ASK of a single level-0 tile into a (d0, d0) array (memory-light for large n).
+    Returns (tile image, level_stats)."""
+    d0 = n // g
+    gy, gx = divmod(int(tile), g)
+    out = np.full((d0, d0), -1, dtype=np.int32)
+    st = (LevelStats * MAX_LEVELS)()
+    t_arr = np.array([tile], dtype=np.int32)
+    cnt = ctypes.c_int64(0)
+    rc = lib().oracle_ask_window(Region(*region), n, maxdwell, g, r, B, _i32(t_arr), 1, _i32(out),
+                                 gx * d0, gy * d0, d0, st, MAX_LEVELS, None, 0, ctypes.byref(cnt))
+    if rc != 0:
+        raise ValueError(f"oracle_ask_window failed rc={rc}")
+    return out, _stats_list(st, MAX_LEVELS)
 
 
 def ask_by_lookup(E: np.ndarray, g: int, r: int, B: int, tiles: Optional[Sequence[int]] = None):

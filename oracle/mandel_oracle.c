@@ -129,7 +129,8 @@ typedef struct {
     int32_t maxdwell;
     int r, B;
     const int32_t *lookup; /* NULL: compute dwells; else read them from this n x n image */
-    int32_t *out;
+    int32_t *out;          /* pixel (x, y) is stored at out[(y - oy) * opitch + (x - ox)]  */
+    int64_t ox, oy, opitch;
     oracle_level_stats *stats;
     int max_levels;
     oracle_region_rec *recs;
@@ -199,7 +200,7 @@ static void ask_region(ask_ctx *c, int64_t x0, int64_t y0, int64_t d, int level)
     if (uniform) {
         for (int64_t y = y0; y < y0 + d; ++y)
             for (int64_t x = x0; x < x0 + d; ++x)
-                c->out[y * c->n + x] = v;
+                c->out[(y - c->oy) * c->opitch + (x - c->ox)] = v;
         if (st)
             st->filled++;
         add_rec(c, x0, y0, d, 0, v, level);
@@ -218,7 +219,7 @@ static void ask_region(ask_ctx *c, int64_t x0, int64_t y0, int64_t d, int level)
     for (int64_t y = y0; y < y0 + d; ++y) {
         for (int64_t x = x0; x < x0 + d; ++x) {
             int32_t w = ctx_dwell(c, x, y);
-            c->out[y * c->n + x] = w;
+            c->out[(y - c->oy) * c->opitch + (x - c->ox)] = w;
             int interior = !(x == x0 || x == x0 + d - 1 || y == y0 || y == y0 + d - 1);
             if (st && interior) {
                 st->leaf_px++;
@@ -260,13 +261,18 @@ static int run_ask(ask_ctx *c, int g, const int32_t *tiles, int64_t ntiles, int6
     return 0;
 }
 
-int oracle_ask(oracle_region reg, int64_t n, int32_t maxdwell, int g, int r, int B,
-               const int32_t *tiles, int64_t ntiles, int32_t *out,
-               oracle_level_stats *stats, int max_levels,
-               oracle_region_rec *recs, int64_t rec_cap, int64_t *rec_count)
+/* The output window: pixels are stored at out[(y - oy) * opitch + (x - ox)]; the caller
+ * guarantees that every pixel of the listed tiles falls inside it. */
+int oracle_ask_window(oracle_region reg, int64_t n, int32_t maxdwell, int g, int r, int B,
+                      const int32_t *tiles, int64_t ntiles, int32_t *out, int64_t ox, int64_t oy,
+                      int64_t opitch, oracle_level_stats *stats, int max_levels,
+                      oracle_region_rec *recs, int64_t rec_cap, int64_t *rec_count)
 {
     ask_ctx c;
     memset(&c, 0, sizeof c);
+    c.ox = ox;
+    c.oy = oy;
+    c.opitch = opitch;
     c.reg = reg;
     c.n = n;
     c.maxdwell = maxdwell;
@@ -282,6 +288,15 @@ int oracle_ask(oracle_region reg, int64_t n, int32_t maxdwell, int g, int r, int
     return run_ask(&c, g, tiles, ntiles, rec_count);
 }
 
+int oracle_ask(oracle_region reg, int64_t n, int32_t maxdwell, int g, int r, int B,
+               const int32_t *tiles, int64_t ntiles, int32_t *out,
+               oracle_level_stats *stats, int max_levels,
+               oracle_region_rec *recs, int64_t rec_cap, int64_t *rec_count)
+{
+    return oracle_ask_window(reg, n, maxdwell, g, r, B, tiles, ntiles, out, 0, 0, n, stats,
+                             max_levels, recs, rec_cap, rec_count);
+}
+
 int oracle_ask_by_lookup(const int32_t *E, int64_t n, int g, int r, int B,
                          const int32_t *tiles, int64_t ntiles, int32_t *out,
                          oracle_level_stats *stats, int max_levels)
@@ -293,6 +308,7 @@ int oracle_ask_by_lookup(const int32_t *E, int64_t n, int g, int r, int B,
     c.B = B;
     c.lookup = E;
     c.out = out;
+    c.opitch = n;
     c.stats = stats;
     c.max_levels = max_levels;
     return run_ask(&c, g, tiles, ntiles, NULL);

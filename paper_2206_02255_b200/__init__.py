@@ -1,0 +1,108 @@
+"""B200-native ASK Mandelbrot (arxiv 2206.02255): the paper's Adaptive Serial Kernels
+subdivision of the Mandelbrot dwell image, plus the exhaustive baseline, on sm_100a.
+
+Python API (torch supplies device memory and streams; every computation runs in
+libmandel_b200.so's CUDA kernels through the C ABI of include/mandel.h):
+
+    exhaustive(region, n, maxdwell, out=None)                  -> int32 (n, n) cuda tensor
+    ask(region, n, maxdwell, g, r, B, out=None, ws=None, tiles=None,
+        scheme="b200", stats=False)                             -> int32 (n, n) cuda tensor
+    ask_stats(ws)                                               -> per-level dict list
+    ask_to_host(region, n, maxdwell, g, r, B, h_out, out, ws)   -> h_out (pinned host)
+    workspace(n, g, r, B)                                       -> uint8 cuda tensor
+"""
+from __future__ import annotations
+
+from typing import List, Optional, Sequence
+
+from . import _lib
+
+SCHEMES = {"sbr": _lib.SCHEME_SBR, "b200": _lib.SCHEME_B200}
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream_ptr(stream) -> int:
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def levels(n: int, g: int, r: int, B: int) -> int:
+    return int(_lib.load().mandel_ask_levels(n, g, r, B))
+
+
+def workspace_bytes(n: int, g: int, r: int, B: int) -> int:
+    v = int(_lib.load().mandel_ask_workspace_bytes(n, g, r, B))
+    if v == 0:
+        raise ValueError(f"invalid ASK parameters n={n} g={g} r={r} B={B}")
+    return v
+
+
+def kernel_count(n: int, g: int, r: int, B: int, scheme: str = "b200") -> int:
+    return int(_lib.load().mandel_ask_kernel_count(n, g, r, B, SCHEMES[scheme]))
+
+
+def workspace(n: int, g: int, r: int, B: int, device=None):
+    torch = _torch()
+    return torch.empty(workspace_bytes(n, g, r, B), dtype=torch.uint8,
+                       device=device if device is not None else "cuda")
+
+
+def _image(n: int, out, device=None):
+    torch = _torch()
+    if out is None:
+        out = torch.empty((n, n), dtype=torch.int32, device=device if device is not None else "cuda")
+    if out.dtype != torch.int32 or out.dim() != 2 or out.shape[0] < n or out.shape[1] < n \
+            or out.stride(1) != 1 or not out.is_cuda:
+        raise ValueError("out must be a cuda int32 (>=n, >=n) tensor with unit column stride")
+    return out
+
+
+def exhaustive(region: Sequence[float], n: int, maxdwell: int, out=None, stream=None):
+    """Exhaustive dwell image: one thread per pixel."""
+    out = _image(n, out)
+    rc = _lib.load().mandel_exhaustive(_lib.region(region), n, maxdwell, out.data_ptr(),
+                                       out.stride(0), _stream_ptr(stream))
+    _lib.check(rc, "mandel_exhaustive")
+    return out
+
+
+def ask(region: Sequence[float], n: int, maxdwell: int, g: int, r: int, B: int, out=None, ws=None,
+        tiles: Optional[Sequence[int]] = None, scheme: str = "b200", stats: bool = False, stream=None):
+    """ASK dwell image over all g*g level-0 regions, or only `tiles`."""
+    out = _image(n, out)
+    if ws is None:
+        ws = workspace(n, g, r, B, device=out.device)
+    t_ptr, t_n, _keep = _lib.tiles_arg(tiles)
+    rc = _lib.load().mandel_ask_tiles(_lib.region(region), n, maxdwell, g, r, B, t_ptr, t_n,
+                                      SCHEMES[scheme], _lib.FLAG_STATS if stats else 0,
+                                      out.data_ptr(), out.stride(0), ws.data_ptr(), ws.numel(),
+                                      _stream_ptr(stream))
+    _lib.check(rc, "mandel_ask_tiles")
+    return out
+
+
+def ask_stats(ws, stream=None) -> List[dict]:
+    """Per-level statistics of the last ASK call on `ws` (synchronises the stream)."""
+    return _lib.stats(ws.data_ptr(), _stream_ptr(stream))
+
+
+def ask_to_host(region, n, maxdwell, g, r, B, h_out, out, ws, tiles=None, scheme="b200", stream=None):
+    """ASK through the C ABI into HOST memory h_out (n x n int32, ideally pinned)."""
+    torch = _torch()
+    if h_out.dtype != torch.int32 or h_out.is_cuda or not h_out.is_contiguous() or h_out.numel() < n * n:
+        raise ValueError("h_out must be a contiguous host int32 tensor of n*n elements")
+    t_ptr, t_n, _keep = _lib.tiles_arg(tiles)
+    rc = _lib.load().mandel_ask_to_host(_lib.region(region), n, maxdwell, g, r, B, t_ptr, t_n,
+                                        SCHEMES[scheme], out.data_ptr(), out.stride(0), ws.data_ptr(),
+                                        ws.numel(), h_out.data_ptr(), _stream_ptr(stream))
+    _lib.check(rc, "mandel_ask_to_host")
+    return h_out
+
+
+def shutdown() -> None:
+    _lib.load().mandel_shutdown()

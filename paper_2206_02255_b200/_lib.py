@@ -1,0 +1,113 @@
+"""ctypes binding of libmandel_b200.so (include/mandel.h) -- argument marshalling only.
+
+Every step of the path runs in the library's sm_100a kernels; this module only converts
+Python/torch arguments to the C ABI.  There is no CPU fallback: if the library is missing
+or a call fails, an exception is raised.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from typing import List, Optional, Sequence
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmandel_b200.so")
+
+MANDEL_OK, MANDEL_EINVAL, MANDEL_EWORKSPACE, MANDEL_ECUDA = 0, 1, 2, 3
+SCHEME_SBR, SCHEME_B200 = 0, 1
+FLAG_STATS = 1
+
+_lock = threading.Lock()
+_lib: Optional[ctypes.CDLL] = None
+
+
+class MandelRegion(ctypes.Structure):
+    _fields_ = [("re_min", ctypes.c_double), ("re_max", ctypes.c_double),
+                ("im_min", ctypes.c_double), ("im_max", ctypes.c_double)]
+
+
+class MandelLevelStats(ctypes.Structure):
+    _fields_ = [("level", ctypes.c_int32), ("side", ctypes.c_int32)] + [
+        (k, ctypes.c_int64) for k in ("regions_in", "filled", "subdivided", "leaves",
+                                       "border_px", "border_iters", "leaf_px", "leaf_iters")]
+
+
+class MandelError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        lib = load()
+        msg = lib.mandel_strerror(code).decode()
+        if code == MANDEL_ECUDA:
+            msg += ": " + lib.mandel_last_cuda_error().decode()
+        super().__init__(f"{what}: {msg} (code {code})")
+        self.code = code
+
+
+# (name, restype, argtypes) of every exported symbol declared in include/mandel.h
+_P = ctypes.c_void_p
+_SIGS = [
+    ("mandel_ask_workspace_bytes", ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
+    ("mandel_ask_levels", ctypes.c_int32, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
+    ("mandel_exhaustive", ctypes.c_int, [MandelRegion, ctypes.c_int64, ctypes.c_int32, _P, ctypes.c_int64, _P]),
+    ("mandel_ask", ctypes.c_int, [MandelRegion, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                  ctypes.c_int32, _P, ctypes.c_int64, _P, ctypes.c_size_t, _P]),
+    ("mandel_ask_tiles", ctypes.c_int, [MandelRegion, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                        ctypes.c_int32, _P, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, _P,
+                                        ctypes.c_int64, _P, ctypes.c_size_t, _P]),
+    ("mandel_ask_to_host", ctypes.c_int, [MandelRegion, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                          ctypes.c_int32, ctypes.c_int32, _P, ctypes.c_int32, ctypes.c_int32, _P,
+                                          ctypes.c_int64, _P, ctypes.c_size_t, _P, _P]),
+    ("mandel_ask_last_stats", ctypes.c_int, [_P, ctypes.POINTER(MandelLevelStats), ctypes.c_int32, _P]),
+    ("mandel_ask_kernel_count", ctypes.c_int32, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                                 ctypes.c_int32]),
+    ("mandel_strerror", ctypes.c_char_p, [ctypes.c_int]),
+    ("mandel_last_cuda_error", ctypes.c_char_p, []),
+    ("mandel_shutdown", None, []),
+]
+EXPORTED = [s[0] for s in _SIGS]
+
+
+def load() -> ctypes.CDLL:
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(
+                    f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                    "(the CUDA extension is required; there is no CPU fallback)")
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, res, args in _SIGS:
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def region(r: Sequence[float]) -> MandelRegion:
+    return MandelRegion(*[float(v) for v in r])
+
+
+def check(code: int, what: str) -> None:
+    if code != MANDEL_OK:
+        raise MandelError(code, what)
+
+
+def tiles_arg(tiles):
+    if tiles is None:
+        return None, 0, None
+    arr = (ctypes.c_int32 * len(tiles))(*[int(t) for t in tiles])
+    return ctypes.cast(arr, ctypes.c_void_p), len(tiles), arr
+
+
+def stats(ws_ptr: int, stream_ptr: int, max_levels: int = 32) -> List[dict]:
+    lib = load()
+    buf = (MandelLevelStats * max_levels)()
+    L = lib.mandel_ask_last_stats(ws_ptr, buf, max_levels, stream_ptr)
+    if L < 0:
+        raise MandelError(-L, "mandel_ask_last_stats")
+    out = []
+    for i in range(min(L, max_levels)):
+        s = buf[i]
+        out.append({k: int(getattr(s, k)) for k, _ in MandelLevelStats._fields_})
+    return out

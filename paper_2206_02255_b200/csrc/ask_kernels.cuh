@@ -1,0 +1,430 @@
+// ask_kernels.cuh -- sm_100a kernels of the exhaustive baseline and the ASK level loop.
+//
+// P:NNN = /root/reference/PAPER.md line NNN.  Data layout in HBM:
+//   image   int32 row-major, pixel (row y, column x) at out[y*pitch + x]
+//   OLT     u32 packed region origin (x | y << 16), two ping-pong buffers
+//   fill    uint2 {packed origin, fill value}, one segment per level
+//   leaf    u32 packed origin of the last level's non-uniform regions
+//   header  counters: subdivided / filled per level, leaves, optional iteration stats
+#pragma once
+#include <limits.h>
+#include <stdint.h>
+
+#include "dwell.cuh"
+
+namespace mandel {
+
+constexpr int MAXL = 32;
+constexpr uint32_t WS_MAGIC = 0x4d41534bu; // "MASK"
+constexpr int DWELL_K = 8;                 // iterations per escape test (dwell.cuh)
+
+struct WsHeader {
+    uint32_t magic, levels, n, g, r, B, ntiles, scheme; // written by k_init
+    uint32_t n_subdiv[MAXL];                           // OLT "count" per level
+    uint32_t n_fill[MAXL];
+    uint32_t n_leaf;
+    uint32_t pad0;
+    unsigned long long border_px[MAXL], border_iters[MAXL];
+    unsigned long long leaf_px, leaf_iters;
+};
+static_assert(sizeof(WsHeader) <= 4096, "header");
+
+__device__ __forceinline__ uint32_t pack_xy(int x, int y) { return (uint32_t)x | ((uint32_t)y << 16); }
+__device__ __forceinline__ int unpack_x(uint32_t o) { return (int)(o & 0xffffu); }
+__device__ __forceinline__ int unpack_y(uint32_t o) { return (int)(o >> 16); }
+
+// Border pixel b in [0, 4d-4) of the region with origin (x0, y0) and side d: top row,
+// bottom row, then the left and right columns without their corners (each pixel once).
+__device__ __forceinline__ void ring_pixel(int b, int d, int x0, int y0, int &x, int &y)
+{
+    if (b < d) {
+        x = x0 + b;
+        y = y0;
+    } else if (b < 2 * d) {
+        x = x0 + (b - d);
+        y = y0 + d - 1;
+    } else if (b < 3 * d - 2) {
+        x = x0;
+        y = y0 + 1 + (b - 2 * d);
+    } else {
+        x = x0 + d - 1;
+        y = y0 + 1 + (b - (3 * d - 2));
+    }
+}
+
+struct ExArgs {
+    PixMap map;
+    int n, maxdwell;
+    long long pitch;
+    int *out;
+};
+
+struct LevelArgs {
+    PixMap map;
+    int maxdwell;
+    long long pitch;
+    int *out;
+    WsHeader *hdr;
+    const uint32_t *olt_in;  // regions of this level
+    uint32_t *olt_out;       // children for the next level
+    uint2 *fill;             // this level's fill segment
+    uint32_t *leaf;
+    const int32_t *tiles;    // k_init only (device-visible, may be NULL)
+    int level, d, r, B, g, ntiles, levels, scheme;
+    int subdivide;           // d / r >= B
+    int log2_q4, log2_row4;  // fill: log2(d*d/4), log2(d/4)
+};
+
+// --------------------------------------------------------------------------- helpers
+__device__ __forceinline__ uint32_t level_count(const LevelArgs &a)
+{
+    // |G_0| = number of tiles; |G_{l}| = r^2 * count_{l-1} ("count")
+    if (a.level == 0)
+        return (uint32_t)a.ntiles;
+    return (uint32_t)(a.r * a.r) * *((volatile uint32_t *)&a.hdr->n_subdiv[a.level - 1]);
+}
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <int TPB>
+__device__ __forceinline__ unsigned long long block_sum_u64(unsigned long long v, unsigned long long *s)
+{
+    v = warp_sum_u64(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0)
+        s[w] = v;
+    __syncthreads();
+    unsigned long long t = 0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < TPB / 32; ++i)
+            t += s[i];
+    return t; // valid in thread 0
+}
+
+// --------------------------------------------------------------------------- Ex
+// Exhaustive approach: one thread per pixel over the n x n grid.
+template <int BX, int BY>
+__global__ void __launch_bounds__(BX *BY) k_exhaustive(ExArgs a)
+{
+    const int x = blockIdx.x * BX + threadIdx.x;
+    const int y = blockIdx.y * BY + threadIdx.y;
+    if (x >= a.n || y >= a.n)
+        return;
+    const int v = dwell<DWELL_K>(pix_re(a.map, x), pix_im(a.map, y), a.maxdwell);
+    a.out[(long long)y * a.pitch + x] = v;
+}
+
+// --------------------------------------------------------------------------- init
+// Level-0 offset list: the initial g x g split ("initial compute grid |G_0|"),
+// canonical order or the caller's tile subset; zero the counters.
+__global__ void k_init(LevelArgs a)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    constexpr int hdr_words = sizeof(WsHeader) / 4;
+    uint32_t *hw = reinterpret_cast<uint32_t *>(a.hdr);
+    if (t >= 8 && t < hdr_words)
+        hw[t] = 0u;
+    if (t == 0) {
+        a.hdr->magic = WS_MAGIC;
+        a.hdr->levels = (uint32_t)a.levels;
+        a.hdr->n = 0; // filled below by thread 1 (keeps t==0 short)
+        a.hdr->g = (uint32_t)a.g;
+        a.hdr->r = (uint32_t)a.r;
+        a.hdr->B = (uint32_t)a.B;
+        a.hdr->ntiles = (uint32_t)a.ntiles;
+        a.hdr->scheme = (uint32_t)a.scheme;
+    }
+    if (t == 1)
+        a.hdr->n = (uint32_t)(a.d * a.g);
+    if (t < a.ntiles) {
+        const int k = a.tiles ? a.tiles[t] : t;
+        const int gx = k % a.g, gy = k / a.g;
+        const_cast<uint32_t *>(a.olt_in)[t] = pack_xy(gx * a.d, gy * a.d);
+    }
+}
+
+// --------------------------------------------------------------------------- decisions
+// Common tail of the per-region decision: uniform -> fill list;
+// non-uniform and d/r >= B -> reserve r^2 consecutive OLT slots with one atomicAdd on the
+// level's count (compact concurrent insertion); else -> leaf list.
+// Returns the reserved base (or UINT_MAX) to the caller's lane/thread.
+__device__ __forceinline__ uint32_t decide(const LevelArgs &a, uint32_t off, int lo, int hi)
+{
+    if (lo == hi) {
+        const uint32_t e = atomicAdd(&a.hdr->n_fill[a.level], 1u);
+        a.fill[e] = make_uint2(off, (uint32_t)lo);
+        return UINT_MAX;
+    }
+    if (a.subdivide)
+        return atomicAdd(&a.hdr->n_subdiv[a.level], 1u);
+    const uint32_t e = atomicAdd(&a.hdr->n_leaf, 1u);
+    a.leaf[e] = off;
+    return UINT_MAX;
+}
+
+// --------------------------------------------------------------------------- SBR scheme
+// ASK-SBR level kernel: one block of TPB threads per region
+// (persistent, grid-stride over the level's OLT).  The block's warps split the region's
+// 4d-4 border pixels, write their dwells to the image (they are final values), and reduce
+// (min, max) with warp reductions + shared memory; uniform iff min == max.
+template <int TPB, bool STATS>
+__global__ void __launch_bounds__(TPB) k_sbr_level(LevelArgs a)
+{
+    __shared__ int s_lo[TPB / 32], s_hi[TPB / 32];
+    __shared__ unsigned long long s_sum[TPB / 32];
+    __shared__ uint32_t s_base;
+    const uint32_t count = level_count(a);
+    const int d = a.d, ring = 4 * d - 4, s = d / a.r, rr = a.r * a.r;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    for (uint32_t ri = blockIdx.x; ri < count; ri += gridDim.x) {
+        const uint32_t off = a.olt_in[ri];
+        const int x0 = unpack_x(off), y0 = unpack_y(off);
+        int lo = INT_MAX, hi = INT_MIN;
+        unsigned long long it = 0;
+        for (int b = threadIdx.x; b < ring; b += TPB) {
+            int x, y;
+            ring_pixel(b, d, x0, y0, x, y);
+            const int v = dwell<DWELL_K>(pix_re(a.map, x), pix_im(a.map, y), a.maxdwell);
+            a.out[(long long)y * a.pitch + x] = v;
+            lo = min(lo, v);
+            hi = max(hi, v);
+            if (STATS)
+                it += (unsigned long long)v;
+        }
+        lo = __reduce_min_sync(0xffffffffu, lo);
+        hi = __reduce_max_sync(0xffffffffu, hi);
+        if (l == 0) {
+            s_lo[w] = lo;
+            s_hi[w] = hi;
+        }
+        if (STATS)
+            it = block_sum_u64<TPB>(it, s_sum);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int i = 1; i < TPB / 32; ++i) {
+                lo = min(lo, s_lo[i]);
+                hi = max(hi, s_hi[i]);
+            }
+            s_base = decide(a, off, lo, hi);
+            if (STATS) {
+                atomicAdd(&a.hdr->border_px[a.level], (unsigned long long)ring);
+                atomicAdd(&a.hdr->border_iters[a.level], it);
+            }
+        }
+        __syncthreads();
+        const uint32_t base = s_base;
+        if (base != UINT_MAX)
+            for (int t = threadIdx.x; t < rr; t += TPB)
+                a.olt_out[(size_t)base * rr + t] = pack_xy(x0 + (t % a.r) * s, y0 + (t / a.r) * s);
+        __syncthreads();
+    }
+}
+
+// Leaf work L, SBR: one block per last-level non-uniform region computes its
+// (d-2)^2 interior pixels (the border is already in the image).
+template <int TPB, bool STATS>
+__global__ void __launch_bounds__(TPB) k_sbr_leaf(LevelArgs a)
+{
+    __shared__ unsigned long long s_sum[TPB / 32];
+    const uint32_t count = *((volatile uint32_t *)&a.hdr->n_leaf);
+    const int d = a.d, m = d - 2, I = m * m;
+    for (uint32_t li = blockIdx.x; li < count; li += gridDim.x) {
+        const uint32_t off = a.leaf[li];
+        const int x0 = unpack_x(off) + 1, y0 = unpack_y(off) + 1;
+        unsigned long long it = 0;
+        for (int p = threadIdx.x; p < I; p += TPB) {
+            const int x = x0 + p % m, y = y0 + p / m;
+            const int v = dwell<DWELL_K>(pix_re(a.map, x), pix_im(a.map, y), a.maxdwell);
+            a.out[(long long)y * a.pitch + x] = v;
+            if (STATS)
+                it += (unsigned long long)v;
+        }
+        if (STATS) {
+            it = block_sum_u64<TPB>(it, s_sum);
+            if (threadIdx.x == 0) {
+                atomicAdd(&a.hdr->leaf_px, (unsigned long long)I);
+                atomicAdd(&a.hdr->leaf_iters, it);
+            }
+        }
+    }
+}
+
+// --------------------------------------------------------------------------- fill
+// Terminal work T ("writes a constant value on each data-element"): every uniform
+// region of the level is filled with its border dwell.  Flat over all 16-byte vectors of
+// all filled regions (grid-stride), streaming 128-bit stores.
+template <bool VEC>
+__global__ void __launch_bounds__(256) k_fill(LevelArgs a)
+{
+    const unsigned long long count = *((volatile uint32_t *)&a.hdr->n_fill[a.level]);
+    const int d = a.d;
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    unsigned long long u = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (VEC) {
+        const unsigned long long total = count << a.log2_q4;
+        const unsigned long long qmask = (1ull << a.log2_q4) - 1ull;
+        const int rmask = (1 << a.log2_row4) - 1;
+        for (; u < total; u += stride) {
+            const uint2 e = a.fill[u >> a.log2_q4];
+            const int rem = (int)(u & qmask);
+            const int row = rem >> a.log2_row4, c4 = rem & rmask;
+            const int x = unpack_x(e.x) + 4 * c4, y = unpack_y(e.x) + row;
+            const int v = (int)e.y;
+            __stcs(reinterpret_cast<int4 *>(a.out + (long long)y * a.pitch + x), make_int4(v, v, v, v));
+        }
+    } else {
+        const unsigned long long per = (unsigned long long)d * d;
+        const unsigned long long total = count * per;
+        for (; u < total; u += stride) {
+            const uint2 e = a.fill[u / per];
+            const int rem = (int)(u % per);
+            const int x = unpack_x(e.x) + rem % d, y = unpack_y(e.x) + rem / d;
+            a.out[(long long)y * a.pitch + x] = (int)e.y;
+        }
+    }
+}
+
+// --------------------------------------------------------------------------- B200 scheme
+// New border pixels of level `level`, written to the image:
+//   level 0: the 4d-4 ring of every level-0 region;
+//   level l>0: for every region subdivided at level l-1 (side D = r d), the pixels of its
+//   children's rings that are not on its own ring: 2(r-1) full-height internal columns
+//   (x0 + k d - 1, x0 + k d; rows y0+1..y0+D-2) and 2(r-1) internal rows without the
+//   column pixels (r segments of d-2 pixels each).
+// One thread per pixel, flat over all new pixels of the level (grid-stride), so the
+// level's whole border work is spread over every SM regardless of region count.
+__host__ __device__ __forceinline__ uint32_t new_border_px_per_parent(int D, int r)
+{
+    const int d = D / r;
+    return (uint32_t)(2 * (r - 1) * (D - 2) + 2 * (r - 1) * r * (d - 2));
+}
+
+template <bool STATS>
+__global__ void __launch_bounds__(256) k_b200_border(LevelArgs a)
+{
+    __shared__ unsigned long long s_sum[8];
+    unsigned long long total, per;
+    const int d = a.d;
+    int D = d * a.r; // parent side (level > 0)
+    if (a.level == 0) {
+        per = (unsigned long long)(4 * d - 4);
+        total = per * (unsigned long long)a.ntiles;
+    } else {
+        per = new_border_px_per_parent(D, a.r);
+        total = per * (unsigned long long)(*((volatile uint32_t *)&a.hdr->n_subdiv[a.level - 1]));
+    }
+    const int rr = a.r * a.r;
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    unsigned long long it = 0, px = 0;
+    for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
+        const uint32_t p = (uint32_t)(t / per);
+        const int loc = (int)(t - (unsigned long long)p * per);
+        int x, y;
+        if (a.level == 0) {
+            const uint32_t off = a.olt_in[p];
+            ring_pixel(loc, d, unpack_x(off), unpack_y(off), x, y);
+        } else {
+            const uint32_t off = a.olt_in[(size_t)p * rr]; // first child = parent origin
+            const int x0 = unpack_x(off), y0 = unpack_y(off);
+            const int pv = 2 * (a.r - 1) * (D - 2);
+            if (loc < pv) {
+                const int line = loc / (D - 2), row = loc - line * (D - 2);
+                x = x0 + (line / 2 + 1) * d - 1 + (line & 1);
+                y = y0 + 1 + row;
+            } else {
+                const int h = loc - pv, seg = d - 2, len = a.r * seg;
+                const int line = h / len, c = h - line * len;
+                const int k = c / seg, o = c - k * seg;
+                y = y0 + (line / 2 + 1) * d - 1 + (line & 1);
+                x = x0 + k * d + 1 + o;
+            }
+        }
+        const int v = dwell<DWELL_K>(pix_re(a.map, x), pix_im(a.map, y), a.maxdwell);
+        a.out[(long long)y * a.pitch + x] = v;
+        if (STATS) {
+            it += (unsigned long long)v;
+            px += 1;
+        }
+    }
+    if (STATS) {
+        it = block_sum_u64<256>(it, s_sum);
+        if (threadIdx.x == 0 && it)
+            atomicAdd(&a.hdr->border_iters[a.level], it);
+        px = block_sum_u64<256>(px, s_sum);
+        if (threadIdx.x == 0 && px)
+            atomicAdd(&a.hdr->border_px[a.level], px);
+    }
+}
+
+// Classification, one warp per region: read the region's 4d-4 ring
+// dwells back from the image, reduce (min, max) with warp reductions, decide, and append
+// (children written by the warp's lanes).
+__global__ void __launch_bounds__(256) k_b200_classify(LevelArgs a)
+{
+    const uint32_t count = level_count(a);
+    const int d = a.d, ring = 4 * d - 4, s = d / a.r, rr = a.r * a.r;
+    const int lane = threadIdx.x & 31;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t ri = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; ri < count; ri += nw) {
+        const uint32_t off = a.olt_in[ri];
+        const int x0 = unpack_x(off), y0 = unpack_y(off);
+        int lo = INT_MAX, hi = INT_MIN;
+        for (int b = lane; b < ring; b += 32) {
+            int x, y;
+            ring_pixel(b, d, x0, y0, x, y);
+            const int v = __ldcg(a.out + (long long)y * a.pitch + x);
+            lo = min(lo, v);
+            hi = max(hi, v);
+        }
+        lo = __reduce_min_sync(0xffffffffu, lo);
+        hi = __reduce_max_sync(0xffffffffu, hi);
+        uint32_t base = 0;
+        if (lane == 0)
+            base = decide(a, off, lo, hi);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (base != UINT_MAX)
+            for (int t = lane; t < rr; t += 32)
+                a.olt_out[(size_t)base * rr + t] = pack_xy(x0 + (t % a.r) * s, y0 + (t / a.r) * s);
+    }
+}
+
+// Leaf interiors, flat: one thread per interior pixel of all leaves (grid-stride).
+template <bool STATS>
+__global__ void __launch_bounds__(256) k_b200_leaf(LevelArgs a)
+{
+    __shared__ unsigned long long s_sum[8];
+    const int d = a.d, m = d - 2;
+    const unsigned long long I = (unsigned long long)m * m;
+    const unsigned long long total = I * (unsigned long long)(*((volatile uint32_t *)&a.hdr->n_leaf));
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    unsigned long long it = 0, px = 0;
+    for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
+        const uint32_t li = (uint32_t)(t / I);
+        const int loc = (int)(t - (unsigned long long)li * I);
+        const uint32_t off = a.leaf[li];
+        const int x = unpack_x(off) + 1 + loc % m, y = unpack_y(off) + 1 + loc / m;
+        const int v = dwell<DWELL_K>(pix_re(a.map, x), pix_im(a.map, y), a.maxdwell);
+        a.out[(long long)y * a.pitch + x] = v;
+        if (STATS) {
+            it += (unsigned long long)v;
+            px += 1;
+        }
+    }
+    if (STATS) {
+        it = block_sum_u64<256>(it, s_sum);
+        if (threadIdx.x == 0 && it)
+            atomicAdd(&a.hdr->leaf_iters, it);
+        px = block_sum_u64<256>(px, s_sum);
+        if (threadIdx.x == 0 && px)
+            atomicAdd(&a.hdr->leaf_px, px);
+    }
+}
+
+} // namespace mandel

@@ -1,0 +1,573 @@
+// mandel.cu -- C ABI (include/mandel.h): validation, workspace layout, the ASK level loop
+// captured once into a CUDA graph per call signature, and launch of the sm_100a kernels.
+//
+// ASK: one flat kernel per subdivision level, executed serially; the level's
+// region count lives in device memory (the OLT "count") and every kernel reads
+// it there, so the whole loop -- all levels, fills and leaves -- is one graph launch with
+// no host round trip (the paper's host loop copies `count` back after every level).
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/mandel.h"
+#include "ask_kernels.cuh"
+
+using namespace mandel;
+
+namespace {
+
+thread_local char g_cuda_err[256] = "";
+
+int cuda_fail(cudaError_t e, const char *what)
+{
+    snprintf(g_cuda_err, sizeof g_cuda_err, "%s: %s", what, cudaGetErrorString(e));
+    return MANDEL_ECUDA;
+}
+
+#define CK(call)                                                                               \
+    do {                                                                                       \
+        cudaError_t e_ = (call);                                                               \
+        if (e_ != cudaSuccess)                                                                 \
+            return cuda_fail(e_, #call);                                                       \
+    } while (0)
+
+bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+int ilog2(int64_t v)
+{
+    int k = 0;
+    while ((int64_t(1) << k) < v)
+        ++k;
+    return k;
+}
+
+bool valid_region(const mandel_region &g)
+{
+    auto fin = [](double v) { return v == v && v < 1e300 && v > -1e300; };
+    return fin(g.re_min) && fin(g.re_max) && fin(g.im_min) && fin(g.im_max) && g.re_min < g.re_max &&
+           g.im_min < g.im_max;
+}
+
+bool valid_grb(int64_t n, int32_t g, int32_t r, int32_t B)
+{
+    return is_pow2(n) && n <= 65536 && is_pow2(g) && is_pow2(r) && is_pow2(B) && r >= 2 && B >= 2 &&
+           (int64_t)g * B <= n;
+}
+
+int levels_of(int64_t n, int32_t g, int32_t r, int32_t B)
+{
+    int64_t d = n / g;
+    int L = 1;
+    while (d / r >= B) {
+        d /= r;
+        ++L;
+    }
+    return L;
+}
+
+// Workspace layout.  cap_l = g^2 r^(2l) (every region may subdivide).
+struct Layout {
+    int L;
+    size_t hdr, tiles, olt[2], fill, leaf, total;
+    size_t fill_off[MAXL]; // element offset of each level's fill segment
+    size_t cap[MAXL];
+};
+
+size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+bool make_layout(int64_t n, int32_t g, int32_t r, int32_t B, Layout &lay)
+{
+    if (!valid_grb(n, g, r, B))
+        return false;
+    lay.L = levels_of(n, g, r, B);
+    if (lay.L > MAXL)
+        return false;
+    size_t c = (size_t)g * g, fsum = 0;
+    for (int l = 0; l < lay.L; ++l) {
+        lay.cap[l] = c;
+        lay.fill_off[l] = fsum;
+        fsum += c;
+        c *= (size_t)r * r;
+    }
+    const size_t capmax = lay.cap[lay.L - 1];
+    size_t o = 0;
+    lay.hdr = o;
+    o += 4096;
+    lay.tiles = o;
+    o = align256(o + (size_t)g * g * 4);
+    lay.olt[0] = o;
+    o = align256(o + capmax * 4);
+    lay.olt[1] = o;
+    o = align256(o + capmax * 4);
+    lay.fill = o;
+    o = align256(o + fsum * 8);
+    lay.leaf = o;
+    o = align256(o + capmax * 4);
+    lay.total = o;
+    return true;
+}
+
+PixMap make_map(const mandel_region &reg, int64_t n)
+{
+    PixMap m;
+    m.x0 = (float)reg.re_min;
+    m.y0 = (float)reg.im_min;
+    m.dx = (float)((reg.re_max - reg.re_min) / (double)n);
+    m.dy = (float)((reg.im_max - reg.im_min) / (double)n);
+    return m;
+}
+
+struct DevInfo {
+    int sms = 0;
+    cudaStream_t cap = nullptr;
+};
+
+struct Key {
+    int dev;
+    mandel_region reg;
+    int64_t n, pitch;
+    int32_t maxdwell, g, r, B, scheme;
+    uint32_t flags;
+    int32_t *out;
+    void *ws;
+    size_t ws_bytes;
+    std::vector<int32_t> tiles;
+    bool operator==(const Key &o) const
+    {
+        return dev == o.dev && memcmp(&reg, &o.reg, sizeof reg) == 0 && n == o.n && pitch == o.pitch &&
+               maxdwell == o.maxdwell && g == o.g && r == o.r && B == o.B && scheme == o.scheme &&
+               flags == o.flags && out == o.out && ws == o.ws && ws_bytes == o.ws_bytes && tiles == o.tiles;
+    }
+};
+
+struct Entry {
+    Key key;
+    cudaGraphExec_t exec = nullptr;
+    int32_t *h_tiles = nullptr; // pinned, mapped (read by k_init through UVA)
+    unsigned long long last_use = 0;
+};
+
+std::mutex g_mu;
+std::vector<Entry> g_cache;
+std::vector<DevInfo> g_dev;
+unsigned long long g_clock = 0;
+constexpr size_t kMaxGraphs = 64;
+
+int dev_info(int dev, DevInfo *&out)
+{
+    if ((int)g_dev.size() <= dev)
+        g_dev.resize(dev + 1);
+    DevInfo &di = g_dev[dev];
+    if (!di.cap) {
+        CK(cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev));
+        CK(cudaStreamCreateWithFlags(&di.cap, cudaStreamNonBlocking));
+    }
+    out = &di;
+    return MANDEL_OK;
+}
+
+template <typename K>
+int resident_grid(K kernel, int tpb, int sms, size_t cap_blocks)
+{
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, tpb, 0) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    size_t g = (size_t)per_sm * sms;
+    if (cap_blocks < g)
+        g = cap_blocks;
+    return (int)(g < 1 ? 1 : g);
+}
+
+// Enqueue the whole ASK call on `s` (called under stream capture).
+int enqueue_ask(const Key &k, const Layout &lay, const int32_t *d_tiles_visible, int ntiles, int sms,
+                cudaStream_t s)
+{
+    char *ws = (char *)k.ws;
+    LevelArgs a;
+    memset(&a, 0, sizeof a);
+    a.map = make_map(k.reg, k.n);
+    a.maxdwell = k.maxdwell;
+    a.pitch = k.pitch;
+    a.out = k.out;
+    a.hdr = (WsHeader *)(ws + lay.hdr);
+    a.leaf = (uint32_t *)(ws + lay.leaf);
+    a.tiles = d_tiles_visible;
+    a.r = k.r;
+    a.B = k.B;
+    a.g = k.g;
+    a.ntiles = ntiles;
+    a.levels = lay.L;
+    a.scheme = k.scheme;
+    const bool stats = (k.flags & MANDEL_FLAG_STATS) != 0;
+    const bool vec_ok = ((uintptr_t)k.out % 16 == 0) && (k.pitch % 4 == 0);
+    const int d0 = (int)(k.n / k.g);
+
+    // init: level-0 OLT + zeroed counters
+    a.level = 0;
+    a.d = d0;
+    a.olt_in = (const uint32_t *)(ws + lay.olt[0]);
+    {
+        int nthr = ntiles > 1024 ? ntiles : 1024;
+        k_init<<<(nthr + 255) / 256, 256, 0, s>>>(a);
+        CK(cudaGetLastError());
+    }
+    int d = d0;
+    for (int l = 0; l < lay.L; ++l) {
+        a.level = l;
+        a.d = d;
+        a.subdivide = (d / k.r >= k.B) ? 1 : 0;
+        a.olt_in = (const uint32_t *)(ws + lay.olt[l & 1]);
+        a.olt_out = (uint32_t *)(ws + lay.olt[(l + 1) & 1]);
+        a.fill = (uint2 *)(ws + lay.fill) + lay.fill_off[l];
+        // max regions at this level for this call
+        size_t cap = (size_t)ntiles;
+        for (int i = 0; i < l; ++i)
+            cap *= (size_t)k.r * k.r;
+        if (k.scheme == MANDEL_SCHEME_SBR) {
+            const int ring = 4 * d - 4;
+#define SBR_LAUNCH(TPB)                                                                        \
+    do {                                                                                       \
+        if (stats) {                                                                           \
+            int gsz = resident_grid(k_sbr_level<TPB, true>, TPB, sms, cap);                    \
+            k_sbr_level<TPB, true><<<gsz, TPB, 0, s>>>(a);                                      \
+        } else {                                                                               \
+            int gsz = resident_grid(k_sbr_level<TPB, false>, TPB, sms, cap);                   \
+            k_sbr_level<TPB, false><<<gsz, TPB, 0, s>>>(a);                                     \
+        }                                                                                      \
+    } while (0)
+            if (ring >= 256)
+                SBR_LAUNCH(256);
+            else if (ring >= 128)
+                SBR_LAUNCH(128);
+            else if (ring >= 64)
+                SBR_LAUNCH(64);
+            else
+                SBR_LAUNCH(32);
+#undef SBR_LAUNCH
+            CK(cudaGetLastError());
+        } else {
+            size_t work = (l == 0) ? cap * (size_t)(4 * d - 4)
+                                   : (cap / ((size_t)k.r * k.r)) * new_border_px_per_parent(d * k.r, k.r);
+            size_t blocks = (work + 255) / 256;
+            if (stats) {
+                int gsz = resident_grid(k_b200_border<true>, 256, sms, blocks);
+                k_b200_border<true><<<gsz, 256, 0, s>>>(a);
+            } else {
+                int gsz = resident_grid(k_b200_border<false>, 256, sms, blocks);
+                k_b200_border<false><<<gsz, 256, 0, s>>>(a);
+            }
+            CK(cudaGetLastError());
+            int gsz = resident_grid(k_b200_classify, 256, sms, (cap + 7) / 8);
+            k_b200_classify<<<gsz, 256, 0, s>>>(a);
+            CK(cudaGetLastError());
+        }
+        // fill (terminal work) of this level's uniform regions
+        {
+            const bool vec = vec_ok && d >= 4;
+            a.log2_q4 = vec ? ilog2((int64_t)d * d / 4) : 0;
+            a.log2_row4 = vec ? ilog2(d / 4) : 0;
+            size_t work = cap * (size_t)d * d / (vec ? 4 : 1);
+            size_t blocks = (work + 255) / 256;
+            if (vec) {
+                int gsz = resident_grid(k_fill<true>, 256, sms, blocks);
+                k_fill<true><<<gsz, 256, 0, s>>>(a);
+            } else {
+                int gsz = resident_grid(k_fill<false>, 256, sms, blocks);
+                k_fill<false><<<gsz, 256, 0, s>>>(a);
+            }
+            CK(cudaGetLastError());
+        }
+        if (l + 1 < lay.L)
+            d /= k.r;
+    }
+    // leaves of the last level
+    {
+        a.level = lay.L - 1;
+        a.d = d;
+        size_t cap = (size_t)ntiles;
+        for (int i = 0; i < lay.L - 1; ++i)
+            cap *= (size_t)k.r * k.r;
+        if (k.scheme == MANDEL_SCHEME_SBR) {
+            const int I = (d - 2) * (d - 2);
+#define LEAF_LAUNCH(TPB)                                                                       \
+    do {                                                                                       \
+        if (stats) {                                                                           \
+            int gsz = resident_grid(k_sbr_leaf<TPB, true>, TPB, sms, cap);                     \
+            k_sbr_leaf<TPB, true><<<gsz, TPB, 0, s>>>(a);                                       \
+        } else {                                                                               \
+            int gsz = resident_grid(k_sbr_leaf<TPB, false>, TPB, sms, cap);                    \
+            k_sbr_leaf<TPB, false><<<gsz, TPB, 0, s>>>(a);                                      \
+        }                                                                                      \
+    } while (0)
+            if (I >= 256)
+                LEAF_LAUNCH(256);
+            else if (I >= 128)
+                LEAF_LAUNCH(128);
+            else if (I >= 64)
+                LEAF_LAUNCH(64);
+            else
+                LEAF_LAUNCH(32);
+#undef LEAF_LAUNCH
+        } else {
+            size_t blocks = (cap * (size_t)(d - 2) * (d - 2) + 255) / 256;
+            if (stats) {
+                int gsz = resident_grid(k_b200_leaf<true>, 256, sms, blocks);
+                k_b200_leaf<true><<<gsz, 256, 0, s>>>(a);
+            } else {
+                int gsz = resident_grid(k_b200_leaf<false>, 256, sms, blocks);
+                k_b200_leaf<false><<<gsz, 256, 0, s>>>(a);
+            }
+        }
+        CK(cudaGetLastError());
+    }
+    return MANDEL_OK;
+}
+
+void free_entry(Entry &e)
+{
+    if (e.exec)
+        cudaGraphExecDestroy(e.exec);
+    if (e.h_tiles)
+        cudaFreeHost(e.h_tiles);
+    e.exec = nullptr;
+    e.h_tiles = nullptr;
+}
+
+int validate_common(const mandel_region &reg, int64_t n, int32_t maxdwell, int32_t *d_out, int64_t pitch)
+{
+    if (!valid_region(reg) || !is_pow2(n) || n > 65536 || maxdwell < 1 || !d_out || pitch < n)
+        return MANDEL_EINVAL;
+    return MANDEL_OK;
+}
+
+} // namespace
+
+extern "C" {
+
+size_t mandel_ask_workspace_bytes(int64_t n, int32_t g, int32_t r, int32_t B)
+{
+    Layout lay;
+    if (!make_layout(n, g, r, B, lay))
+        return 0;
+    return lay.total;
+}
+
+int32_t mandel_ask_levels(int64_t n, int32_t g, int32_t r, int32_t B)
+{
+    if (!valid_grb(n, g, r, B))
+        return 0;
+    return levels_of(n, g, r, B);
+}
+
+int32_t mandel_ask_kernel_count(int64_t n, int32_t g, int32_t r, int32_t B, int32_t scheme)
+{
+    if (!valid_grb(n, g, r, B))
+        return 0;
+    const int L = levels_of(n, g, r, B);
+    return 1 + L * (scheme == MANDEL_SCHEME_SBR ? 2 : 3) + 1;
+}
+
+int mandel_exhaustive(mandel_region reg, int64_t n, int32_t maxdwell, int32_t *d_out, int64_t out_pitch,
+                      void *stream)
+{
+    int rc = validate_common(reg, n, maxdwell, d_out, out_pitch);
+    if (rc)
+        return rc;
+    ExArgs a;
+    a.map = make_map(reg, n);
+    a.n = (int)n;
+    a.maxdwell = maxdwell;
+    a.pitch = out_pitch;
+    a.out = d_out;
+    constexpr int BX = 16, BY = 16;
+    dim3 grid((unsigned)((n + BX - 1) / BX), (unsigned)((n + BY - 1) / BY));
+    k_exhaustive<BX, BY><<<grid, dim3(BX, BY), 0, (cudaStream_t)stream>>>(a);
+    CK(cudaGetLastError());
+    return MANDEL_OK;
+}
+
+int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, int32_t r, int32_t B,
+                     const int32_t *h_tile_ids, int32_t n_tiles, int32_t scheme, uint32_t flags, int32_t *d_out,
+                     int64_t out_pitch, void *d_ws, size_t ws_bytes, void *stream)
+{
+    int rc = validate_common(reg, n, maxdwell, d_out, out_pitch);
+    if (rc)
+        return rc;
+    if (!valid_grb(n, g, r, B) || !d_ws || (scheme != MANDEL_SCHEME_SBR && scheme != MANDEL_SCHEME_B200) ||
+        (flags & ~MANDEL_FLAG_STATS) != 0)
+        return MANDEL_EINVAL;
+    Layout lay;
+    if (!make_layout(n, g, r, B, lay))
+        return MANDEL_EINVAL;
+    if (ws_bytes < lay.total)
+        return MANDEL_EWORKSPACE;
+    if ((uintptr_t)d_ws % 256 != 0)
+        return MANDEL_EINVAL;
+    const int64_t G = (int64_t)g * g;
+    std::vector<int32_t> tiles;
+    if (h_tile_ids) {
+        if (n_tiles < 0 || n_tiles > G)
+            return MANDEL_EINVAL;
+        std::vector<char> seen((size_t)G, 0);
+        tiles.assign(h_tile_ids, h_tile_ids + n_tiles);
+        for (int32_t t : tiles) {
+            if (t < 0 || t >= G || seen[(size_t)t])
+                return MANDEL_EINVAL;
+            seen[(size_t)t] = 1;
+        }
+    } else if (n_tiles != 0) {
+        return MANDEL_EINVAL;
+    }
+    const int ntiles = h_tile_ids ? n_tiles : (int)G;
+
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_mu);
+    DevInfo *di = nullptr;
+    if ((rc = dev_info(dev, di)))
+        return rc;
+
+    Key key{dev, reg, n, out_pitch, maxdwell, g, r, B, scheme, flags, d_out, d_ws, ws_bytes, tiles};
+    Entry *hit = nullptr;
+    for (auto &e : g_cache)
+        if (e.key == key) {
+            hit = &e;
+            break;
+        }
+    if (!hit) {
+        if (g_cache.size() >= kMaxGraphs) { // evict least recently used
+            size_t lru = 0;
+            for (size_t i = 1; i < g_cache.size(); ++i)
+                if (g_cache[i].last_use < g_cache[lru].last_use)
+                    lru = i;
+            free_entry(g_cache[lru]);
+            g_cache.erase(g_cache.begin() + (long)lru);
+        }
+        Entry e;
+        e.key = key;
+        if (h_tile_ids && ntiles > 0) {
+            CK(cudaHostAlloc((void **)&e.h_tiles, (size_t)ntiles * 4, cudaHostAllocMapped | cudaHostAllocPortable));
+            memcpy(e.h_tiles, tiles.data(), (size_t)ntiles * 4);
+        }
+        int32_t *d_tiles = nullptr;
+        if (e.h_tiles) {
+            cudaError_t ce = cudaHostGetDevicePointer((void **)&d_tiles, e.h_tiles, 0);
+            if (ce != cudaSuccess) {
+                free_entry(e);
+                return cuda_fail(ce, "cudaHostGetDevicePointer");
+            }
+        }
+        cudaGraph_t graph = nullptr;
+        cudaError_t ce = cudaStreamBeginCapture(di->cap, cudaStreamCaptureModeThreadLocal);
+        if (ce != cudaSuccess) {
+            free_entry(e);
+            return cuda_fail(ce, "cudaStreamBeginCapture");
+        }
+        int erc = enqueue_ask(key, lay, d_tiles, ntiles, di->sms, di->cap);
+        ce = cudaStreamEndCapture(di->cap, &graph);
+        if (erc || ce != cudaSuccess) {
+            if (graph)
+                cudaGraphDestroy(graph);
+            free_entry(e);
+            return erc ? erc : cuda_fail(ce, "cudaStreamEndCapture");
+        }
+        ce = cudaGraphInstantiate(&e.exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ce != cudaSuccess) {
+            free_entry(e);
+            return cuda_fail(ce, "cudaGraphInstantiate");
+        }
+        g_cache.push_back(e);
+        hit = &g_cache.back();
+    }
+    hit->last_use = ++g_clock;
+    CK(cudaGraphLaunch(hit->exec, (cudaStream_t)stream));
+    return MANDEL_OK;
+}
+
+int mandel_ask(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, int32_t r, int32_t B, int32_t *d_out,
+               int64_t out_pitch, void *d_ws, size_t ws_bytes, void *stream)
+{
+    return mandel_ask_tiles(reg, n, maxdwell, g, r, B, nullptr, 0, MANDEL_SCHEME_B200, 0u, d_out, out_pitch, d_ws,
+                            ws_bytes, stream);
+}
+
+int mandel_ask_to_host(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, int32_t r, int32_t B,
+                       const int32_t *h_tile_ids, int32_t n_tiles, int32_t scheme, int32_t *d_out, int64_t out_pitch,
+                       void *d_ws, size_t ws_bytes, int32_t *h_out, void *stream)
+{
+    if (!h_out)
+        return MANDEL_EINVAL;
+    int rc = mandel_ask_tiles(reg, n, maxdwell, g, r, B, h_tile_ids, n_tiles, scheme, 0u, d_out, out_pitch, d_ws,
+                              ws_bytes, stream);
+    if (rc)
+        return rc;
+    CK(cudaMemcpy2DAsync(h_out, (size_t)n * 4, d_out, (size_t)out_pitch * 4, (size_t)n * 4, (size_t)n,
+                         cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    return MANDEL_OK;
+}
+
+int mandel_ask_last_stats(const void *d_ws, mandel_level_stats *h_out, int32_t max_levels, void *stream)
+{
+    if (!d_ws || (!h_out && max_levels > 0) || max_levels < 0)
+        return -MANDEL_EINVAL;
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    WsHeader h;
+    CK(cudaMemcpy(&h, d_ws, sizeof h, cudaMemcpyDeviceToHost));
+    if (h.magic != WS_MAGIC || h.levels < 1 || h.levels > (uint32_t)MAXL)
+        return -MANDEL_EINVAL;
+    const int L = (int)h.levels;
+    int64_t d = (int64_t)h.n / h.g;
+    int64_t regions = h.ntiles;
+    for (int l = 0; l < L && l < max_levels; ++l) {
+        mandel_level_stats &s = h_out[l];
+        s.level = l;
+        s.side = (int32_t)d;
+        s.regions_in = regions;
+        s.filled = h.n_fill[l];
+        s.subdivided = h.n_subdiv[l];
+        s.leaves = (l == L - 1) ? h.n_leaf : 0;
+        s.border_px = (int64_t)h.border_px[l];
+        s.border_iters = (int64_t)h.border_iters[l];
+        s.leaf_px = (l == L - 1) ? (int64_t)h.leaf_px : 0;
+        s.leaf_iters = (l == L - 1) ? (int64_t)h.leaf_iters : 0;
+        regions = (int64_t)h.n_subdiv[l] * h.r * h.r;
+        d /= h.r;
+    }
+    return L;
+}
+
+const char *mandel_strerror(int code)
+{
+    switch (code) {
+    case MANDEL_OK:
+        return "ok";
+    case MANDEL_EINVAL:
+        return "invalid argument";
+    case MANDEL_EWORKSPACE:
+        return "workspace too small";
+    case MANDEL_ECUDA:
+        return "CUDA error";
+    default:
+        return "unknown error";
+    }
+}
+
+const char *mandel_last_cuda_error(void) { return g_cuda_err; }
+
+void mandel_shutdown(void)
+{
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (auto &e : g_cache)
+        free_entry(e);
+    g_cache.clear();
+    for (auto &d : g_dev)
+        if (d.cap)
+            cudaStreamDestroy(d.cap);
+    g_dev.clear();
+}
+
+} // extern "C"

@@ -1,0 +1,110 @@
+"""The C-ABI library loads and exports every symbol include/mandel.h declares; the host-only
+entry points (sizes, validation) behave as documented.  No kernel is launched here."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2206_02255_b200 as mb
+from paper_2206_02255_b200 import _lib, build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    build.build()
+    return _lib.load()
+
+
+def _declared_functions():
+    src = open(os.path.join(ROOT, "include", "mandel.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(mandel_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(lib):
+    declared = _declared_functions()
+    assert len(declared) >= 10
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert sorted(_lib.EXPORTED) == declared
+
+
+def test_sass_is_sm100a():
+    so = _lib.LIB_PATH
+    out = os.popen(f"/usr/local/cuda/bin/cuobjdump --list-elf {so} 2>&1").read()
+    assert "sm_100a" in out
+
+
+def test_no_fma_in_dwell_kernels():
+    """-fmad=false + __f*_rn: the dwell loops must not contain FFMA (R4)."""
+    sass = os.popen(f"/usr/local/cuda/bin/cuobjdump -sass {_lib.LIB_PATH} 2>&1").read()
+    funcs = re.split(r"\n\s*Function : ", sass)
+    checked = 0
+    for f in funcs[1:]:
+        name = f.split("\n", 1)[0]
+        if any(k in name for k in ("k_exhaustive", "k_sbr_level", "k_sbr_leaf", "k_b200_border", "k_b200_leaf")):
+            assert "FFMA" not in f, name
+            assert "FMUL" in f and "FADD" in f, name
+            checked += 1
+    assert checked >= 5
+
+
+def test_levels_and_workspace(lib):
+    assert mb.levels(1024, 4, 2, 32) == 4      # C1: 256,128,64,32
+    assert mb.levels(32768, 16, 2, 32) == 7    # C3: 2048 .. 32
+    assert mb.levels(65536, 16, 2, 32) == 8    # C4
+    assert mb.levels(32768, 16, 4, 32) == 4    # C5: 2048,512,128,32
+    assert mb.levels(8192, 2, 4, 32) == 4      # non-exact tiling: 4096,1024,256,64
+    assert mb.levels(64, 8, 2, 8) == 1
+    # worst case: 2 OLTs + leaf list of (n/B_last)^2 u32 + 4/3 of it as 8-byte fill entries
+    ws = mb.workspace_bytes(65536, 16, 2, 32)
+    M = (65536 // 32) ** 2
+    assert 3 * 4 * M + 8 * M < ws < 3 * 4 * M + 8 * M * 4 // 3 + 2 * 1024 * 1024
+    assert mb.kernel_count(32768, 16, 2, 32, "b200") == 1 + 7 * 3 + 1
+    assert mb.kernel_count(32768, 16, 2, 32, "sbr") == 1 + 7 * 2 + 1
+
+
+@pytest.mark.parametrize("n,g,r,B", [(1000, 4, 2, 32), (1024, 3, 2, 32), (1024, 4, 1, 32),
+                                     (1024, 4, 2, 1), (1024, 64, 2, 32), (131072, 16, 2, 32),
+                                     (1024, 4, 3, 32), (0, 1, 2, 2)])
+def test_invalid_parameters_rejected(lib, n, g, r, B):
+    assert lib.mandel_ask_workspace_bytes(n, g, r, B) == 0
+    assert lib.mandel_ask_levels(n, g, r, B) == 0
+
+
+def test_validation_before_any_launch(lib):
+    reg = _lib.region((-1.5, 0.5, -1.0, 1.0))
+    fake = ctypes.c_void_p(256)
+    # bad region / n / maxdwell / pointer / pitch -> EINVAL synchronously (no CUDA touched)
+    assert lib.mandel_exhaustive(_lib.region((0.5, -1.5, -1, 1)), 64, 10, fake, 64, None) == 1
+    assert lib.mandel_exhaustive(reg, 63, 10, fake, 64, None) == 1
+    assert lib.mandel_exhaustive(reg, 64, 0, fake, 64, None) == 1
+    assert lib.mandel_exhaustive(reg, 64, 10, None, 64, None) == 1
+    assert lib.mandel_exhaustive(reg, 64, 10, fake, 32, None) == 1
+    assert lib.mandel_exhaustive(_lib.region((float("nan"), 1, 0, 1)), 64, 10, fake, 64, None) == 1
+    ws_need = lib.mandel_ask_workspace_bytes(64, 4, 2, 4)
+    # workspace too small
+    assert lib.mandel_ask(reg, 64, 10, 4, 2, 4, fake, 64, fake, ws_need - 1, None) == 2
+    # bad scheme / flags / duplicate or out-of-range tiles
+    args = (reg, 64, 10, 4, 2, 4)
+    t = (ctypes.c_int32 * 2)(3, 3)
+    assert lib.mandel_ask_tiles(*args, ctypes.cast(t, ctypes.c_void_p), 2, 1, 0, fake, 64, fake, ws_need, None) == 1
+    t = (ctypes.c_int32 * 1)(16)
+    assert lib.mandel_ask_tiles(*args, ctypes.cast(t, ctypes.c_void_p), 1, 1, 0, fake, 64, fake, ws_need, None) == 1
+    assert lib.mandel_ask_tiles(*args, None, 0, 7, 0, fake, 64, fake, ws_need, None) == 1
+    assert lib.mandel_ask_tiles(*args, None, 0, 1, 8, fake, 64, fake, ws_need, None) == 1
+    assert lib.mandel_strerror(2) == b"workspace too small"
+
+
+def test_product_has_no_oracle_dependency():
+    """The product package never imports or links the oracle."""
+    pkg = os.path.join(ROOT, "paper_2206_02255_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt, f
+                assert "mandel_oracle" not in txt and "liboracle" not in txt, f

@@ -1,0 +1,205 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element,
+bit-exact (integer dwells).  Sizes span several tiles/levels and ragged cases; the full
+BASELINE sizes are checked on sampled tiles/pixels the oracle computes one by one, in the
+launch configuration bench.py times."""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+SCHEMES = ("b200", "sbr")
+
+
+@pytest.fixture(scope="module")
+def mb():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2206_02255_b200 import build
+    build.build()
+    import paper_2206_02255_b200 as m
+    return m
+
+
+def _trim(stats):
+    out = [s for s in stats if s["regions_in"] > 0]
+    return out
+
+
+def _cmp_stats(gpu, orc, scheme):
+    gpu = _trim(gpu)
+    assert len(gpu) == len(orc)
+    for a, b in zip(gpu, orc):
+        for k in ("regions_in", "filled", "subdivided", "leaves", "leaf_px", "leaf_iters"):
+            assert a[k] == b[k], (k, a, b)
+        if scheme == "sbr":  # the paper's scheme recomputes every region's full border
+            assert a["border_px"] == b["border_px"] and a["border_iters"] == b["border_iters"]
+        else:                # the B200 scheme computes each border pixel once
+            assert a["border_px"] <= b["border_px"] and a["border_iters"] <= b["border_iters"]
+
+
+# ----------------------------------------------------------------------------- exhaustive
+@pytest.mark.parametrize("w", [W.C1] + list(W.random_small_workloads(12, seed=W.SEED + 11, max_n=512)),
+                         ids=lambda w: w.name)
+def test_exhaustive_parity(mb, w):
+    out = mb.exhaustive(w.region, w.n, w.maxdwell)
+    E = oracle.exhaustive(w.region, w.n, w.maxdwell)
+    assert np.array_equal(out.cpu().numpy(), E)
+
+
+def test_exhaustive_pitched(mb):
+    n = 128
+    buf = torch.full((n, n + 37), -7, dtype=torch.int32, device="cuda")  # row pitch n + 37
+    mb.exhaustive(W.SEAHORSE_REGION, n, 900, out=buf)
+    E = oracle.exhaustive(W.SEAHORSE_REGION, n, 900)
+    got = buf.cpu().numpy()
+    assert np.array_equal(got[:, :n], E)
+    assert np.all(got[:, n:] == -7)
+
+
+# ----------------------------------------------------------------------------- ASK
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_ask_c1(mb, scheme):
+    w = W.C1
+    ws = mb.workspace(w.n, w.g, w.r, w.B)
+    out = mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, ws=ws, scheme=scheme, stats=True)
+    A, st = oracle.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B)
+    assert np.array_equal(out.cpu().numpy(), A)
+    _cmp_stats(mb.ask_stats(ws), st, scheme)
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+@pytest.mark.parametrize("w", list(W.random_small_workloads(30, seed=W.SEED + 12, max_n=512)),
+                         ids=lambda w: w.name)
+def test_ask_random_small(mb, w, scheme):
+    ws = mb.workspace(w.n, w.g, w.r, w.B)
+    out = mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, ws=ws, scheme=scheme, stats=True)
+    A, st = oracle.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B)
+    assert np.array_equal(out.cpu().numpy(), A)
+    _cmp_stats(mb.ask_stats(ws), st, scheme)
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+@pytest.mark.parametrize("n,g,r,B,md,region", [
+    (256, 2, 2, 2, 300, W.DEFAULT_REGION),      # smallest leaves (side 2: empty interior)
+    (512, 4, 8, 2, 500, W.SEAHORSE_REGION),     # r = 8, leaf side 2..15
+    (1024, 2, 4, 32, 700, W.DEFAULT_REGION),    # non-exact tiling: 512,128,32
+    (2048, 2, 8, 16, 256, W.DEFAULT_REGION),    # non-exact: 1024,128,16
+    (256, 128, 2, 2, 100, W.DEFAULT_REGION),    # g*B == n: single level, 16384 tiles
+    (512, 1, 2, 4, 1000, W.SEAHORSE_REGION),    # g = 1: one level-0 region
+    (256, 4, 2, 8, 1, W.DEFAULT_REGION),        # maxdwell 1: everything uniform
+    (256, 4, 2, 8, 64, W.INTERIOR_REGION),      # closed form: all maxdwell
+    (256, 4, 2, 8, 64, W.ESCAPE_REGION),        # closed form: all 1
+    (2048, 8, 2, 16, 3000, (-0.75, -0.5, 0.0, 0.25)),  # maxdwell not a multiple of the chunk
+])
+def test_ask_edge_cases(mb, scheme, n, g, r, B, md, region):
+    ws = mb.workspace(n, g, r, B)
+    out = mb.ask(region, n, md, g, r, B, ws=ws, scheme=scheme, stats=True)
+    A, st = oracle.ask(region, n, md, g, r, B)
+    assert np.array_equal(out.cpu().numpy(), A)
+    _cmp_stats(mb.ask_stats(ws), st, scheme)
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_ask_tiles_subset_and_pitch(mb, scheme):
+    n, g, r, B, md = 512, 8, 2, 8, 800
+    rng = np.random.default_rng(W.SEED)
+    tiles = rng.permutation(g * g)[:23].tolist()
+    buf = torch.full((n, n + 4), -5, dtype=torch.int32, device="cuda")  # pitch n+4 (vector path)
+    ws = mb.workspace(n, g, r, B)
+    mb.ask(W.SEAHORSE_REGION, n, md, g, r, B, out=buf, ws=ws, tiles=tiles, scheme=scheme, stats=True)
+    A, st = oracle.ask(W.SEAHORSE_REGION, n, md, g, r, B, tiles=tiles)
+    got = buf.cpu().numpy()
+    mine = A != -1                                   # pixels of the listed tiles
+    assert mine.sum() == len(tiles) * (n // g) ** 2
+    assert np.array_equal(got[:, :n][mine], A[mine])
+    assert np.all(got[:, :n][~mine] == -5) and np.all(got[:, n:] == -5)
+    _cmp_stats(mb.ask_stats(ws), st, scheme)
+
+
+def test_ask_unaligned_pitch_scalar_fill(mb):
+    n, g, r, B, md = 256, 4, 2, 8, 500
+    buf = torch.full((n, n + 3), -1, dtype=torch.int32, device="cuda")
+    mb.ask(W.DEFAULT_REGION, n, md, g, r, B, out=buf)
+    A, _ = oracle.ask(W.DEFAULT_REGION, n, md, g, r, B)
+    assert np.array_equal(buf.cpu().numpy()[:, :n], A)
+
+
+def test_ask_equals_lookup_of_gpu_exhaustive(mb):
+    """mandel_ask == ask_by_lookup(mandel_exhaustive), on the seahorse window."""
+    n, g, r, B, md = 2048, 16, 4, 8, 2048
+    E = mb.exhaustive(W.SEAHORSE_REGION, n, md).cpu().numpy()
+    A = mb.ask(W.SEAHORSE_REGION, n, md, g, r, B).cpu().numpy()
+    L, _ = oracle.ask_by_lookup(E, g, r, B)
+    assert np.array_equal(A, L)
+
+
+def test_repeat_calls_reuse_graph_and_are_deterministic(mb):
+    w = W.C1
+    ws = mb.workspace(w.n, w.g, w.r, w.B)
+    a = mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, ws=ws).clone()
+    for _ in range(3):
+        b = mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, ws=ws)
+        assert torch.equal(a, b)
+    # a different region through the same workspace/output (new graph) still matches
+    b = mb.ask(W.SEAHORSE_REGION, w.n, w.maxdwell, w.g, w.r, w.B, ws=ws)
+    A, _ = oracle.ask(W.SEAHORSE_REGION, w.n, w.maxdwell, w.g, w.r, w.B)
+    assert np.array_equal(b.cpu().numpy(), A)
+
+
+def test_ask_to_host(mb):
+    w = W.C1
+    ws = mb.workspace(w.n, w.g, w.r, w.B)
+    out = torch.empty((w.n, w.n), dtype=torch.int32, device="cuda")
+    h = torch.empty(w.n * w.n, dtype=torch.int32).pin_memory()
+    mb.ask_to_host(w.region, w.n, w.maxdwell, w.g, w.r, w.B, h, out, ws)
+    A, _ = oracle.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B)
+    assert np.array_equal(h.numpy().reshape(w.n, w.n), A)
+
+
+# ----------------------------------------------------------------------------- full sizes
+def _sample_tiles(g, k, seed):
+    rng = np.random.default_rng(seed)
+    return sorted(rng.choice(g * g, size=k, replace=False).tolist())
+
+
+@pytest.mark.parametrize("wname", ["C3", "C5"])
+def test_full_size_ask_sampled_tiles(mb, wname):
+    """BASELINE C3 / C5 at full size in bench.py's launch configuration (all g*g tiles, B200
+    scheme): sampled level-0 tiles equal the oracle's recursion on those tiles."""
+    w = W.CONFIGS[wname]
+    ws = mb.workspace(w.n, w.g, w.r, w.B)
+    out = mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, ws=ws, stats=True)
+    torch.cuda.synchronize()
+    st = mb.ask_stats(ws)
+    d0 = w.n // w.g
+    tiles = _sample_tiles(w.g, 3, W.SEED + (3 if wname == "C3" else 5))
+    for t in tiles:
+        gy, gx = divmod(t, w.g)
+        A, _ = oracle.ask_tile(w.region, w.n, w.maxdwell, w.g, w.r, w.B, t)
+        got = out[gy * d0:(gy + 1) * d0, gx * d0:(gx + 1) * d0].cpu().numpy()
+        assert np.array_equal(got, A), t
+    # structural identities at full size
+    st = _trim(st)
+    for a, b in zip(st, st[1:]):
+        assert b["regions_in"] == w.r * w.r * a["subdivided"]
+    for s in st:
+        assert s["regions_in"] == s["filled"] + s["subdivided"] + s["leaves"]
+
+
+@pytest.mark.parametrize("wname", ["C3", "C5"])
+def test_full_size_exhaustive_sampled_pixels(mb, wname):
+    w = W.CONFIGS[wname]
+    out = mb.exhaustive(w.region, w.n, w.maxdwell)
+    rng = np.random.default_rng(W.SEED)
+    ii = rng.integers(0, w.n, 4000)
+    jj = rng.integers(0, w.n, 4000)
+    ref = oracle.dwell_pixels(w.region, w.n, w.maxdwell, ii, jj)
+    got = out[torch.as_tensor(ii, device="cuda"), torch.as_tensor(jj, device="cuda")].cpu().numpy()
+    assert np.array_equal(got, ref)
+    # plus two full rows (a ragged mix of inside / outside)
+    for i in (w.n // 2 - 1, w.n // 3):
+        assert np.array_equal(out[i].cpu().numpy(), oracle.exhaustive(w.region, w.n, w.maxdwell, i, 1)[0])
