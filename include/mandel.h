@@ -94,7 +94,22 @@ enum {
 };
 
 /* flags */
-#define MANDEL_FLAG_STATS 1u /* also accumulate border/leaf pixel + iteration counters */
+#define MANDEL_FLAG_STATS 1u  /* also accumulate border/leaf pixel + iteration counters   */
+#define MANDEL_FLAG_TIMING 2u /* record a CUDA event after every kernel of the call (graph
+                                 event-record nodes) for mandel_ask_kernel_times()          */
+#define MANDEL_FLAG_TILE_COST 4u /* accumulate executed iterations per level-0 tile for
+                                    mandel_ask_tile_costs() (per-pixel atomics: preview use) */
+
+/* Kernel kinds reported by mandel_ask_kernel_times (value = kind * 100 + level). */
+enum {
+    MANDEL_KIND_INIT = 0,          /* level-0 offset list + counters                          */
+    MANDEL_KIND_B200_BORDER = 1,   /* new border pixels of a level (dwell)                    */
+    MANDEL_KIND_B200_CLASSIFY = 2, /* warp-per-region uniformity test + list appends          */
+    MANDEL_KIND_FILL = 3,          /* fill of the level's uniform regions                     */
+    MANDEL_KIND_B200_LEAF = 4,     /* leaf interiors, flat                                    */
+    MANDEL_KIND_SBR_LEVEL = 5,     /* paper SBR: block-per-region border + decision           */
+    MANDEL_KIND_SBR_LEAF = 6       /* paper SBR: block-per-leaf interior                      */
+};
 
 /* Bytes of workspace mandel_ask / mandel_ask_tiles need for these parameters (worst case
  * over all images: every region at every level may subdivide).  0 if invalid. */
@@ -132,6 +147,17 @@ int mandel_ask_to_host(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g
  * Writes min(levels, max_levels) entries; returns the number of levels (>= 0) or -code. */
 int mandel_ask_last_stats(const void *d_ws, mandel_level_stats *h_out, int32_t max_levels,
                           void *stream);
+
+/* Device time of every kernel of the most recent mandel_ask_tiles call made with
+ * MANDEL_FLAG_TIMING (waits for it to finish).  Writes up to max_kernels entries of ms[]
+ * (milliseconds, may be NULL) and kind_level[] (may be NULL); returns the kernel count or
+ * -code. */
+int mandel_ask_kernel_times(float *ms, int32_t *kind_level, int32_t max_kernels);
+
+/* Executed iterations per level-0 tile (canonical id order, g*g entries, u64) of the last
+ * call on d_ws made with MANDEL_FLAG_TILE_COST (synchronises `stream`).  Writes up to
+ * max_tiles entries; returns g*g or -code.  Used to rank tiles for the multi-GPU deal. */
+int mandel_ask_tile_costs(const void *d_ws, uint64_t *h_costs, int32_t max_tiles, void *stream);
 
 /* Number of kernel launches one mandel_ask_tiles call issues for these parameters. */
 int32_t mandel_ask_kernel_count(int64_t n, int32_t g, int32_t r, int32_t B, int32_t scheme);

@@ -72,14 +72,19 @@ def exhaustive(region: Sequence[float], n: int, maxdwell: int, out=None, stream=
 
 
 def ask(region: Sequence[float], n: int, maxdwell: int, g: int, r: int, B: int, out=None, ws=None,
-        tiles: Optional[Sequence[int]] = None, scheme: str = "b200", stats: bool = False, stream=None):
-    """ASK dwell image over all g*g level-0 regions, or only `tiles`."""
+        tiles: Optional[Sequence[int]] = None, scheme: str = "b200", stats: bool = False,
+        timing: bool = False, tile_cost: bool = False, stream=None):
+    """ASK dwell image over all g*g level-0 regions, or only `tiles`.
+    stats: accumulate per-level counters (ask_stats); timing: per-kernel events
+    (kernel_times)."""
     out = _image(n, out)
     if ws is None:
         ws = workspace(n, g, r, B, device=out.device)
     t_ptr, t_n, _keep = _lib.tiles_arg(tiles)
     rc = _lib.load().mandel_ask_tiles(_lib.region(region), n, maxdwell, g, r, B, t_ptr, t_n,
-                                      SCHEMES[scheme], _lib.FLAG_STATS if stats else 0,
+                                      SCHEMES[scheme],
+                                      (_lib.FLAG_STATS if stats else 0) | (_lib.FLAG_TIMING if timing else 0)
+                                      | (_lib.FLAG_TILE_COST if tile_cost else 0),
                                       out.data_ptr(), out.stride(0), ws.data_ptr(), ws.numel(),
                                       _stream_ptr(stream))
     _lib.check(rc, "mandel_ask_tiles")
@@ -102,6 +107,30 @@ def ask_to_host(region, n, maxdwell, g, r, B, h_out, out, ws, tiles=None, scheme
                                         ws.numel(), h_out.data_ptr(), _stream_ptr(stream))
     _lib.check(rc, "mandel_ask_to_host")
     return h_out
+
+
+def tile_costs(ws, g: int, stream=None) -> List[int]:
+    """Executed iterations per level-0 tile of the last ask(..., tile_cost=True) on `ws`."""
+    return _lib.tile_costs(ws.data_ptr(), g, _stream_ptr(stream))
+
+
+def preview_costs(region, n: int, maxdwell: int, g: int, r: int, B: int, shrink: int = 16,
+                  dwell_shrink: int = 8, scheme: str = "b200") -> List[int]:
+    """Per-tile cost estimate for the cost-ranked deal: ASK itself on an
+    n/shrink preview with maxdwell/dwell_shrink and B/shrink (>= 2), same g and r."""
+    pn = max(g * 2, n // shrink)
+    pB = max(2, B // shrink)
+    while g * pB > pn:
+        pB //= 2
+    pmd = max(1, maxdwell // dwell_shrink)
+    ws = workspace(pn, g, r, pB)
+    ask(region, pn, pmd, g, r, pB, ws=ws, scheme=scheme, tile_cost=True)
+    return tile_costs(ws, g)
+
+
+def kernel_times() -> List[dict]:
+    """Per-kernel device times (ms) of the most recent ask(..., timing=True) call."""
+    return _lib.kernel_times()
 
 
 def shutdown() -> None:

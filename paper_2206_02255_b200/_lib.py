@@ -17,6 +17,10 @@ LIB_PATH = os.path.join(HERE, "libmandel_b200.so")
 MANDEL_OK, MANDEL_EINVAL, MANDEL_EWORKSPACE, MANDEL_ECUDA = 0, 1, 2, 3
 SCHEME_SBR, SCHEME_B200 = 0, 1
 FLAG_STATS = 1
+FLAG_TIMING = 2
+FLAG_TILE_COST = 4
+KIND_NAMES = {0: "init", 1: "b200_border", 2: "b200_classify", 3: "fill", 4: "b200_leaf",
+              5: "sbr_level", 6: "sbr_leaf"}
 
 _lock = threading.Lock()
 _lib: Optional[ctypes.CDLL] = None
@@ -60,6 +64,8 @@ _SIGS = [
     ("mandel_ask_last_stats", ctypes.c_int, [_P, ctypes.POINTER(MandelLevelStats), ctypes.c_int32, _P]),
     ("mandel_ask_kernel_count", ctypes.c_int32, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                                  ctypes.c_int32]),
+    ("mandel_ask_kernel_times", ctypes.c_int, [_P, _P, ctypes.c_int32]),
+    ("mandel_ask_tile_costs", ctypes.c_int, [_P, _P, ctypes.c_int32, _P]),
     ("mandel_strerror", ctypes.c_char_p, [ctypes.c_int]),
     ("mandel_last_cuda_error", ctypes.c_char_p, []),
     ("mandel_shutdown", None, []),
@@ -111,3 +117,25 @@ def stats(ws_ptr: int, stream_ptr: int, max_levels: int = 32) -> List[dict]:
         s = buf[i]
         out.append({k: int(getattr(s, k)) for k, _ in MandelLevelStats._fields_})
     return out
+
+
+def kernel_times(max_kernels: int = 256) -> List[dict]:
+    """Per-kernel device times of the last MANDEL_FLAG_TIMING call."""
+    lib = load()
+    ms = (ctypes.c_float * max_kernels)()
+    kl = (ctypes.c_int32 * max_kernels)()
+    nk = lib.mandel_ask_kernel_times(ctypes.cast(ms, ctypes.c_void_p), ctypes.cast(kl, ctypes.c_void_p),
+                                     max_kernels)
+    if nk < 0:
+        raise MandelError(-nk, "mandel_ask_kernel_times")
+    return [{"kind": KIND_NAMES[kl[i] // 100], "level": kl[i] % 100, "ms": float(ms[i])}
+            for i in range(min(nk, max_kernels))]
+
+
+def tile_costs(ws_ptr: int, g: int, stream_ptr: int) -> List[int]:
+    lib = load()
+    buf = (ctypes.c_uint64 * (g * g))()
+    rc = lib.mandel_ask_tile_costs(ws_ptr, ctypes.cast(buf, ctypes.c_void_p), g * g, stream_ptr)
+    if rc < 0:
+        raise MandelError(-rc, "mandel_ask_tile_costs")
+    return [int(v) for v in buf]

@@ -73,7 +73,17 @@ struct LevelArgs {
     int level, d, r, B, g, ntiles, levels, scheme;
     int subdivide;           // d / r >= B
     int log2_q4, log2_row4;  // fill: log2(d*d/4), log2(d/4)
+    unsigned long long *tile_cost; // MANDEL_FLAG_TILE_COST: iterations per level-0 tile
+    int d0;                  // level-0 side
 };
+
+// Per-level-0-tile executed-iteration counter (stats builds only; used by the multi-GPU
+// cost-ranked deal's preview run).
+__device__ __forceinline__ void add_tile_cost(const LevelArgs &a, int x, int y, int v)
+{
+    if (a.tile_cost)
+        atomicAdd(&a.tile_cost[(y / a.d0) * a.g + x / a.d0], (unsigned long long)v);
+}
 
 // --------------------------------------------------------------------------- helpers
 __device__ __forceinline__ uint32_t level_count(const LevelArgs &a)
@@ -143,6 +153,8 @@ __global__ void k_init(LevelArgs a)
     }
     if (t == 1)
         a.hdr->n = (uint32_t)(a.d * a.g);
+    if (a.tile_cost && t < a.g * a.g)
+        a.tile_cost[t] = 0ull;
     if (t < a.ntiles) {
         const int k = a.tiles ? a.tiles[t] : t;
         const int gx = k % a.g, gy = k / a.g;
@@ -195,8 +207,10 @@ __global__ void __launch_bounds__(TPB) k_sbr_level(LevelArgs a)
             a.out[(long long)y * a.pitch + x] = v;
             lo = min(lo, v);
             hi = max(hi, v);
-            if (STATS)
+            if (STATS) {
                 it += (unsigned long long)v;
+                add_tile_cost(a, x, y, v);
+            }
         }
         lo = __reduce_min_sync(0xffffffffu, lo);
         hi = __reduce_max_sync(0xffffffffu, hi);
@@ -243,8 +257,10 @@ __global__ void __launch_bounds__(TPB) k_sbr_leaf(LevelArgs a)
             const int x = x0 + p % m, y = y0 + p / m;
             const int v = dwell<DWELL_K>(pix_re(a.map, x), pix_im(a.map, y), a.maxdwell);
             a.out[(long long)y * a.pitch + x] = v;
-            if (STATS)
+            if (STATS) {
                 it += (unsigned long long)v;
+                add_tile_cost(a, x, y, v);
+            }
         }
         if (STATS) {
             it = block_sum_u64<TPB>(it, s_sum);
@@ -351,6 +367,7 @@ __global__ void __launch_bounds__(256) k_b200_border(LevelArgs a)
         if (STATS) {
             it += (unsigned long long)v;
             px += 1;
+            add_tile_cost(a, x, y, v);
         }
     }
     if (STATS) {
@@ -415,6 +432,7 @@ __global__ void __launch_bounds__(256) k_b200_leaf(LevelArgs a)
         if (STATS) {
             it += (unsigned long long)v;
             px += 1;
+            add_tile_cost(a, x, y, v);
         }
     }
     if (STATS) {

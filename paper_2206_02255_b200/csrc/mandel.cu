@@ -70,7 +70,7 @@ int levels_of(int64_t n, int32_t g, int32_t r, int32_t B)
 // Workspace layout.  cap_l = g^2 r^(2l) (every region may subdivide).
 struct Layout {
     int L;
-    size_t hdr, tiles, olt[2], fill, leaf, total;
+    size_t hdr, tiles, olt[2], fill, leaf, tile_cost, total;
     size_t fill_off[MAXL]; // element offset of each level's fill segment
     size_t cap[MAXL];
 };
@@ -105,6 +105,8 @@ bool make_layout(int64_t n, int32_t g, int32_t r, int32_t B, Layout &lay)
     o = align256(o + fsum * 8);
     lay.leaf = o;
     o = align256(o + capmax * 4);
+    lay.tile_cost = o;
+    o = align256(o + (size_t)g * g * 8);
     lay.total = o;
     return true;
 }
@@ -147,12 +149,15 @@ struct Entry {
     cudaGraphExec_t exec = nullptr;
     int32_t *h_tiles = nullptr; // pinned, mapped (read by k_init through UVA)
     unsigned long long last_use = 0;
+    std::vector<cudaEvent_t> evs; // MANDEL_FLAG_TIMING only
+    std::vector<int32_t> kinds;
+    unsigned long long id = 0;
 };
 
 std::mutex g_mu;
 std::vector<Entry> g_cache;
 std::vector<DevInfo> g_dev;
-unsigned long long g_clock = 0;
+unsigned long long g_clock = 0, g_next_id = 0, g_last_timed = 0;
 constexpr size_t kMaxGraphs = 64;
 
 int dev_info(int dev, DevInfo *&out)
@@ -180,9 +185,37 @@ int resident_grid(K kernel, int tpb, int sms, size_t cap_blocks)
     return (int)(g < 1 ? 1 : g);
 }
 
+// Per-kernel timing inside the graph (MANDEL_FLAG_TIMING): an external event-record node
+// before the first kernel and after every kernel.
+struct Timing {
+    bool on = false;
+    std::vector<cudaEvent_t> evs;
+    std::vector<int32_t> kinds; // kind * 100 + level, one per kernel
+};
+
+int mark(Timing *tm, int kind, int level, cudaStream_t s)
+{
+    if (!tm || !tm->on)
+        return MANDEL_OK;
+    cudaEvent_t ev;
+    CK(cudaEventCreate(&ev));
+    tm->evs.push_back(ev);
+    if (kind >= 0)
+        tm->kinds.push_back(kind * 100 + level);
+    CK(cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal));
+    return MANDEL_OK;
+}
+
+#define MARK(kind, level)                                                                      \
+    do {                                                                                       \
+        int m_ = mark(tm, (kind), (level), s);                                                 \
+        if (m_)                                                                                \
+            return m_;                                                                         \
+    } while (0)
+
 // Enqueue the whole ASK call on `s` (called under stream capture).
 int enqueue_ask(const Key &k, const Layout &lay, const int32_t *d_tiles_visible, int ntiles, int sms,
-                cudaStream_t s)
+                cudaStream_t s, Timing *tm)
 {
     char *ws = (char *)k.ws;
     LevelArgs a;
@@ -200,7 +233,9 @@ int enqueue_ask(const Key &k, const Layout &lay, const int32_t *d_tiles_visible,
     a.ntiles = ntiles;
     a.levels = lay.L;
     a.scheme = k.scheme;
-    const bool stats = (k.flags & MANDEL_FLAG_STATS) != 0;
+    a.d0 = (int)(k.n / k.g);
+    a.tile_cost = (k.flags & MANDEL_FLAG_TILE_COST) ? (unsigned long long *)(ws + lay.tile_cost) : nullptr;
+    const bool stats = (k.flags & (MANDEL_FLAG_STATS | MANDEL_FLAG_TILE_COST)) != 0;
     const bool vec_ok = ((uintptr_t)k.out % 16 == 0) && (k.pitch % 4 == 0);
     const int d0 = (int)(k.n / k.g);
 
@@ -210,8 +245,12 @@ int enqueue_ask(const Key &k, const Layout &lay, const int32_t *d_tiles_visible,
     a.olt_in = (const uint32_t *)(ws + lay.olt[0]);
     {
         int nthr = ntiles > 1024 ? ntiles : 1024;
+        if (nthr < k.g * k.g)
+            nthr = k.g * k.g;
+        MARK(-1, 0);
         k_init<<<(nthr + 255) / 256, 256, 0, s>>>(a);
         CK(cudaGetLastError());
+        MARK(MANDEL_KIND_INIT, 0);
     }
     int d = d0;
     for (int l = 0; l < lay.L; ++l) {
@@ -247,6 +286,7 @@ int enqueue_ask(const Key &k, const Layout &lay, const int32_t *d_tiles_visible,
                 SBR_LAUNCH(32);
 #undef SBR_LAUNCH
             CK(cudaGetLastError());
+            MARK(MANDEL_KIND_SBR_LEVEL, l);
         } else {
             size_t work = (l == 0) ? cap * (size_t)(4 * d - 4)
                                    : (cap / ((size_t)k.r * k.r)) * new_border_px_per_parent(d * k.r, k.r);
@@ -259,9 +299,11 @@ int enqueue_ask(const Key &k, const Layout &lay, const int32_t *d_tiles_visible,
                 k_b200_border<false><<<gsz, 256, 0, s>>>(a);
             }
             CK(cudaGetLastError());
+            MARK(MANDEL_KIND_B200_BORDER, l);
             int gsz = resident_grid(k_b200_classify, 256, sms, (cap + 7) / 8);
             k_b200_classify<<<gsz, 256, 0, s>>>(a);
             CK(cudaGetLastError());
+            MARK(MANDEL_KIND_B200_CLASSIFY, l);
         }
         // fill (terminal work) of this level's uniform regions
         {
@@ -278,6 +320,7 @@ int enqueue_ask(const Key &k, const Layout &lay, const int32_t *d_tiles_visible,
                 k_fill<false><<<gsz, 256, 0, s>>>(a);
             }
             CK(cudaGetLastError());
+            MARK(MANDEL_KIND_FILL, l);
         }
         if (l + 1 < lay.L)
             d /= k.r;
@@ -321,6 +364,7 @@ int enqueue_ask(const Key &k, const Layout &lay, const int32_t *d_tiles_visible,
             }
         }
         CK(cudaGetLastError());
+        MARK(k.scheme == MANDEL_SCHEME_SBR ? MANDEL_KIND_SBR_LEAF : MANDEL_KIND_B200_LEAF, lay.L - 1);
     }
     return MANDEL_OK;
 }
@@ -331,6 +375,9 @@ void free_entry(Entry &e)
         cudaGraphExecDestroy(e.exec);
     if (e.h_tiles)
         cudaFreeHost(e.h_tiles);
+    for (auto ev : e.evs)
+        cudaEventDestroy(ev);
+    e.evs.clear();
     e.exec = nullptr;
     e.h_tiles = nullptr;
 }
@@ -396,7 +443,7 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
     if (rc)
         return rc;
     if (!valid_grb(n, g, r, B) || !d_ws || (scheme != MANDEL_SCHEME_SBR && scheme != MANDEL_SCHEME_B200) ||
-        (flags & ~MANDEL_FLAG_STATS) != 0)
+        (flags & ~(MANDEL_FLAG_STATS | MANDEL_FLAG_TIMING | MANDEL_FLAG_TILE_COST)) != 0)
         return MANDEL_EINVAL;
     Layout lay;
     if (!make_layout(n, g, r, B, lay))
@@ -465,7 +512,12 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
             free_entry(e);
             return cuda_fail(ce, "cudaStreamBeginCapture");
         }
-        int erc = enqueue_ask(key, lay, d_tiles, ntiles, di->sms, di->cap);
+        Timing tm;
+        tm.on = (flags & MANDEL_FLAG_TIMING) != 0;
+        int erc = enqueue_ask(key, lay, d_tiles, ntiles, di->sms, di->cap, &tm);
+        e.evs = tm.evs;
+        e.kinds = tm.kinds;
+        e.id = ++g_next_id;
         ce = cudaStreamEndCapture(di->cap, &graph);
         if (erc || ce != cudaSuccess) {
             if (graph)
@@ -484,7 +536,31 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
     }
     hit->last_use = ++g_clock;
     CK(cudaGraphLaunch(hit->exec, (cudaStream_t)stream));
+    if (!hit->evs.empty())
+        g_last_timed = hit->id;
     return MANDEL_OK;
+}
+
+int mandel_ask_kernel_times(float *ms, int32_t *kind_level, int32_t max_kernels)
+{
+    std::lock_guard<std::mutex> lk(g_mu);
+    const Entry *hit = nullptr;
+    for (auto &e : g_cache)
+        if (e.id == g_last_timed && !e.evs.empty())
+            hit = &e;
+    if (!hit)
+        return -MANDEL_EINVAL;
+    CK(cudaEventSynchronize(hit->evs.back()));
+    const int nk = (int)hit->kinds.size();
+    for (int i = 0; i < nk && i < max_kernels; ++i) {
+        float t = 0.0f;
+        CK(cudaEventElapsedTime(&t, hit->evs[(size_t)i], hit->evs[(size_t)i + 1]));
+        if (ms)
+            ms[i] = t;
+        if (kind_level)
+            kind_level[i] = hit->kinds[(size_t)i];
+    }
+    return nk;
 }
 
 int mandel_ask(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, int32_t r, int32_t B, int32_t *d_out,
@@ -504,8 +580,19 @@ int mandel_ask_to_host(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g
                               ws_bytes, stream);
     if (rc)
         return rc;
-    CK(cudaMemcpy2DAsync(h_out, (size_t)n * 4, d_out, (size_t)out_pitch * 4, (size_t)n * 4, (size_t)n,
-                         cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    if (h_tile_ids) { // only the tiles' pixels: one 2-D copy per tile
+        const int64_t d0 = n / g;
+        for (int32_t i = 0; i < n_tiles; ++i) {
+            const int64_t gy = h_tile_ids[i] / g, gx = h_tile_ids[i] % g;
+            const size_t off_h = (size_t)(gy * d0) * (size_t)n + (size_t)(gx * d0);
+            const size_t off_d = (size_t)(gy * d0) * (size_t)out_pitch + (size_t)(gx * d0);
+            CK(cudaMemcpy2DAsync(h_out + off_h, (size_t)n * 4, d_out + off_d, (size_t)out_pitch * 4,
+                                 (size_t)d0 * 4, (size_t)d0, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+        }
+    } else {
+        CK(cudaMemcpy2DAsync(h_out, (size_t)n * 4, d_out, (size_t)out_pitch * 4, (size_t)n * 4, (size_t)n,
+                             cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    }
     CK(cudaStreamSynchronize((cudaStream_t)stream));
     return MANDEL_OK;
 }
@@ -538,6 +625,24 @@ int mandel_ask_last_stats(const void *d_ws, mandel_level_stats *h_out, int32_t m
         d /= h.r;
     }
     return L;
+}
+
+int mandel_ask_tile_costs(const void *d_ws, uint64_t *h_costs, int32_t max_tiles, void *stream)
+{
+    if (!d_ws || !h_costs || max_tiles < 0)
+        return -MANDEL_EINVAL;
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    WsHeader h;
+    CK(cudaMemcpy(&h, d_ws, sizeof h, cudaMemcpyDeviceToHost));
+    if (h.magic != WS_MAGIC)
+        return -MANDEL_EINVAL;
+    Layout lay;
+    if (!make_layout((int64_t)h.n, (int32_t)h.g, (int32_t)h.r, (int32_t)h.B, lay))
+        return -MANDEL_EINVAL;
+    const int G = (int)(h.g * h.g);
+    const int cnt = G < max_tiles ? G : max_tiles;
+    CK(cudaMemcpy(h_costs, (const char *)d_ws + lay.tile_cost, (size_t)cnt * 8, cudaMemcpyDeviceToHost));
+    return G;
 }
 
 const char *mandel_strerror(int code)
