@@ -99,6 +99,9 @@ enum {
                                  event-record nodes) for mandel_ask_kernel_times()          */
 #define MANDEL_FLAG_TILE_COST 4u /* accumulate executed iterations per level-0 tile for
                                     mandel_ask_tile_costs() (per-pixel atomics: preview use) */
+#define MANDEL_FLAG_FLAT 8u      /* B200 scheme: plain one-thread-per-pixel border and leaf
+                                    kernels instead of the lane-refill ones (A/B baseline;
+                                    same image)                                            */
 
 /* Kernel kinds reported by mandel_ask_kernel_times (value = kind * 100 + level). */
 enum {

@@ -12,13 +12,16 @@ import threading
 from typing import List, Optional, Sequence
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmandel_b200.so")
+# MANDEL_B200_LIB: alternative build of the same library (tuning sweeps build variants with
+# different -D knobs into gpurun_out/); default: the in-tree build.
+LIB_PATH = os.environ.get("MANDEL_B200_LIB") or os.path.join(HERE, "libmandel_b200.so")
 
 MANDEL_OK, MANDEL_EINVAL, MANDEL_EWORKSPACE, MANDEL_ECUDA = 0, 1, 2, 3
 SCHEME_SBR, SCHEME_B200 = 0, 1
 FLAG_STATS = 1
 FLAG_TIMING = 2
 FLAG_TILE_COST = 4
+FLAG_FLAT = 8
 KIND_NAMES = {0: "init", 1: "b200_border", 2: "b200_classify", 3: "fill", 4: "b200_leaf",
               5: "sbr_level", 6: "sbr_leaf"}
 

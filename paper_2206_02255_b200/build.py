@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SRC_DIR = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmandel_b200.so")
 SOURCES = ["mandel.cu"]
-DEPS = ["mandel.cu", "ask_kernels.cuh", "dwell.cuh", os.path.join("..", "..", "include", "mandel.h")]
+DEPS = ["mandel.cu", "ask_kernels.cuh", "dwell.cuh", "refill.cuh", os.path.join("..", "..", "include", "mandel.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 NVCC_FLAGS = [
@@ -31,21 +31,26 @@ def _stale() -> bool:
     return any(os.path.getmtime(os.path.join(SRC_DIR, d)) > t for d in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """Build the library (in-tree by default).  `out`/`defines`: a variant with extra -D
+    knobs (e.g. MANDEL_RF_T=4) at another path, for tuning sweeps."""
+    target = out or LIB
+    if out is None and not defines and not force and not _stale():
         return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *NVCC_FLAGS, "-o", tmp, *[os.path.join(SRC_DIR, s) for s in SOURCES]]
+    tmp = target + f".tmp{os.getpid()}"
+    cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", tmp,
+           *[os.path.join(SRC_DIR, s) for s in SOURCES]]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc failed building libmandel_b200.so")
     if verbose:
         sys.stderr.write(res.stderr)
-    with open(os.path.join(HERE, "ptxas_info.txt"), "w") as f:
-        f.write(res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    if out is None:
+        with open(os.path.join(HERE, "ptxas_info.txt"), "w") as f:
+            f.write(res.stderr)
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

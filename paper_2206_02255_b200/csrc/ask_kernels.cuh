@@ -11,12 +11,25 @@
 #include <stdint.h>
 
 #include "dwell.cuh"
+#include "refill.cuh"
 
 namespace mandel {
 
 constexpr int MAXL = 32;
 constexpr uint32_t WS_MAGIC = 0x4d41534bu; // "MASK"
 constexpr int DWELL_K = 8;                 // iterations per escape test (dwell.cuh)
+#ifndef MANDEL_RF_K
+#define MANDEL_RF_K 16
+#endif
+#ifndef MANDEL_RF_T
+#define MANDEL_RF_T 8
+#endif
+#ifndef MANDEL_RF_CH
+#define MANDEL_RF_CH 128
+#endif
+constexpr int RF_K = MANDEL_RF_K;   // lane-refill chunk (iterations per escape test)
+constexpr int RF_T = MANDEL_RF_T;   // frozen lanes that trigger a warp refill
+constexpr int RF_CH = MANDEL_RF_CH; // indices a warp grabs per cursor atomic
 
 struct WsHeader {
     uint32_t magic, levels, n, g, r, B, ntiles, scheme; // written by k_init
@@ -26,6 +39,7 @@ struct WsHeader {
     uint32_t pad0;
     unsigned long long border_px[MAXL], border_iters[MAXL];
     unsigned long long leaf_px, leaf_iters;
+    unsigned long long cursor[MAXL + 1]; // lane-refill work cursors: border level l, leaves
 };
 static_assert(sizeof(WsHeader) <= 4096, "header");
 
@@ -75,7 +89,32 @@ struct LevelArgs {
     int log2_q4, log2_row4;  // fill: log2(d*d/4), log2(d/4)
     unsigned long long *tile_cost; // MANDEL_FLAG_TILE_COST: iterations per level-0 tile
     int d0;                  // level-0 side
+    // Column lines, transposed (B200 scheme, leaf side u >= 8): every pixel
+    // on a column x with x mod u in {0, u-1} -- the only columns any region ring uses -- is
+    // also stored at colT[(2 (x / u) + (x mod u != 0)) * colT_pitch + y], so classification
+    // reads ring columns as contiguous runs instead of one 32-byte image sector per pixel.
+    int *colT;               // NULL: classify reads columns from the image
+    int u_log2;
+    long long colT_pitch;    // = n
 };
+
+__device__ __forceinline__ bool on_col_line(const LevelArgs &a, int x)
+{
+    const int m = x & ((1 << a.u_log2) - 1);
+    return m == 0 || m == (1 << a.u_log2) - 1;
+}
+__device__ __forceinline__ long long colT_index(const LevelArgs &a, int x, int y)
+{
+    const int m = x & ((1 << a.u_log2) - 1);
+    return (long long)(2 * (x >> a.u_log2) + (m != 0)) * a.colT_pitch + y;
+}
+// Store a ring pixel's dwell: image, plus the transposed column copy when x is a column line.
+__device__ __forceinline__ void store_ring(const LevelArgs &a, int x, int y, int v)
+{
+    a.out[(long long)y * a.pitch + x] = v;
+    if (a.colT && on_col_line(a, x))
+        a.colT[colT_index(a, x, y)] = v;
+}
 
 // Per-level-0-tile executed-iteration counter (stats builds only; used by the multi-GPU
 // cost-ranked deal's preview run).
@@ -363,7 +402,7 @@ __global__ void __launch_bounds__(256) k_b200_border(LevelArgs a)
             }
         }
         const int v = dwell<DWELL_K>(pix_re(a.map, x), pix_im(a.map, y), a.maxdwell);
-        a.out[(long long)y * a.pitch + x] = v;
+        store_ring(a, x, y, v);
         if (STATS) {
             it += (unsigned long long)v;
             px += 1;
@@ -396,7 +435,8 @@ __global__ void __launch_bounds__(256) k_b200_classify(LevelArgs a)
         for (int b = lane; b < ring; b += 32) {
             int x, y;
             ring_pixel(b, d, x0, y0, x, y);
-            const int v = __ldcg(a.out + (long long)y * a.pitch + x);
+            const int v = (a.colT && b >= 2 * d) ? __ldcg(a.colT + colT_index(a, x, y))
+                                                 : __ldcg(a.out + (long long)y * a.pitch + x);
             lo = min(lo, v);
             hi = max(hi, v);
         }
@@ -443,6 +483,141 @@ __global__ void __launch_bounds__(256) k_b200_leaf(LevelArgs a)
         if (threadIdx.x == 0 && px)
             atomicAdd(&a.hdr->leaf_px, px);
     }
+}
+
+// --------------------------------------------------------------------------- lane refill
+// B200 border and leaf kernels on the lane-refill engine (refill.cuh): the
+// same flat index spaces as k_b200_border / k_b200_leaf, computed by persistent warps whose
+// lanes take a new pixel as soon as theirs is done.
+
+// 32-bit fast path for the index split t -> (unit, local) when t < 2^32.
+__device__ __forceinline__ void split_index(unsigned long long t, uint32_t per, uint32_t &p, uint32_t &loc)
+{
+    if ((t >> 32) == 0ull) {
+        const uint32_t t32 = (uint32_t)t;
+        p = t32 / per;
+        loc = t32 - p * per;
+    } else {
+        p = (uint32_t)(t / per);
+        loc = (uint32_t)(t - (unsigned long long)p * per);
+    }
+}
+
+// Leaf interiors: t = leaf * (d-2)^2 + row-major interior offset.
+struct LeafMap {
+    const uint32_t *leaf;
+    uint32_t m, I; // m = d - 2, I = m * m
+    __device__ __forceinline__ void operator()(unsigned long long t, int &x, int &y) const
+    {
+        uint32_t li, loc;
+        split_index(t, I, li, loc);
+        const uint32_t off = leaf[li];
+        const uint32_t row = loc / m;
+        x = unpack_x(off) + 1 + (int)(loc - row * m);
+        y = unpack_y(off) + 1 + (int)row;
+    }
+};
+
+// New border pixels of a level (same enumeration as k_b200_border).
+struct BorderMap {
+    const uint32_t *olt;
+    int level, d, r, D;
+    uint32_t per;
+    __device__ __forceinline__ void operator()(unsigned long long t, int &x, int &y) const
+    {
+        uint32_t p, loc;
+        split_index(t, per, p, loc);
+        if (level == 0) {
+            const uint32_t off = olt[p];
+            ring_pixel((int)loc, d, unpack_x(off), unpack_y(off), x, y);
+            return;
+        }
+        const uint32_t off = olt[(size_t)p * (uint32_t)(r * r)]; // first child = parent origin
+        const int x0 = unpack_x(off), y0 = unpack_y(off);
+        const uint32_t pv = (uint32_t)(2 * (r - 1) * (D - 2));
+        if (loc < pv) {
+            const uint32_t line = loc / (uint32_t)(D - 2), row = loc - line * (uint32_t)(D - 2);
+            x = x0 + ((int)line / 2 + 1) * d - 1 + (int)(line & 1);
+            y = y0 + 1 + (int)row;
+        } else {
+            const uint32_t h = loc - pv, seg = (uint32_t)(d - 2), len = (uint32_t)r * seg;
+            const uint32_t line = h / len, c = h - line * len;
+            const uint32_t k = c / seg, o = c - k * seg;
+            y = y0 + ((int)line / 2 + 1) * d - 1 + (int)(line & 1);
+            x = x0 + (int)k * d + 1 + (int)o;
+        }
+    }
+};
+
+template <bool STATS, bool RING>
+struct StoreSink {
+    const LevelArgs *a;
+    unsigned long long iters, px;
+    __device__ __forceinline__ void operator()(int x, int y, int v)
+    {
+        if (RING)
+            store_ring(*a, x, y, v);
+        else
+            a->out[(long long)y * a->pitch + x] = v;
+        if (STATS) {
+            iters += (unsigned long long)v;
+            px += 1;
+            add_tile_cost(*a, x, y, v);
+        }
+    }
+};
+
+template <bool STATS, bool RING>
+__device__ __forceinline__ void sink_flush(const StoreSink<STATS, RING> &sk, unsigned long long *it_dst,
+                                           unsigned long long *px_dst)
+{
+    if (!STATS)
+        return;
+    __shared__ unsigned long long s_sum[8];
+    const unsigned long long it = block_sum_u64<256>(sk.iters, s_sum);
+    if (threadIdx.x == 0 && it)
+        atomicAdd(it_dst, it);
+    const unsigned long long px = block_sum_u64<256>(sk.px, s_sum);
+    if (threadIdx.x == 0 && px)
+        atomicAdd(px_dst, px);
+}
+
+template <bool STATS>
+__global__ void __launch_bounds__(256) k_b200_border_rf(LevelArgs a)
+{
+    BorderMap map;
+    map.olt = a.olt_in;
+    map.level = a.level;
+    map.d = a.d;
+    map.r = a.r;
+    map.D = a.d * a.r;
+    unsigned long long total;
+    if (a.level == 0) {
+        map.per = (uint32_t)(4 * a.d - 4);
+        total = (unsigned long long)map.per * (unsigned long long)a.ntiles;
+    } else {
+        map.per = new_border_px_per_parent(map.D, a.r);
+        total = (unsigned long long)map.per *
+                (unsigned long long)(*((volatile uint32_t *)&a.hdr->n_subdiv[a.level - 1]));
+    }
+    StoreSink<STATS, true> sink{&a, 0ull, 0ull};
+    refill_loop<RF_K, RF_T, RF_CH>(a.map, a.maxdwell, total, &a.hdr->cursor[a.level], map, sink);
+    sink_flush<STATS, true>(sink, &a.hdr->border_iters[a.level], &a.hdr->border_px[a.level]);
+}
+
+template <bool STATS>
+__global__ void __launch_bounds__(256) k_b200_leaf_rf(LevelArgs a)
+{
+    LeafMap map;
+    map.leaf = a.leaf;
+    map.m = (uint32_t)(a.d - 2);
+    map.I = map.m * map.m;
+    const unsigned long long total =
+        (unsigned long long)map.I * (unsigned long long)(*((volatile uint32_t *)&a.hdr->n_leaf));
+    StoreSink<STATS, false> sink{&a, 0ull, 0ull};
+    if (map.I > 0)
+        refill_loop<RF_K, RF_T, RF_CH>(a.map, a.maxdwell, total, &a.hdr->cursor[MAXL], map, sink);
+    sink_flush<STATS, false>(sink, &a.hdr->leaf_iters, &a.hdr->leaf_px);
 }
 
 } // namespace mandel

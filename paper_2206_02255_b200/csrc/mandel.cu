@@ -70,7 +70,8 @@ int levels_of(int64_t n, int32_t g, int32_t r, int32_t B)
 // Workspace layout.  cap_l = g^2 r^(2l) (every region may subdivide).
 struct Layout {
     int L;
-    size_t hdr, tiles, olt[2], fill, leaf, tile_cost, total;
+    size_t hdr, tiles, olt[2], fill, leaf, tile_cost, colT, colT_bytes, total;
+    int u_log2; // log2 of the leaf side u = (n/g) / r^(L-1)
     size_t fill_off[MAXL]; // element offset of each level's fill segment
     size_t cap[MAXL];
 };
@@ -107,6 +108,14 @@ bool make_layout(int64_t n, int32_t g, int32_t r, int32_t B, Layout &lay)
     o = align256(o + capmax * 4);
     lay.tile_cost = o;
     o = align256(o + (size_t)g * g * 8);
+    // transposed column lines (used when the leaf side u >= 8): 2 n/u columns of n rows
+    int64_t u = n / g;
+    for (int l = 1; l < lay.L; ++l)
+        u /= r;
+    lay.u_log2 = ilog2(u);
+    lay.colT = o;
+    lay.colT_bytes = (u >= 8) ? (size_t)(2 * (n / u)) * (size_t)n * 4 : 0;
+    o = align256(o + lay.colT_bytes);
     lay.total = o;
     return true;
 }
@@ -236,6 +245,12 @@ int enqueue_ask(const Key &k, const Layout &lay, const int32_t *d_tiles_visible,
     a.d0 = (int)(k.n / k.g);
     a.tile_cost = (k.flags & MANDEL_FLAG_TILE_COST) ? (unsigned long long *)(ws + lay.tile_cost) : nullptr;
     const bool stats = (k.flags & (MANDEL_FLAG_STATS | MANDEL_FLAG_TILE_COST)) != 0;
+    const bool flat = (k.flags & MANDEL_FLAG_FLAT) != 0;
+    if (k.scheme == MANDEL_SCHEME_B200 && lay.colT_bytes) {
+        a.colT = (int *)(ws + lay.colT);
+        a.u_log2 = lay.u_log2;
+        a.colT_pitch = k.n;
+    }
     const bool vec_ok = ((uintptr_t)k.out % 16 == 0) && (k.pitch % 4 == 0);
     const int d0 = (int)(k.n / k.g);
 
@@ -291,12 +306,23 @@ int enqueue_ask(const Key &k, const Layout &lay, const int32_t *d_tiles_visible,
             size_t work = (l == 0) ? cap * (size_t)(4 * d - 4)
                                    : (cap / ((size_t)k.r * k.r)) * new_border_px_per_parent(d * k.r, k.r);
             size_t blocks = (work + 255) / 256;
-            if (stats) {
-                int gsz = resident_grid(k_b200_border<true>, 256, sms, blocks);
-                k_b200_border<true><<<gsz, 256, 0, s>>>(a);
-            } else {
-                int gsz = resident_grid(k_b200_border<false>, 256, sms, blocks);
-                k_b200_border<false><<<gsz, 256, 0, s>>>(a);
+            if (flat) {
+                if (stats) {
+                    int gsz = resident_grid(k_b200_border<true>, 256, sms, blocks);
+                    k_b200_border<true><<<gsz, 256, 0, s>>>(a);
+                } else {
+                    int gsz = resident_grid(k_b200_border<false>, 256, sms, blocks);
+                    k_b200_border<false><<<gsz, 256, 0, s>>>(a);
+                }
+            } else { // lane refill: persistent warps, one per 32 pixels of work at most
+                const size_t rf_blocks = (work + 255) / 256;
+                if (stats) {
+                    int gsz = resident_grid(k_b200_border_rf<true>, 256, sms, rf_blocks);
+                    k_b200_border_rf<true><<<gsz, 256, 0, s>>>(a);
+                } else {
+                    int gsz = resident_grid(k_b200_border_rf<false>, 256, sms, rf_blocks);
+                    k_b200_border_rf<false><<<gsz, 256, 0, s>>>(a);
+                }
             }
             CK(cudaGetLastError());
             MARK(MANDEL_KIND_B200_BORDER, l);
@@ -355,12 +381,22 @@ int enqueue_ask(const Key &k, const Layout &lay, const int32_t *d_tiles_visible,
 #undef LEAF_LAUNCH
         } else {
             size_t blocks = (cap * (size_t)(d - 2) * (d - 2) + 255) / 256;
-            if (stats) {
-                int gsz = resident_grid(k_b200_leaf<true>, 256, sms, blocks);
-                k_b200_leaf<true><<<gsz, 256, 0, s>>>(a);
+            if (flat) {
+                if (stats) {
+                    int gsz = resident_grid(k_b200_leaf<true>, 256, sms, blocks);
+                    k_b200_leaf<true><<<gsz, 256, 0, s>>>(a);
+                } else {
+                    int gsz = resident_grid(k_b200_leaf<false>, 256, sms, blocks);
+                    k_b200_leaf<false><<<gsz, 256, 0, s>>>(a);
+                }
             } else {
-                int gsz = resident_grid(k_b200_leaf<false>, 256, sms, blocks);
-                k_b200_leaf<false><<<gsz, 256, 0, s>>>(a);
+                if (stats) {
+                    int gsz = resident_grid(k_b200_leaf_rf<true>, 256, sms, blocks);
+                    k_b200_leaf_rf<true><<<gsz, 256, 0, s>>>(a);
+                } else {
+                    int gsz = resident_grid(k_b200_leaf_rf<false>, 256, sms, blocks);
+                    k_b200_leaf_rf<false><<<gsz, 256, 0, s>>>(a);
+                }
             }
         }
         CK(cudaGetLastError());
@@ -443,7 +479,7 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
     if (rc)
         return rc;
     if (!valid_grb(n, g, r, B) || !d_ws || (scheme != MANDEL_SCHEME_SBR && scheme != MANDEL_SCHEME_B200) ||
-        (flags & ~(MANDEL_FLAG_STATS | MANDEL_FLAG_TIMING | MANDEL_FLAG_TILE_COST)) != 0)
+        (flags & ~(MANDEL_FLAG_STATS | MANDEL_FLAG_TIMING | MANDEL_FLAG_TILE_COST | MANDEL_FLAG_FLAT)) != 0)
         return MANDEL_EINVAL;
     Layout lay;
     if (!make_layout(n, g, r, B, lay))
