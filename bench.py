@@ -179,6 +179,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-verify", action="store_true", help="skip the N>1 verification gather")
     ap.add_argument("--ref-budget", type=float, default=12.0)
     args = ap.parse_args()
 
@@ -194,6 +195,7 @@ def main():
 
     import paper_2206_02255_b200 as mb
     from paper_2206_02255_b200 import deal as deal_mod
+    from paper_2206_02255_b200 import multigpu
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -204,6 +206,7 @@ def main():
 
     # ---- partition (untimed planning is re-timed below as preview_ms)
     preview_ms = 0.0
+    parts = [list(range(w.g * w.g))]
     if world > 1:
         if args.deal == "costrank":
             torch.cuda.synchronize()
@@ -259,18 +262,25 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
     my_total = sum(step_ms)
-    if world > 1:
-        t = torch.tensor([my_total, float(exec_iters), float(border_iters), float(leaf_iters)],
-                         dtype=torch.float64, device=dev)
-        tmax = t[:1].clone()
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        tsum = t[1:].clone()
-        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
-        total_ms = float(tmax.item())
-        exec_iters_all = float(tsum[0].item())
-    else:
-        total_ms = my_total
-        exec_iters_all = float(exec_iters)
+    total_ms = multigpu.max_over_ranks(my_total, device=dev)
+    exec_iters_all = multigpu.sum_over_ranks([float(exec_iters)], device=dev)[0]
+
+    # ---- verification gather to rank 0 (N > 1 only; timed separately, not part of `value`)
+    gather = None
+    if world > 1 and not args.no_verify:
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        full = multigpu.gather_image(out, parts, w.g, rank)
+        torch.cuda.synchronize()
+        g_ms = 1e3 * (time.perf_counter() - t0)
+        gather = {"ms": multigpu.max_over_ranks(g_ms, device=dev),
+                  "bytes_to_rank0": 4 * (n * n - len(parts[0]) * (n // w.g) ** 2)}
+        if rank == 0:
+            ref = torch.empty_like(out)
+            mb.ask(w.region, n, w.maxdwell, w.g, w.r, w.B, out=ref, scheme=args.scheme)
+            gather["bit_exact_vs_1gpu_ask"] = bool(torch.equal(full, ref))
+            del ref
     ms_per_step = total_ms / args.steps
     value = n * n / (ms_per_step / 1e3) / 1e6  # Mpixel/s, whole job
 
@@ -375,6 +385,7 @@ def main():
             "mismatch_fraction_vs_exhaustive": extra.get("mismatch_fraction_vs_exhaustive"),
             "executed_iters_per_step": exec_iters_all,
             "preview_ms": preview_ms,
+            "verify_gather": gather,
             "kernel_ms_per_step": kt_sum,
             "clocks": clocks, "e2e": e2e,
             "gpu_launches": kernels_per_step * args.steps,

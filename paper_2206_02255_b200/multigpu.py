@@ -1,0 +1,101 @@
+"""Multi-GPU plumbing of the ASK path (north_star "Multi-GPU partition").
+
+Level-0 regions are independent -- every ASK decision is local to a region --
+so each rank runs mandel_ask_tiles on its own tiles and the hot path has no collective.
+This module holds the host-side logic around it, written against torch.distributed so the
+same code runs over NCCL on the GPU box and over gloo in the CPU tests:
+
+  rank_tiles(...)        the rank's level-0 tiles under a deal (deal.py)
+  max_over_ranks(v)      all_reduce(MAX) of a float (device-timed step totals)
+  sum_over_ranks(vs)     all_reduce(SUM) of counters
+  gather_image(...)      verification only: every rank packs its tiles into one contiguous
+                         buffer, rank 0 receives them (batched point-to-point; NCCL over
+                         NVLink on the box) and unpacks them into the full n x n image.
+"""
+from __future__ import annotations
+
+from typing import List, Optional, Sequence
+
+from . import deal as deal_mod
+
+
+def _dist():
+    import torch.distributed as dist
+    return dist
+
+
+def rank_tiles(method: str, g: int, world: int, rank: int,
+               costs: Optional[Sequence[float]] = None) -> List[int]:
+    parts = deal_mod.deal(method, g, world, costs)
+    return parts[rank]
+
+
+def max_over_ranks(value: float, device=None) -> float:
+    import torch
+    dist = _dist()
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(values: Sequence[float], device=None) -> List[float]:
+    import torch
+    dist = _dist()
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return [float(v) for v in values]
+    t = torch.tensor([float(v) for v in values], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return [float(v) for v in t.tolist()]
+
+
+def pack_tiles(img, tiles: Sequence[int], g: int):
+    """Contiguous (len(tiles), d0, d0) copy of the listed tiles of the n x n image `img`."""
+    import torch
+    n = img.shape[0]
+    d0 = n // g
+    out = torch.empty((len(tiles), d0, d0), dtype=img.dtype, device=img.device)
+    for i, k in enumerate(tiles):
+        gy, gx = divmod(int(k), g)
+        out[i].copy_(img[gy * d0:(gy + 1) * d0, gx * d0:(gx + 1) * d0])
+    return out
+
+
+def unpack_tiles(img, packed, tiles: Sequence[int], g: int) -> None:
+    n = img.shape[0]
+    d0 = n // g
+    for i, k in enumerate(tiles):
+        gy, gx = divmod(int(k), g)
+        img[gy * d0:(gy + 1) * d0, gx * d0:(gx + 1) * d0].copy_(packed[i])
+
+
+def gather_image(img, parts: Sequence[Sequence[int]], g: int, rank: int, dst: int = 0):
+    """Assemble the full image on rank `dst` from every rank's tiles (verification only, not
+    on the timed path).  `parts[r]` are rank r's tiles; `img` is this rank's n x n buffer
+    (only its own tiles are meaningful).  Returns the assembled image on dst, None elsewhere."""
+    import torch
+    dist = _dist()
+    world = len(parts)
+    mine = pack_tiles(img, parts[rank], g)
+    if world == 1:
+        return img
+    if rank != dst:
+        if len(parts[rank]):
+            dist.send(mine.reshape(-1), dst)
+        return None
+    full = img
+    unpack_tiles(full, mine, parts[rank], g)
+    d0 = img.shape[0] // g
+    bufs, ops = {}, []
+    for r in range(world):
+        if r == dst or not len(parts[r]):
+            continue
+        bufs[r] = torch.empty(len(parts[r]) * d0 * d0, dtype=img.dtype, device=img.device)
+        ops.append(dist.P2POp(dist.irecv, bufs[r], r))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    for r, b in bufs.items():
+        unpack_tiles(full, b.reshape(len(parts[r]), d0, d0), parts[r], g)
+    return full

@@ -1,0 +1,93 @@
+"""N > 1 host logic on CPU (gloo, world size 2): the level-0 tile deal, MAX/SUM reductions
+and the verification gather of paper_2206_02255_b200.multigpu.  Each rank's tile image comes
+from the oracle (CPU), so the data path of the CUDA kernels is not involved here; the GPU
+parity tests cover mandel_ask_tiles itself."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import workloads as W
+from paper_2206_02255_b200 import deal, multigpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("method", ["cyclic", "diagonal", "costrank"])
+@pytest.mark.parametrize("g,world", [(16, 2), (16, 8), (4, 3), (8, 8), (2, 8)])
+def test_deal_partitions(method, g, world):
+    rng = np.random.default_rng(W.SEED)
+    costs = rng.pareto(1.5, g * g).tolist() if method == "costrank" else None
+    parts = deal.deal(method, g, world, costs)
+    assert len(parts) == world
+    flat = sorted(k for p in parts for k in p)
+    assert flat == list(range(g * g))                       # disjoint and complete
+    sizes = [len(p) for p in parts]
+    assert max(sizes) - min(sizes) <= 1 or method == "diagonal"
+
+
+def test_costrank_balances_skewed_costs():
+    # the survey's point: column-striped cyclic dealing is unbalanced on a
+    # tile-cost map with a heavy column; cost-ranked boustrophedon dealing is not.
+    g, world = 16, 8
+    costs = np.ones((g, g))
+    costs[:, 5] = 40.0
+    costs = costs.ravel().tolist()
+    cyc = deal.imbalance(deal.cyclic(g, world), costs)
+    cr = deal.imbalance(deal.costrank(costs, world), costs)
+    assert cyc > 2.0 and cr < 1.1
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, md, g, r, B = 256, 400, 8, 2, 8
+        region = W.SEAHORSE_REGION
+        # every rank must derive the same deal: identical (synthetic) per-tile costs
+        costs = [float(k % 7 + 1) for k in range(g * g)]
+        parts = deal.deal("costrank", g, world, costs)
+        mine = multigpu.rank_tiles("costrank", g, world, rank, costs)
+        assert mine == parts[rank]
+        img, _ = oracle.ask(region, n, md, g, r, B, tiles=mine)
+        full = multigpu.gather_image(torch.from_numpy(img), parts, g, rank)
+        tmax = multigpu.max_over_ranks(10.0 + rank)
+        tsum = multigpu.sum_over_ranks([1.0, float(rank)])
+        if rank == 0:
+            ref, _ = oracle.ask(region, n, md, g, r, B)
+            q.put(("ok", bool(np.array_equal(full.numpy(), ref)), tmax, tsum))
+        else:
+            q.put(("ok", full is None, tmax, tsum))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put(("err", repr(e), None, None))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gather_and_reductions_world2():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for status, ok, tmax, tsum in res:
+        assert status == "ok", ok
+        assert ok is True
+        assert tmax == 11.0
+        assert tsum == [2.0, 1.0]
