@@ -102,6 +102,8 @@ enum {
 #define MANDEL_FLAG_FLAT 8u      /* B200 scheme: plain one-thread-per-pixel border and leaf
                                     kernels instead of the lane-refill ones (A/B baseline;
                                     same image)                                            */
+#define MANDEL_FLAG_SERIAL 16u   /* run every fill on the main stream after its level instead
+                                    of as a concurrent graph branch (A/B; same image)       */
 
 /* Kernel kinds reported by mandel_ask_kernel_times (value = kind * 100 + level). */
 enum {

@@ -73,11 +73,13 @@ def exhaustive(region: Sequence[float], n: int, maxdwell: int, out=None, stream=
 
 def ask(region: Sequence[float], n: int, maxdwell: int, g: int, r: int, B: int, out=None, ws=None,
         tiles: Optional[Sequence[int]] = None, scheme: str = "b200", stats: bool = False,
-        timing: bool = False, tile_cost: bool = False, flat: bool = False, stream=None):
+        timing: bool = False, tile_cost: bool = False, flat: bool = False, serial: bool = False,
+        stream=None):
     """ASK dwell image over all g*g level-0 regions, or only `tiles`.
     stats: accumulate per-level counters (ask_stats); timing: per-kernel events
     (kernel_times); flat: B200 scheme with the plain thread-per-pixel border/leaf kernels
-    instead of the lane-refill ones (A/B comparison, same image)."""
+    instead of the lane-refill ones; serial: fills on the main stream instead of concurrent
+    graph branches (A/B comparisons, same image)."""
     out = _image(n, out)
     if ws is None:
         ws = workspace(n, g, r, B, device=out.device)
@@ -86,7 +88,8 @@ def ask(region: Sequence[float], n: int, maxdwell: int, g: int, r: int, B: int, 
                                       SCHEMES[scheme],
                                       (_lib.FLAG_STATS if stats else 0) | (_lib.FLAG_TIMING if timing else 0)
                                       | (_lib.FLAG_TILE_COST if tile_cost else 0)
-                                      | (_lib.FLAG_FLAT if flat else 0),
+                                      | (_lib.FLAG_FLAT if flat else 0)
+                                      | (_lib.FLAG_SERIAL if serial else 0),
                                       out.data_ptr(), out.stride(0), ws.data_ptr(), ws.numel(),
                                       _stream_ptr(stream))
     _lib.check(rc, "mandel_ask_tiles")

@@ -22,6 +22,7 @@ FLAG_STATS = 1
 FLAG_TIMING = 2
 FLAG_TILE_COST = 4
 FLAG_FLAT = 8
+FLAG_SERIAL = 16
 KIND_NAMES = {0: "init", 1: "b200_border", 2: "b200_classify", 3: "fill", 4: "b200_leaf",
               5: "sbr_level", 6: "sbr_leaf"}
 

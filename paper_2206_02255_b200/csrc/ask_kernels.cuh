@@ -18,18 +18,32 @@ namespace mandel {
 constexpr int MAXL = 32;
 constexpr uint32_t WS_MAGIC = 0x4d41534bu; // "MASK"
 constexpr int DWELL_K = 8;                 // iterations per escape test (dwell.cuh)
-#ifndef MANDEL_RF_K
-#define MANDEL_RF_K 16
+// Lane-refill knobs (refill.cuh), tuned on B200 at C3/C5 (profiles/r01_tune_refill*.txt):
+// K iterations per escape test, T parked lanes that trigger a warp refill, CH indices a warp
+// grabs per cursor atomic; separately for the border (short, level-synchronous launches:
+// smaller grabs balance better) and leaf kernels.
+#ifndef MANDEL_RFB_K
+#define MANDEL_RFB_K 16
 #endif
-#ifndef MANDEL_RF_T
-#define MANDEL_RF_T 8
+#ifndef MANDEL_RFB_T
+#define MANDEL_RFB_T 4
 #endif
-#ifndef MANDEL_RF_CH
-#define MANDEL_RF_CH 128
+#ifndef MANDEL_RFB_CH
+#define MANDEL_RFB_CH 64
 #endif
-constexpr int RF_K = MANDEL_RF_K;   // lane-refill chunk (iterations per escape test)
-constexpr int RF_T = MANDEL_RF_T;   // frozen lanes that trigger a warp refill
-constexpr int RF_CH = MANDEL_RF_CH; // indices a warp grabs per cursor atomic
+#ifndef MANDEL_RFL_K
+#define MANDEL_RFL_K 32
+#endif
+#ifndef MANDEL_RFL_T
+#define MANDEL_RFL_T 4
+#endif
+#ifndef MANDEL_RFL_CH
+#define MANDEL_RFL_CH 128
+#endif
+#ifndef MANDEL_RF_MINB
+#define MANDEL_RF_MINB 6
+#endif
+constexpr int RF_MINB = MANDEL_RF_MINB; // resident 256-thread blocks per SM (register cap)
 
 struct WsHeader {
     uint32_t magic, levels, n, g, r, B, ntiles, scheme; // written by k_init
@@ -96,6 +110,7 @@ struct LevelArgs {
     int *colT;               // NULL: classify reads columns from the image
     int u_log2;
     long long colT_pitch;    // = n
+    FastDiv fd[4];           // lane-refill index maps (host-computed divisors)
 };
 
 __device__ __forceinline__ bool on_col_line(const LevelArgs &a, int x)
@@ -490,30 +505,16 @@ __global__ void __launch_bounds__(256) k_b200_leaf(LevelArgs a)
 // same flat index spaces as k_b200_border / k_b200_leaf, computed by persistent warps whose
 // lanes take a new pixel as soon as theirs is done.
 
-// 32-bit fast path for the index split t -> (unit, local) when t < 2^32.
-__device__ __forceinline__ void split_index(unsigned long long t, uint32_t per, uint32_t &p, uint32_t &loc)
-{
-    if ((t >> 32) == 0ull) {
-        const uint32_t t32 = (uint32_t)t;
-        p = t32 / per;
-        loc = t32 - p * per;
-    } else {
-        p = (uint32_t)(t / per);
-        loc = (uint32_t)(t - (unsigned long long)p * per);
-    }
-}
-
 // Leaf interiors: t = leaf * (d-2)^2 + row-major interior offset.
 struct LeafMap {
     const uint32_t *leaf;
-    uint32_t m, I; // m = d - 2, I = m * m
-    __device__ __forceinline__ void operator()(unsigned long long t, int &x, int &y) const
+    FastDiv fI, fm; // I = (d-2)^2, m = d-2
+    __device__ __forceinline__ void operator()(uint32_t t, int &x, int &y) const
     {
-        uint32_t li, loc;
-        split_index(t, I, li, loc);
+        const uint32_t li = fdiv(t, fI), loc = t - li * fI.d;
         const uint32_t off = leaf[li];
-        const uint32_t row = loc / m;
-        x = unpack_x(off) + 1 + (int)(loc - row * m);
+        const uint32_t row = fdiv(loc, fm);
+        x = unpack_x(off) + 1 + (int)(loc - row * fm.d);
         y = unpack_y(off) + 1 + (int)row;
     }
 };
@@ -522,11 +523,10 @@ struct LeafMap {
 struct BorderMap {
     const uint32_t *olt;
     int level, d, r, D;
-    uint32_t per;
-    __device__ __forceinline__ void operator()(unsigned long long t, int &x, int &y) const
+    FastDiv fper, fcol, fseg, flen; // per, D-2, d-2, r*(d-2)
+    __device__ __forceinline__ void operator()(uint32_t t, int &x, int &y) const
     {
-        uint32_t p, loc;
-        split_index(t, per, p, loc);
+        const uint32_t p = fdiv(t, fper), loc = t - p * fper.d;
         if (level == 0) {
             const uint32_t off = olt[p];
             ring_pixel((int)loc, d, unpack_x(off), unpack_y(off), x, y);
@@ -534,15 +534,15 @@ struct BorderMap {
         }
         const uint32_t off = olt[(size_t)p * (uint32_t)(r * r)]; // first child = parent origin
         const int x0 = unpack_x(off), y0 = unpack_y(off);
-        const uint32_t pv = (uint32_t)(2 * (r - 1) * (D - 2));
+        const uint32_t pv = (uint32_t)(2 * (r - 1)) * fcol.d;
         if (loc < pv) {
-            const uint32_t line = loc / (uint32_t)(D - 2), row = loc - line * (uint32_t)(D - 2);
+            const uint32_t line = fdiv(loc, fcol), row = loc - line * fcol.d;
             x = x0 + ((int)line / 2 + 1) * d - 1 + (int)(line & 1);
             y = y0 + 1 + (int)row;
         } else {
-            const uint32_t h = loc - pv, seg = (uint32_t)(d - 2), len = (uint32_t)r * seg;
-            const uint32_t line = h / len, c = h - line * len;
-            const uint32_t k = c / seg, o = c - k * seg;
+            const uint32_t h = loc - pv;
+            const uint32_t line = fdiv(h, flen), c = h - line * flen.d;
+            const uint32_t k = fdiv(c, fseg), o = c - k * fseg.d;
             y = y0 + ((int)line / 2 + 1) * d - 1 + (int)(line & 1);
             x = x0 + (int)k * d + 1 + (int)o;
         }
@@ -583,40 +583,43 @@ __device__ __forceinline__ void sink_flush(const StoreSink<STATS, RING> &sk, uns
 }
 
 template <bool STATS>
-__global__ void __launch_bounds__(256) k_b200_border_rf(LevelArgs a)
+__global__ void __launch_bounds__(256, RF_MINB) k_b200_border_rf(LevelArgs a)
 {
+    __shared__ ParkedPoint s_q[8][RF_QCAP];
     BorderMap map;
     map.olt = a.olt_in;
     map.level = a.level;
     map.d = a.d;
     map.r = a.r;
     map.D = a.d * a.r;
-    unsigned long long total;
-    if (a.level == 0) {
-        map.per = (uint32_t)(4 * a.d - 4);
-        total = (unsigned long long)map.per * (unsigned long long)a.ntiles;
-    } else {
-        map.per = new_border_px_per_parent(map.D, a.r);
-        total = (unsigned long long)map.per *
-                (unsigned long long)(*((volatile uint32_t *)&a.hdr->n_subdiv[a.level - 1]));
-    }
+    map.fper = a.fd[0];
+    map.fcol = a.fd[1];
+    map.fseg = a.fd[2];
+    map.flen = a.fd[3];
+    uint32_t count = (a.level == 0) ? (uint32_t)a.ntiles
+                                    : *((volatile uint32_t *)&a.hdr->n_subdiv[a.level - 1]);
+    const uint32_t total = map.fper.d * count;
     StoreSink<STATS, true> sink{&a, 0ull, 0ull};
-    refill_loop<RF_K, RF_T, RF_CH>(a.map, a.maxdwell, total, &a.hdr->cursor[a.level], map, sink);
+    refill_loop<MANDEL_RFB_K, MANDEL_RFB_T, MANDEL_RFB_CH>(a.map, a.maxdwell, total, &a.hdr->cursor[a.level],
+                                                           map, sink,
+                                   s_q[threadIdx.x >> 5]);
     sink_flush<STATS, true>(sink, &a.hdr->border_iters[a.level], &a.hdr->border_px[a.level]);
 }
 
 template <bool STATS>
-__global__ void __launch_bounds__(256) k_b200_leaf_rf(LevelArgs a)
+__global__ void __launch_bounds__(256, RF_MINB) k_b200_leaf_rf(LevelArgs a)
 {
+    __shared__ ParkedPoint s_q[8][RF_QCAP];
     LeafMap map;
     map.leaf = a.leaf;
-    map.m = (uint32_t)(a.d - 2);
-    map.I = map.m * map.m;
-    const unsigned long long total =
-        (unsigned long long)map.I * (unsigned long long)(*((volatile uint32_t *)&a.hdr->n_leaf));
+    map.fI = a.fd[0];
+    map.fm = a.fd[1];
+    const uint32_t total = map.fI.d * *((volatile uint32_t *)&a.hdr->n_leaf);
     StoreSink<STATS, false> sink{&a, 0ull, 0ull};
-    if (map.I > 0)
-        refill_loop<RF_K, RF_T, RF_CH>(a.map, a.maxdwell, total, &a.hdr->cursor[MAXL], map, sink);
+    if (map.fI.d > 0)
+        refill_loop<MANDEL_RFL_K, MANDEL_RFL_T, MANDEL_RFL_CH>(a.map, a.maxdwell, total, &a.hdr->cursor[MAXL],
+                                                               map, sink,
+                                       s_q[threadIdx.x >> 5]);
     sink_flush<STATS, false>(sink, &a.hdr->leaf_iters, &a.hdr->leaf_px);
 }
 

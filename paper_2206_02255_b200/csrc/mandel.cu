@@ -120,6 +120,16 @@ bool make_layout(int64_t n, int32_t g, int32_t r, int32_t B, Layout &lay)
     return true;
 }
 
+// FastDiv for a divisor that may be 0 (then the map is never evaluated: d.d = 0 marks it).
+FastDiv fastdiv_nz(uint32_t d)
+{
+    if (d == 0) {
+        FastDiv f{0u, 0u, 0u, 0u};
+        return f;
+    }
+    return make_fastdiv(d);
+}
+
 PixMap make_map(const mandel_region &reg, int64_t n)
 {
     PixMap m;
@@ -132,7 +142,9 @@ PixMap make_map(const mandel_region &reg, int64_t n)
 
 struct DevInfo {
     int sms = 0;
-    cudaStream_t cap = nullptr;
+    cudaStream_t cap = nullptr;  // capture origin stream
+    cudaStream_t side = nullptr; // capture side stream (fill branches)
+    cudaEvent_t fork = nullptr;  // fork/join event used during capture
 };
 
 struct Key {
@@ -159,7 +171,7 @@ struct Entry {
     int32_t *h_tiles = nullptr; // pinned, mapped (read by k_init through UVA)
     unsigned long long last_use = 0;
     std::vector<cudaEvent_t> evs; // MANDEL_FLAG_TIMING only
-    std::vector<int32_t> kinds;
+    std::vector<int32_t> kinds, t_start, t_end;
     unsigned long long id = 0;
 };
 
@@ -177,6 +189,8 @@ int dev_info(int dev, DevInfo *&out)
     if (!di.cap) {
         CK(cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev));
         CK(cudaStreamCreateWithFlags(&di.cap, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&di.side, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&di.fork, cudaEventDisableTiming));
     }
     out = &di;
     return MANDEL_OK;
@@ -195,37 +209,63 @@ int resident_grid(K kernel, int tpb, int sms, size_t cap_blocks)
 }
 
 // Per-kernel timing inside the graph (MANDEL_FLAG_TIMING): an external event-record node
-// before the first kernel and after every kernel.
+// on the kernel's own stream right before and right after every kernel.
 struct Timing {
     bool on = false;
-    std::vector<cudaEvent_t> evs;
-    std::vector<int32_t> kinds; // kind * 100 + level, one per kernel
+    std::vector<cudaEvent_t> evs;        // all events (owned by the cache entry)
+    std::vector<int32_t> start, end;     // per kernel: indices into evs
+    std::vector<int32_t> kinds;          // per kernel: kind * 100 + level
+    int32_t open = -1;
 };
 
-int mark(Timing *tm, int kind, int level, cudaStream_t s)
+int t_begin(Timing *tm, cudaStream_t st)
 {
     if (!tm || !tm->on)
         return MANDEL_OK;
     cudaEvent_t ev;
     CK(cudaEventCreate(&ev));
+    tm->open = (int32_t)tm->evs.size();
     tm->evs.push_back(ev);
-    if (kind >= 0)
-        tm->kinds.push_back(kind * 100 + level);
-    CK(cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal));
+    CK(cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal));
     return MANDEL_OK;
 }
 
-#define MARK(kind, level)                                                                      \
+int t_end(Timing *tm, int kind, int level, cudaStream_t st)
+{
+    if (!tm || !tm->on)
+        return MANDEL_OK;
+    cudaEvent_t ev;
+    CK(cudaEventCreate(&ev));
+    tm->start.push_back(tm->open);
+    tm->end.push_back((int32_t)tm->evs.size());
+    tm->kinds.push_back(kind * 100 + level);
+    tm->evs.push_back(ev);
+    CK(cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal));
+    return MANDEL_OK;
+}
+
+#define TBEGIN(st)                                                                             \
     do {                                                                                       \
-        int m_ = mark(tm, (kind), (level), s);                                                 \
+        int m_ = t_begin(tm, (st));                                                            \
+        if (m_)                                                                                \
+            return m_;                                                                         \
+    } while (0)
+#define TEND(kind, level, st)                                                                  \
+    do {                                                                                       \
+        int m_ = t_end(tm, (kind), (level), (st));                                             \
         if (m_)                                                                                \
             return m_;                                                                         \
     } while (0)
 
 // Enqueue the whole ASK call on `s` (called under stream capture).
+// Fills (HBM-bound) run on the side stream s2 as graph branches forked after each level's
+// classification and joined at the end, overlapping the ALU-bound dwell kernels; a fill
+// writes only the interior of regions that are terminal, which no later kernel reads.
 int enqueue_ask(const Key &k, const Layout &lay, const int32_t *d_tiles_visible, int ntiles, int sms,
-                cudaStream_t s, Timing *tm)
+                cudaStream_t s, cudaStream_t s2, cudaEvent_t fork, Timing *tm)
 {
+    const bool overlap = (k.flags & MANDEL_FLAG_SERIAL) == 0;
+    cudaStream_t sf = overlap ? s2 : s; // stream of the fill kernels
     char *ws = (char *)k.ws;
     LevelArgs a;
     memset(&a, 0, sizeof a);
@@ -262,10 +302,10 @@ int enqueue_ask(const Key &k, const Layout &lay, const int32_t *d_tiles_visible,
         int nthr = ntiles > 1024 ? ntiles : 1024;
         if (nthr < k.g * k.g)
             nthr = k.g * k.g;
-        MARK(-1, 0);
+        TBEGIN(s);
         k_init<<<(nthr + 255) / 256, 256, 0, s>>>(a);
         CK(cudaGetLastError());
-        MARK(MANDEL_KIND_INIT, 0);
+        TEND(MANDEL_KIND_INIT, 0, s);
     }
     int d = d0;
     for (int l = 0; l < lay.L; ++l) {
@@ -291,6 +331,7 @@ int enqueue_ask(const Key &k, const Layout &lay, const int32_t *d_tiles_visible,
             k_sbr_level<TPB, false><<<gsz, TPB, 0, s>>>(a);                                     \
         }                                                                                      \
     } while (0)
+            TBEGIN(s);
             if (ring >= 256)
                 SBR_LAUNCH(256);
             else if (ring >= 128)
@@ -301,11 +342,12 @@ int enqueue_ask(const Key &k, const Layout &lay, const int32_t *d_tiles_visible,
                 SBR_LAUNCH(32);
 #undef SBR_LAUNCH
             CK(cudaGetLastError());
-            MARK(MANDEL_KIND_SBR_LEVEL, l);
+            TEND(MANDEL_KIND_SBR_LEVEL, l, s);
         } else {
             size_t work = (l == 0) ? cap * (size_t)(4 * d - 4)
                                    : (cap / ((size_t)k.r * k.r)) * new_border_px_per_parent(d * k.r, k.r);
             size_t blocks = (work + 255) / 256;
+            TBEGIN(s);
             if (flat) {
                 if (stats) {
                     int gsz = resident_grid(k_b200_border<true>, 256, sms, blocks);
@@ -316,6 +358,11 @@ int enqueue_ask(const Key &k, const Layout &lay, const int32_t *d_tiles_visible,
                 }
             } else { // lane refill: persistent warps, one per 32 pixels of work at most
                 const size_t rf_blocks = (work + 255) / 256;
+                const uint32_t per = (l == 0) ? (uint32_t)(4 * d - 4) : new_border_px_per_parent(d * k.r, k.r);
+                a.fd[0] = fastdiv_nz(per);
+                a.fd[1] = fastdiv_nz((uint32_t)(d * k.r - 2));
+                a.fd[2] = fastdiv_nz((uint32_t)(d - 2));
+                a.fd[3] = fastdiv_nz((uint32_t)(k.r * (d - 2)));
                 if (stats) {
                     int gsz = resident_grid(k_b200_border_rf<true>, 256, sms, rf_blocks);
                     k_b200_border_rf<true><<<gsz, 256, 0, s>>>(a);
@@ -325,11 +372,12 @@ int enqueue_ask(const Key &k, const Layout &lay, const int32_t *d_tiles_visible,
                 }
             }
             CK(cudaGetLastError());
-            MARK(MANDEL_KIND_B200_BORDER, l);
+            TEND(MANDEL_KIND_B200_BORDER, l, s);
             int gsz = resident_grid(k_b200_classify, 256, sms, (cap + 7) / 8);
+            TBEGIN(s);
             k_b200_classify<<<gsz, 256, 0, s>>>(a);
             CK(cudaGetLastError());
-            MARK(MANDEL_KIND_B200_CLASSIFY, l);
+            TEND(MANDEL_KIND_B200_CLASSIFY, l, s);
         }
         // fill (terminal work) of this level's uniform regions
         {
@@ -338,15 +386,20 @@ int enqueue_ask(const Key &k, const Layout &lay, const int32_t *d_tiles_visible,
             a.log2_row4 = vec ? ilog2(d / 4) : 0;
             size_t work = cap * (size_t)d * d / (vec ? 4 : 1);
             size_t blocks = (work + 255) / 256;
+            if (overlap) { // fork: the fill of level l waits only for its classification
+                CK(cudaEventRecord(fork, s));
+                CK(cudaStreamWaitEvent(sf, fork, 0));
+            }
+            TBEGIN(sf);
             if (vec) {
                 int gsz = resident_grid(k_fill<true>, 256, sms, blocks);
-                k_fill<true><<<gsz, 256, 0, s>>>(a);
+                k_fill<true><<<gsz, 256, 0, sf>>>(a);
             } else {
                 int gsz = resident_grid(k_fill<false>, 256, sms, blocks);
-                k_fill<false><<<gsz, 256, 0, s>>>(a);
+                k_fill<false><<<gsz, 256, 0, sf>>>(a);
             }
             CK(cudaGetLastError());
-            MARK(MANDEL_KIND_FILL, l);
+            TEND(MANDEL_KIND_FILL, l, sf);
         }
         if (l + 1 < lay.L)
             d /= k.r;
@@ -358,6 +411,7 @@ int enqueue_ask(const Key &k, const Layout &lay, const int32_t *d_tiles_visible,
         size_t cap = (size_t)ntiles;
         for (int i = 0; i < lay.L - 1; ++i)
             cap *= (size_t)k.r * k.r;
+        TBEGIN(s);
         if (k.scheme == MANDEL_SCHEME_SBR) {
             const int I = (d - 2) * (d - 2);
 #define LEAF_LAUNCH(TPB)                                                                       \
@@ -390,6 +444,8 @@ int enqueue_ask(const Key &k, const Layout &lay, const int32_t *d_tiles_visible,
                     k_b200_leaf<false><<<gsz, 256, 0, s>>>(a);
                 }
             } else {
+                a.fd[0] = fastdiv_nz((uint32_t)((d - 2) * (d - 2)));
+                a.fd[1] = fastdiv_nz((uint32_t)(d - 2));
                 if (stats) {
                     int gsz = resident_grid(k_b200_leaf_rf<true>, 256, sms, blocks);
                     k_b200_leaf_rf<true><<<gsz, 256, 0, s>>>(a);
@@ -400,7 +456,11 @@ int enqueue_ask(const Key &k, const Layout &lay, const int32_t *d_tiles_visible,
             }
         }
         CK(cudaGetLastError());
-        MARK(k.scheme == MANDEL_SCHEME_SBR ? MANDEL_KIND_SBR_LEAF : MANDEL_KIND_B200_LEAF, lay.L - 1);
+        TEND(k.scheme == MANDEL_SCHEME_SBR ? MANDEL_KIND_SBR_LEAF : MANDEL_KIND_B200_LEAF, lay.L - 1, s);
+    }
+    if (overlap) { // join the fill branches
+        CK(cudaEventRecord(fork, sf));
+        CK(cudaStreamWaitEvent(s, fork, 0));
     }
     return MANDEL_OK;
 }
@@ -479,7 +539,8 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
     if (rc)
         return rc;
     if (!valid_grb(n, g, r, B) || !d_ws || (scheme != MANDEL_SCHEME_SBR && scheme != MANDEL_SCHEME_B200) ||
-        (flags & ~(MANDEL_FLAG_STATS | MANDEL_FLAG_TIMING | MANDEL_FLAG_TILE_COST | MANDEL_FLAG_FLAT)) != 0)
+        (flags & ~(MANDEL_FLAG_STATS | MANDEL_FLAG_TIMING | MANDEL_FLAG_TILE_COST | MANDEL_FLAG_FLAT |
+                   MANDEL_FLAG_SERIAL)) != 0)
         return MANDEL_EINVAL;
     Layout lay;
     if (!make_layout(n, g, r, B, lay))
@@ -550,9 +611,11 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
         }
         Timing tm;
         tm.on = (flags & MANDEL_FLAG_TIMING) != 0;
-        int erc = enqueue_ask(key, lay, d_tiles, ntiles, di->sms, di->cap, &tm);
+        int erc = enqueue_ask(key, lay, d_tiles, ntiles, di->sms, di->cap, di->side, di->fork, &tm);
         e.evs = tm.evs;
         e.kinds = tm.kinds;
+        e.t_start = tm.start;
+        e.t_end = tm.end;
         e.id = ++g_next_id;
         ce = cudaStreamEndCapture(di->cap, &graph);
         if (erc || ce != cudaSuccess) {
@@ -586,11 +649,13 @@ int mandel_ask_kernel_times(float *ms, int32_t *kind_level, int32_t max_kernels)
             hit = &e;
     if (!hit)
         return -MANDEL_EINVAL;
-    CK(cudaEventSynchronize(hit->evs.back()));
+    for (auto ev : hit->evs)
+        CK(cudaEventSynchronize(ev));
     const int nk = (int)hit->kinds.size();
     for (int i = 0; i < nk && i < max_kernels; ++i) {
         float t = 0.0f;
-        CK(cudaEventElapsedTime(&t, hit->evs[(size_t)i], hit->evs[(size_t)i + 1]));
+        CK(cudaEventElapsedTime(&t, hit->evs[(size_t)hit->t_start[(size_t)i]],
+                                hit->evs[(size_t)hit->t_end[(size_t)i]]));
         if (ms)
             ms[i] = t;
         if (kind_level)
@@ -705,9 +770,14 @@ void mandel_shutdown(void)
     for (auto &e : g_cache)
         free_entry(e);
     g_cache.clear();
-    for (auto &d : g_dev)
+    for (auto &d : g_dev) {
         if (d.cap)
             cudaStreamDestroy(d.cap);
+        if (d.side)
+            cudaStreamDestroy(d.side);
+        if (d.fork)
+            cudaEventDestroy(d.fork);
+    }
     g_dev.clear();
 }
 

@@ -100,7 +100,7 @@ def test_validation_before_any_launch(lib):
     t = (ctypes.c_int32 * 1)(16)
     assert lib.mandel_ask_tiles(*args, ctypes.cast(t, ctypes.c_void_p), 1, 1, 0, fake, 64, fake, ws_need, None) == 1
     assert lib.mandel_ask_tiles(*args, None, 0, 7, 0, fake, 64, fake, ws_need, None) == 1
-    assert lib.mandel_ask_tiles(*args, None, 0, 1, 16, fake, 64, fake, ws_need, None) == 1
+    assert lib.mandel_ask_tiles(*args, None, 0, 1, 32, fake, 64, fake, ws_need, None) == 1
     assert lib.mandel_strerror(2) == b"workspace too small"
 
 

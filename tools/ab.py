@@ -17,14 +17,15 @@ import torch
 import paper_2206_02255_b200 as mb
 import workloads as W
 
-VARIANTS = {"b200": dict(scheme="b200"), "flat": dict(scheme="b200", flat=True), "sbr": dict(scheme="sbr")}
+VARIANTS = {"b200": dict(scheme="b200"), "flat": dict(scheme="b200", flat=True), "sbr": dict(scheme="sbr"),
+            "serial": dict(scheme="b200", serial=True), "sbr_serial": dict(scheme="sbr", serial=True)}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("workloads", nargs="*", default=["C3", "C5"])
     ap.add_argument("--reps", type=int, default=5)
-    ap.add_argument("--variants", default="b200,flat,sbr")
+    ap.add_argument("--variants", default="b200,serial,flat,sbr")
     ap.add_argument("--ex", action="store_true")
     a = ap.parse_args()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -63,7 +64,18 @@ def main():
                 ts.append(s.elapsed_time(e))
                 for k in mb.kernel_times():
                     kt[k["kind"]] = kt.get(k["kind"], 0.0) + k["ms"] / a.reps
+            tn = []
+            mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, **kw)  # capture this graph
+            torch.cuda.synchronize()
+            for _ in range(a.reps):
+                flush.zero_()
+                s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+                s.record()
+                mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, **kw)
+                e.record(); e.synchronize()
+                tn.append(s.elapsed_time(e))
             res[v] = {"ms_mean": sum(ts) / len(ts), "ms_min": min(ts), "iters": iters,
+                      "ms_notiming_mean": sum(tn) / len(tn),
                       "giter_s_exec": iters / (min(ts) / 1e3) / 1e9, "same_image": same,
                       "kernels": {k: round(x, 4) for k, x in kt.items()}}
         print(json.dumps(res), flush=True)

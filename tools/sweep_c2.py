@@ -1,0 +1,121 @@
+"""BASELINE.json config 2: the {g, r, B} sweep at n=8192, maxdwell=2048 on one B200, against
+the paper's cost model (costmodel.py).
+
+    python tools/sweep_c2.py [--reps 3] [--scheme b200] [--out gpurun_out/sweep_c2.json]
+
+Per point (60, g in {2..32}, r in {2,4,8}, B in {16..128}): device time of one mandel_ask
+graph launch (min over reps, L2 flushed between), level statistics and executed iterations.
+Calibration (c-6 protocol, never fitted to the sweep it predicts): t_unit from the exhaustive
+run alone; P(r) = r^(D-2) with D fitted from the g16 r2 B32 reference run's region counts;
+lambda solved from that run's time.  Then the other 59 points are predicted and the report
+gives the predicted and measured argmin, the regret, Spearman rho and the top-5 overlap,
+for both tau conventions (R5).
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+from paper_2206_02255_b200 import costmodel as cm  # noqa: E402
+
+
+def time_ms(fn, flush, reps):
+    import torch
+    fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+        s.record()
+        fn()
+        e.record()
+        e.synchronize()
+        ts.append(s.elapsed_time(e))
+    return min(ts)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--scheme", default="b200")
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "sweep_c2.json"))
+    ap.add_argument("--from-json", help="re-run the model analysis on a saved sweep (no GPU)")
+    a = ap.parse_args()
+    if a.from_json:
+        rep = json.load(open(a.from_json))
+        rep.setdefault("sum_dwell_ex", 52356729130 if rep["n"] == 8192 and rep["maxdwell"] == 2048 else None)
+        analyse(rep)
+        with open(a.out, "w") as f:
+            json.dump(rep, f, indent=1, default=str)
+        return
+    import torch
+    import paper_2206_02255_b200 as mb
+    n, md = W.C2_N, W.C2_MAXDWELL
+    region = W.DEFAULT_REGION
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    out = torch.empty((n, n), dtype=torch.int32, device="cuda")
+    t_ex = time_ms(lambda: mb.exhaustive(region, n, md, out=out), flush, a.reps)
+    ex_img = out.clone()
+    sum_dwell = int(ex_img.sum(dtype=torch.int64).item())
+    pts = []
+    for w in W.c2_sweep():
+        ws = mb.workspace(n, w.g, w.r, w.B)
+        t = time_ms(lambda: mb.ask(region, n, md, w.g, w.r, w.B, out=out, ws=ws, scheme=a.scheme), flush, a.reps)
+        mb.ask(region, n, md, w.g, w.r, w.B, out=out, ws=ws, scheme=a.scheme, stats=True)
+        st = mb.ask_stats(ws)
+        st = [s for s in st if s["regions_in"] > 0]
+        mism = int((out != ex_img).sum().item())
+        pts.append({"g": w.g, "r": w.r, "B": w.B, "ms": t, "levels": len(st),
+                    "regions": [s["regions_in"] for s in st],
+                    "iters": sum(s["border_iters"] + s["leaf_iters"] for s in st),
+                    "mismatch_vs_ex": mism / (n * n)})
+        print(json.dumps(pts[-1]), flush=True)
+        del ws
+    report = {"n": n, "maxdwell": md, "scheme": a.scheme, "t_ex_ms": t_ex, "sum_dwell_ex": sum_dwell,
+              "points": pts}
+    analyse(report)
+    os.makedirs(os.path.dirname(a.out), exist_ok=True)
+    with open(a.out, "w") as f:
+        json.dump(report, f, indent=1, default=str)
+
+
+def analyse(report):
+    """Calibrate on the g16 r2 B32 reference point and predict the rest, for both tau
+    conventions (R5) and two readings of the application work A ("A ...
+    corresponds to the dwell"): maxdwell (literal) and the measured mean dwell of Ex."""
+    n, md, t_ex, pts = report["n"], report["maxdwell"], report["t_ex_ms"], report["points"]
+    ref = next(p for p in pts if (p["g"], p["r"], p["B"]) == (16, 2, 32))
+    meas = {(p["g"], p["r"], p["B"]): p["ms"] for p in pts}
+    best_meas = min(meas, key=meas.get)
+    report["model"] = {}
+    A_modes = {"A=maxdwell": float(md)}
+    if report.get("sum_dwell_ex"):
+        A_modes["A=mean_dwell"] = report["sum_dwell_ex"] / float(n * n)
+    for a_name, A in A_modes.items():
+        for tau_mode in ("literal", "leaf"):
+            cal = cm.calibrate(n, A, t_ex / 1e3, (16, 2, 32), ref["regions"], ref["ms"] / 1e3,
+                               tau_mode=tau_mode)
+            pred = {k: 1e3 * cal.predict_time(n, *k) for k in meas}
+            others = [k for k in meas if k != (16, 2, 32)]
+            best_pred = min(others, key=pred.get)
+            top5_m = set(sorted(meas, key=meas.get)[:5])
+            top5_p = set(sorted(others, key=pred.get)[:5])
+            key = f"{a_name},tau={tau_mode}"
+            report["model"][key] = {"A": A,
+                "t_unit_s": cal.t_unit, "D": cal.D, "P(r)": {r: cal.P(r) for r in (2, 4, 8)}, "lambda": cal.lam,
+                "pred_argmin": best_pred, "meas_argmin": best_meas,
+                "regret": meas[best_pred] / meas[best_meas] - 1.0,
+                "spearman": cm.spearman([meas[k] for k in others], [pred[k] for k in others]),
+                "top5_overlap": len(top5_m & top5_p),
+                "pred_ms": {f"{k[0]},{k[1]},{k[2]}": v for k, v in pred.items()}}
+            print(key, json.dumps({k: v for k, v in report["model"][key].items() if k != "pred_ms"}), flush=True)
+    return report
+
+
+if __name__ == "__main__":
+    main()
