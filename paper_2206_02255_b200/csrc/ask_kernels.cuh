@@ -32,10 +32,10 @@ constexpr int DWELL_K = 8;                 // iterations per escape test (dwell.
 #define MANDEL_RFB_CH 64
 #endif
 #ifndef MANDEL_RFL_K
-#define MANDEL_RFL_K 32
+#define MANDEL_RFL_K 16
 #endif
 #ifndef MANDEL_RFL_T
-#define MANDEL_RFL_T 4
+#define MANDEL_RFL_T 8
 #endif
 #ifndef MANDEL_RFL_CH
 #define MANDEL_RFL_CH 128
@@ -51,6 +51,11 @@ struct WsHeader {
     uint32_t n_fill[MAXL];
     uint32_t n_leaf;
     uint32_t pad0;
+    // LPT ordering: subdivided parents / leaves whose ring reached
+    // maxdwell/2 ("hot": likely long pixels) fill their list from the front, the others
+    // ("cold") from the back, so the next kernel hands out hot work first.
+    uint32_t n_sub_hot[MAXL], n_sub_cold[MAXL];
+    uint32_t n_leaf_hot, n_leaf_cold;
     unsigned long long border_px[MAXL], border_iters[MAXL];
     unsigned long long leaf_px, leaf_iters;
     unsigned long long cursor[MAXL + 1]; // lane-refill work cursors: border level l, leaves
@@ -111,7 +116,35 @@ struct LevelArgs {
     int u_log2;
     long long colT_pitch;    // = n
     FastDiv fd[4];           // lane-refill index maps (host-computed divisors)
+    uint32_t capP;           // parent slots of an OLT buffer (= OLT entries / r^2)
+    uint32_t capL;           // leaf list entries
 };
+
+// Hot/cold list addressing: the q-th subdivided parent of level l-1 (q < hot count: front
+// slot q; else back slot capP-1-(q-hot)), the ri-th region of this level, the li-th leaf.
+__device__ __forceinline__ uint32_t sub_hot(const LevelArgs &a)
+{
+    return a.level > 0 ? *((volatile uint32_t *)&a.hdr->n_sub_hot[a.level - 1]) : 0u;
+}
+__device__ __forceinline__ uint32_t parent_slot(const LevelArgs &a, uint32_t q, uint32_t nh)
+{
+    return q < nh ? q : a.capP - 1u - (q - nh);
+}
+__device__ __forceinline__ uint32_t region_origin(const LevelArgs &a, uint32_t ri, uint32_t nh)
+{
+    if (a.level == 0)
+        return a.olt_in[ri];
+    const uint32_t rr = (uint32_t)(a.r * a.r), q = ri / rr;
+    return a.olt_in[(size_t)parent_slot(a, q, nh) * rr + (ri - q * rr)];
+}
+__device__ __forceinline__ uint32_t leaf_hot(const LevelArgs &a)
+{
+    return *((volatile uint32_t *)&a.hdr->n_leaf_hot);
+}
+__device__ __forceinline__ uint32_t leaf_origin(const LevelArgs &a, uint32_t li, uint32_t nh)
+{
+    return a.leaf[li < nh ? li : a.capL - 1u - (li - nh)];
+}
 
 __device__ __forceinline__ bool on_col_line(const LevelArgs &a, int x)
 {
@@ -219,8 +252,9 @@ __global__ void k_init(LevelArgs a)
 // --------------------------------------------------------------------------- decisions
 // Common tail of the per-region decision: uniform -> fill list;
 // non-uniform and d/r >= B -> reserve r^2 consecutive OLT slots with one atomicAdd on the
-// level's count (compact concurrent insertion); else -> leaf list.
-// Returns the reserved base (or UINT_MAX) to the caller's lane/thread.
+// level's count (compact concurrent insertion; hot parents from the front of the
+// buffer, cold ones from the back); else -> leaf list.
+// Returns the reserved parent slot (or UINT_MAX) to the caller's lane/thread.
 __device__ __forceinline__ uint32_t decide(const LevelArgs &a, uint32_t off, int lo, int hi)
 {
     if (lo == hi) {
@@ -228,10 +262,18 @@ __device__ __forceinline__ uint32_t decide(const LevelArgs &a, uint32_t off, int
         a.fill[e] = make_uint2(off, (uint32_t)lo);
         return UINT_MAX;
     }
-    if (a.subdivide)
-        return atomicAdd(&a.hdr->n_subdiv[a.level], 1u);
-    const uint32_t e = atomicAdd(&a.hdr->n_leaf, 1u);
-    a.leaf[e] = off;
+    const bool hot = 2 * hi >= a.maxdwell;
+    if (a.subdivide) {
+        atomicAdd(&a.hdr->n_subdiv[a.level], 1u);
+        if (hot)
+            return atomicAdd(&a.hdr->n_sub_hot[a.level], 1u);
+        return a.capP - 1u - atomicAdd(&a.hdr->n_sub_cold[a.level], 1u);
+    }
+    atomicAdd(&a.hdr->n_leaf, 1u);
+    if (hot)
+        a.leaf[atomicAdd(&a.hdr->n_leaf_hot, 1u)] = off;
+    else
+        a.leaf[a.capL - 1u - atomicAdd(&a.hdr->n_leaf_cold, 1u)] = off;
     return UINT_MAX;
 }
 
@@ -249,8 +291,9 @@ __global__ void __launch_bounds__(TPB) k_sbr_level(LevelArgs a)
     const uint32_t count = level_count(a);
     const int d = a.d, ring = 4 * d - 4, s = d / a.r, rr = a.r * a.r;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const uint32_t nh = sub_hot(a);
     for (uint32_t ri = blockIdx.x; ri < count; ri += gridDim.x) {
-        const uint32_t off = a.olt_in[ri];
+        const uint32_t off = region_origin(a, ri, nh);
         const int x0 = unpack_x(off), y0 = unpack_y(off);
         int lo = INT_MAX, hi = INT_MIN;
         unsigned long long it = 0;
@@ -303,8 +346,9 @@ __global__ void __launch_bounds__(TPB) k_sbr_leaf(LevelArgs a)
     __shared__ unsigned long long s_sum[TPB / 32];
     const uint32_t count = *((volatile uint32_t *)&a.hdr->n_leaf);
     const int d = a.d, m = d - 2, I = m * m;
+    const uint32_t nh = leaf_hot(a);
     for (uint32_t li = blockIdx.x; li < count; li += gridDim.x) {
-        const uint32_t off = a.leaf[li];
+        const uint32_t off = leaf_origin(a, li, nh);
         const int x0 = unpack_x(off) + 1, y0 = unpack_y(off) + 1;
         unsigned long long it = 0;
         for (int p = threadIdx.x; p < I; p += TPB) {
@@ -391,6 +435,7 @@ __global__ void __launch_bounds__(256) k_b200_border(LevelArgs a)
         total = per * (unsigned long long)(*((volatile uint32_t *)&a.hdr->n_subdiv[a.level - 1]));
     }
     const int rr = a.r * a.r;
+    const uint32_t nh = sub_hot(a);
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     unsigned long long it = 0, px = 0;
     for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
@@ -401,7 +446,7 @@ __global__ void __launch_bounds__(256) k_b200_border(LevelArgs a)
             const uint32_t off = a.olt_in[p];
             ring_pixel(loc, d, unpack_x(off), unpack_y(off), x, y);
         } else {
-            const uint32_t off = a.olt_in[(size_t)p * rr]; // first child = parent origin
+            const uint32_t off = a.olt_in[(size_t)parent_slot(a, p, nh) * rr]; // first child = parent origin
             const int x0 = unpack_x(off), y0 = unpack_y(off);
             const int pv = 2 * (a.r - 1) * (D - 2);
             if (loc < pv) {
@@ -434,36 +479,68 @@ __global__ void __launch_bounds__(256) k_b200_border(LevelArgs a)
     }
 }
 
-// Classification, one warp per region: read the region's 4d-4 ring
-// dwells back from the image, reduce (min, max) with warp reductions, decide, and append
-// (children written by the warp's lanes).
+// Classification: read each region's 4d-4 ring dwells back (rows from the
+// image, columns from colT), reduce (min, max) with warp reductions, decide, and append
+// (children written by the region's lanes).  WPR warps per region: one warp for small rings;
+// the whole 256-thread block for large ones (d >= 256, i.e. the first levels, where a warp
+// per region would serialise ~d/8 dependent load rounds).
+template <int WPR>
 __global__ void __launch_bounds__(256) k_b200_classify(LevelArgs a)
 {
+    constexpr int TPR = 32 * WPR; // threads per region
+    __shared__ int s_lo[8], s_hi[8];
+    __shared__ uint32_t s_base[8 / WPR];
     const uint32_t count = level_count(a);
     const int d = a.d, ring = 4 * d - 4, s = d / a.r, rr = a.r * a.r;
-    const int lane = threadIdx.x & 31;
-    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-    for (uint32_t ri = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; ri < count; ri += nw) {
-        const uint32_t off = a.olt_in[ri];
+    const int t = threadIdx.x % TPR, w = threadIdx.x >> 5, slot = threadIdx.x / TPR;
+    const uint32_t per_block = 256 / TPR;
+    const uint32_t nh = sub_hot(a);
+    for (uint32_t ri0 = blockIdx.x * per_block; ri0 < count; ri0 += gridDim.x * per_block) {
+        const uint32_t ri = ri0 + slot;
+        const bool valid = ri < count;
+        const uint32_t off = valid ? region_origin(a, ri, nh) : 0u;
         const int x0 = unpack_x(off), y0 = unpack_y(off);
         int lo = INT_MAX, hi = INT_MIN;
-        for (int b = lane; b < ring; b += 32) {
-            int x, y;
-            ring_pixel(b, d, x0, y0, x, y);
-            const int v = (a.colT && b >= 2 * d) ? __ldcg(a.colT + colT_index(a, x, y))
-                                                 : __ldcg(a.out + (long long)y * a.pitch + x);
-            lo = min(lo, v);
-            hi = max(hi, v);
+        if (valid) {
+#pragma unroll 4
+            for (int b = t; b < ring; b += TPR) {
+                int x, y;
+                ring_pixel(b, d, x0, y0, x, y);
+                const int v = (a.colT && b >= 2 * d) ? __ldcg(a.colT + colT_index(a, x, y))
+                                                     : __ldcg(a.out + (long long)y * a.pitch + x);
+                lo = min(lo, v);
+                hi = max(hi, v);
+            }
         }
         lo = __reduce_min_sync(0xffffffffu, lo);
         hi = __reduce_max_sync(0xffffffffu, hi);
-        uint32_t base = 0;
-        if (lane == 0)
-            base = decide(a, off, lo, hi);
-        base = __shfl_sync(0xffffffffu, base, 0);
+        if (WPR > 1) {
+            if ((threadIdx.x & 31) == 0) {
+                s_lo[w] = lo;
+                s_hi[w] = hi;
+            }
+            __syncthreads();
+            if (t == 0) {
+                for (int k = 1; k < WPR; ++k) {
+                    lo = min(lo, s_lo[k]);
+                    hi = max(hi, s_hi[k]);
+                }
+            }
+        }
+        if (t == 0)
+            s_base[slot] = valid ? decide(a, off, lo, hi) : UINT_MAX;
+        if (WPR > 1)
+            __syncthreads();
+        else
+            __syncwarp();
+        const uint32_t base = s_base[slot];
         if (base != UINT_MAX)
-            for (int t = lane; t < rr; t += 32)
-                a.olt_out[(size_t)base * rr + t] = pack_xy(x0 + (t % a.r) * s, y0 + (t / a.r) * s);
+            for (int c = t; c < rr; c += TPR)
+                a.olt_out[(size_t)base * rr + c] = pack_xy(x0 + (c % a.r) * s, y0 + (c / a.r) * s);
+        if (WPR > 1)
+            __syncthreads();
+        else
+            __syncwarp();
     }
 }
 
@@ -476,11 +553,12 @@ __global__ void __launch_bounds__(256) k_b200_leaf(LevelArgs a)
     const unsigned long long I = (unsigned long long)m * m;
     const unsigned long long total = I * (unsigned long long)(*((volatile uint32_t *)&a.hdr->n_leaf));
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    const uint32_t nh = leaf_hot(a);
     unsigned long long it = 0, px = 0;
     for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
         const uint32_t li = (uint32_t)(t / I);
         const int loc = (int)(t - (unsigned long long)li * I);
-        const uint32_t off = a.leaf[li];
+        const uint32_t off = leaf_origin(a, li, nh);
         const int x = unpack_x(off) + 1 + loc % m, y = unpack_y(off) + 1 + loc / m;
         const int v = dwell<DWELL_K>(pix_re(a.map, x), pix_im(a.map, y), a.maxdwell);
         a.out[(long long)y * a.pitch + x] = v;
@@ -508,11 +586,12 @@ __global__ void __launch_bounds__(256) k_b200_leaf(LevelArgs a)
 // Leaf interiors: t = leaf * (d-2)^2 + row-major interior offset.
 struct LeafMap {
     const uint32_t *leaf;
-    FastDiv fI, fm; // I = (d-2)^2, m = d-2
+    uint32_t nh, capL; // hot leaves at the front, cold ones at the back (leaf_origin)
+    FastDiv fI, fm;    // I = (d-2)^2, m = d-2
     __device__ __forceinline__ void operator()(uint32_t t, int &x, int &y) const
     {
         const uint32_t li = fdiv(t, fI), loc = t - li * fI.d;
-        const uint32_t off = leaf[li];
+        const uint32_t off = leaf[li < nh ? li : capL - 1u - (li - nh)];
         const uint32_t row = fdiv(loc, fm);
         x = unpack_x(off) + 1 + (int)(loc - row * fm.d);
         y = unpack_y(off) + 1 + (int)row;
@@ -522,6 +601,7 @@ struct LeafMap {
 // New border pixels of a level (same enumeration as k_b200_border).
 struct BorderMap {
     const uint32_t *olt;
+    uint32_t nh, capP; // hot parents at the front, cold ones at the back (parent_slot)
     int level, d, r, D;
     FastDiv fper, fcol, fseg, flen; // per, D-2, d-2, r*(d-2)
     __device__ __forceinline__ void operator()(uint32_t t, int &x, int &y) const
@@ -532,7 +612,8 @@ struct BorderMap {
             ring_pixel((int)loc, d, unpack_x(off), unpack_y(off), x, y);
             return;
         }
-        const uint32_t off = olt[(size_t)p * (uint32_t)(r * r)]; // first child = parent origin
+        const uint32_t slot = p < nh ? p : capP - 1u - (p - nh);
+        const uint32_t off = olt[(size_t)slot * (uint32_t)(r * r)]; // first child = parent origin
         const int x0 = unpack_x(off), y0 = unpack_y(off);
         const uint32_t pv = (uint32_t)(2 * (r - 1)) * fcol.d;
         if (loc < pv) {
@@ -588,6 +669,8 @@ __global__ void __launch_bounds__(256, RF_MINB) k_b200_border_rf(LevelArgs a)
     __shared__ ParkedPoint s_q[8][RF_QCAP];
     BorderMap map;
     map.olt = a.olt_in;
+    map.nh = sub_hot(a);
+    map.capP = a.capP;
     map.level = a.level;
     map.d = a.d;
     map.r = a.r;
@@ -612,6 +695,8 @@ __global__ void __launch_bounds__(256, RF_MINB) k_b200_leaf_rf(LevelArgs a)
     __shared__ ParkedPoint s_q[8][RF_QCAP];
     LeafMap map;
     map.leaf = a.leaf;
+    map.nh = leaf_hot(a);
+    map.capL = a.capL;
     map.fI = a.fd[0];
     map.fm = a.fd[1];
     const uint32_t total = map.fI.d * *((volatile uint32_t *)&a.hdr->n_leaf);

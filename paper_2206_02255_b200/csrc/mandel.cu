@@ -188,6 +188,7 @@ int dev_info(int dev, DevInfo *&out)
     DevInfo &di = g_dev[dev];
     if (!di.cap) {
         CK(cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev));
+        CK(cudaMemcpyToSymbol(c_num_sms, &di.sms, sizeof(int)));
         CK(cudaStreamCreateWithFlags(&di.cap, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithFlags(&di.side, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&di.fork, cudaEventDisableTiming));
@@ -283,6 +284,8 @@ int enqueue_ask(const Key &k, const Layout &lay, const int32_t *d_tiles_visible,
     a.levels = lay.L;
     a.scheme = k.scheme;
     a.d0 = (int)(k.n / k.g);
+    a.capL = (uint32_t)lay.cap[lay.L - 1];
+    a.capP = (uint32_t)(lay.cap[lay.L - 1] / ((size_t)k.r * k.r));
     a.tile_cost = (k.flags & MANDEL_FLAG_TILE_COST) ? (unsigned long long *)(ws + lay.tile_cost) : nullptr;
     const bool stats = (k.flags & (MANDEL_FLAG_STATS | MANDEL_FLAG_TILE_COST)) != 0;
     const bool flat = (k.flags & MANDEL_FLAG_FLAT) != 0;
@@ -373,9 +376,14 @@ int enqueue_ask(const Key &k, const Layout &lay, const int32_t *d_tiles_visible,
             }
             CK(cudaGetLastError());
             TEND(MANDEL_KIND_B200_BORDER, l, s);
-            int gsz = resident_grid(k_b200_classify, 256, sms, (cap + 7) / 8);
             TBEGIN(s);
-            k_b200_classify<<<gsz, 256, 0, s>>>(a);
+            if (d >= 256) {
+                int gsz = resident_grid(k_b200_classify<8>, 256, sms, cap);
+                k_b200_classify<8><<<gsz, 256, 0, s>>>(a);
+            } else {
+                int gsz = resident_grid(k_b200_classify<1>, 256, sms, (cap + 7) / 8);
+                k_b200_classify<1><<<gsz, 256, 0, s>>>(a);
+            }
             CK(cudaGetLastError());
             TEND(MANDEL_KIND_B200_CLASSIFY, l, s);
         }

@@ -7,7 +7,7 @@
 // pixels at maxdwell), and the warp runs as long as its slowest lane.  Here every warp is
 // persistent and keeps its 32 lanes busy:
 //
-//   * a warp grabs CH consecutive indices at a time from a per-launch cursor in the
+//   * a warp grabs up to CH consecutive indices at a time from a per-launch cursor in the
 //     workspace header (one atomicAdd by lane 0) and deals them to its idle lanes in order
 //     (ballot + popc rank), so neighbouring pixels run side by side;
 //   * busy lanes iterate in unrolled chunks of K steps (dwell.cuh's 7-op step) with one
@@ -15,10 +15,10 @@
 //   * a lane whose pixel escaped (or reached maxdwell) during the chunk parks that
 //     chunk-start point in a per-warp queue in shared memory and is refilled at once, as
 //     soon as T lanes are parked;
-//   * whenever 32 points are queued the warp replays them together, one lane each: one
-//     step at a time from the chunk start, which yields the exact first-escape index
-//     (escape is permanent), then stores the dwell.  Replays thus run with
-//     all 32 lanes busy instead of stalling the warp once per escaping lane.
+//   * whenever 32 points are queued the warp replays them together, one lane each: a
+//     bisection over the K steps after the chunk start finds the exact first-escape index
+//     (escape is permanent), then the dwell is stored.  Replays thus run
+//     with all 32 lanes busy instead of stalling the warp once per escaping lane.
 //
 // The image equals the plain kernels' (each pixel's dwell is a pure function); only which
 // lane computes which pixel, and when, changes.  Pixels with |c|^2 > 3.9 (outside every
@@ -74,28 +74,43 @@ struct ParkedPoint {
 
 constexpr int RF_QCAP = 64; // per-warp queue entries (< 32 left over + < 32 new)
 
+// SM count of the device the kernels run on (set by the host before capture).
+__constant__ int c_num_sms;
+
 // Replay the queued points q[0..cnt) (cnt <= 32), one per lane, and store their dwells.
-template <class Sink>
+// A parked point escaped (or reached maxdwell) within the K steps after its chunk start, so
+// its dwell is sit + j* with j* the first j in [1, K] where P(j) = "escaped at step j, or
+// sit + j >= maxdwell" holds.  P is monotone (escape is permanent), so j* is
+// found by bisection: K/2 + K/4 + ... + 1 = K - 1 steps and log2 K tests, instead of up to K
+// steps with a test each.  Every lane runs the same instruction sequence (no divergence).
+template <int K, class Sink>
 __device__ __forceinline__ void replay_batch(const ParkedPoint *q, int cnt, const PixMap &pm, unsigned md,
-                                             int maxdwell, Sink &sink)
+                                             Sink &sink)
 {
+    static_assert((K & (K - 1)) == 0, "K must be a power of two");
     const int lane = threadIdx.x & 31;
     if (lane < cnt) {
         const ParkedPoint p = q[lane];
         const float cr = pix_re(pm, p.px), ci = pix_im(pm, p.py);
-        float x = p.x, y = p.y;
-        float x2 = __fmul_rn(x, x), y2 = __fmul_rn(y, y); // as the chunk start had them
-        unsigned it = p.it;
-        int v = maxdwell;
-        while (it < md) {
-            MANDEL_STEP(x, y, x2, y2, cr, ci);
-            ++it;
-            if (__fadd_rn(x2, y2) > 4.0f) {
-                v = (int)it;
-                break;
+        float bx = p.x, by = p.y;
+        float bx2 = __fmul_rn(bx, bx), by2 = __fmul_rn(by, by); // as the chunk start had them
+        unsigned lo = p.it;                                     // P false at lo (not escaped)
+#pragma unroll
+        for (int h = K / 2; h >= 1; h /= 2) {
+            float x = bx, y = by, x2 = bx2, y2 = by2;
+#pragma unroll
+            for (int k = 0; k < h; ++k)
+                MANDEL_STEP(x, y, x2, y2, cr, ci);
+            const bool hit = !(__fadd_rn(x2, y2) <= 4.0f) || lo + (unsigned)h >= md;
+            if (!hit) { // first hit lies beyond lo + h
+                bx = x;
+                by = y;
+                bx2 = x2;
+                by2 = y2;
+                lo += (unsigned)h;
             }
         }
-        sink(p.px, p.py, v);
+        sink(p.px, p.py, (int)(lo + 1u));
     }
     __syncwarp();
 }
@@ -103,11 +118,30 @@ __device__ __forceinline__ void replay_batch(const ParkedPoint *q, int cnt, cons
 // Map: __device__ void operator()(uint32_t t, int &x, int &y) const      (t < 2^32)
 // Sink: __device__ void operator()(int x, int y, int v)                   (store + stats)
 // q: this warp's RF_QCAP-entry queue in shared memory.
+// The grab size adapts to the launch: at most CH, but small enough that every warp of the
+// grid gets about 4 grabs (small levels -- e.g. one rank's share of a multi-GPU run -- would
+// otherwise leave most warps idle while a few run whole grabs of maxdwell pixels), and >= 8.
 template <int K, int T, int CH, class Map, class Sink>
 __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint32_t total,
                                             unsigned long long *cursor, const Map &map, Sink &sink,
                                             ParkedPoint *q)
 {
+    // Active warps: a launch with few pixels per lane runs like a thread-per-pixel kernel
+    // (every warp waits for its slowest lane and there is nothing to refill from), so only
+    // ~total/(32*PPL) warps work -- but never fewer than 2 per SM sub-partition (592 on
+    // B200), below which one warp per scheduler is latency-bound.  Warp w of block b has
+    // rank w*gridDim+b, so the active warps spread over all SMs.  (Idle warps return here and
+    // still reach the caller's block-wide reductions.)
+    constexpr uint32_t PPL = 8;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t min_active = 8u * (uint32_t)c_num_sms;
+    uint32_t active = total / (32u * PPL);
+    active = active < min_active ? min_active : active;
+    active = active > nwarps ? nwarps : active;
+    if ((threadIdx.x >> 5) * gridDim.x + blockIdx.x >= active)
+        return;
+    uint32_t grab = total / (4u * active);
+    grab = grab < 8u ? 8u : (grab > (uint32_t)CH ? (uint32_t)CH : grab);
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
@@ -140,7 +174,7 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
             __syncwarp();
             if (qn >= 32) {
                 qn -= 32;
-                replay_batch(q + qn, 32, pm, md, maxdwell, sink);
+                replay_batch<K>(q + qn, 32, pm, md, sink);
             }
         }
         unsigned need = __ballot_sync(FULL, !has);
@@ -148,14 +182,14 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
             if (pos >= end) {
                 unsigned long long b = 0;
                 if (lane == 0)
-                    b = atomicAdd(cursor, (unsigned long long)CH);
+                    b = atomicAdd(cursor, (unsigned long long)grab);
                 b = __shfl_sync(FULL, b, 0);
                 if (b >= total) {
                     exhausted = true;
                     break;
                 }
                 pos = (uint32_t)b;
-                end = (uint32_t)min(b + (unsigned long long)CH, (unsigned long long)total);
+                end = (uint32_t)min(b + (unsigned long long)grab, (unsigned long long)total);
             }
             const unsigned cnt = __popc(need);
             const unsigned avail = end - pos;
@@ -203,7 +237,7 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
     }
     // drain the queue
     if (qn > 0)
-        replay_batch(q, qn, pm, md, maxdwell, sink);
+        replay_batch<K>(q, qn, pm, md, sink);
 }
 
 } // namespace mandel

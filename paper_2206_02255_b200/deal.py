@@ -7,7 +7,9 @@ Deals (tile id k = gy * g + gx, canonical order):
   cyclic     k -> rank k mod P                       (plain cyclic deal)
   diagonal   k -> rank (gx + gy) mod P               (balances conjugate mirror pairs)
   costrank   tiles sorted by an estimated cost (descending, ties by id), dealt
-             boustrophedon 0..P-1, P-1..0, ...       (cost-ranked cyclic deal)
+             boustrophedon 0..P-1, P-1..0, ...       (cost-ranked cyclic deal); each rank
+             keeps its tiles in that descending order, which becomes its level-0 OLT order
+             (longest-first: the level-0 kernel's tail is short work)
 """
 from __future__ import annotations
 
@@ -28,7 +30,7 @@ def costrank(costs: Sequence[float], world: int) -> List[List[int]]:
     for i, k in enumerate(order):
         rnd, pos = divmod(i, world)
         out[pos if rnd % 2 == 0 else world - 1 - pos].append(k)
-    return [sorted(t) for t in out]
+    return out  # each rank's tiles in descending cost: its level-0 work starts with the longest
 
 
 def deal(method: str, g: int, world: int, costs: Optional[Sequence[float]] = None) -> List[List[int]]:

@@ -203,3 +203,38 @@ def test_full_size_exhaustive_sampled_pixels(mb, wname):
     # plus two full rows (a ragged mix of inside / outside)
     for i in (w.n // 2 - 1, w.n // 3):
         assert np.array_equal(out[i].cpu().numpy(), oracle.exhaustive(w.region, w.n, w.maxdwell, i, 1)[0])
+
+
+@pytest.mark.parametrize("md", [1, 2, 3, 7, 8, 9, 15, 16, 17, 31, 32, 33, 63, 65, 100, 257])
+def test_ask_maxdwell_not_multiple_of_chunk(mb, md):
+    """The lane-refill kernels run K-step chunks and find the exact dwell by bisection over
+    the last chunk, capped at maxdwell: maxdwell values around multiples of K (8, 16, 32)."""
+    n, g, r, B = 256, 4, 2, 8
+    for region in (W.DEFAULT_REGION, W.SEAHORSE_REGION):
+        ws = mb.workspace(n, g, r, B)
+        out = mb.ask(region, n, md, g, r, B, ws=ws)
+        A, _ = oracle.ask(region, n, md, g, r, B)
+        assert np.array_equal(out.cpu().numpy(), A), (region, md)
+        ex = mb.exhaustive(region, n, md).cpu().numpy()
+        assert np.array_equal(ex, oracle.exhaustive(region, n, md)), (region, md)
+
+
+def test_ask_large_region_outside_radius(mb):
+    """|c|^2 > 3.9 pixels take the per-step path (escape permanence is not guaranteed
+    there): a window straddling |c| = 2 on the negative real axis, including c = -2."""
+    region = (-2.25, -1.75, -0.25, 0.25)
+    n, g, r, B, md = 256, 2, 2, 8, 700
+    out = mb.ask(region, n, md, g, r, B)
+    A, _ = oracle.ask(region, n, md, g, r, B)
+    assert np.array_equal(out.cpu().numpy(), A)
+
+
+@pytest.mark.parametrize("flags", [dict(flat=True), dict(serial=True), dict(flat=True, serial=True)])
+@pytest.mark.parametrize("w", [W.C1, W.Workload("sea2k", W.SEAHORSE_REGION, 2048, 1500, 8, 4, 16)],
+                         ids=lambda w: w.name if hasattr(w, "name") else str(w))
+def test_ask_ab_variants(mb, w, flags):
+    """The A/B variants (plain thread-per-pixel kernels, fills on the main stream) produce
+    the same image as the oracle too."""
+    out = mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, **flags)
+    A, _ = oracle.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B)
+    assert np.array_equal(out.cpu().numpy(), A)

@@ -40,7 +40,9 @@ SCALE = {"ms": 1.0, "us": 1e-3, "ns": 1e-6, "s": 1e3,
 def kind_of(name: str) -> str:
     m = re.search(r"k_(b200_border_rf|b200_border|b200_classify|b200_leaf_rf|b200_leaf|fill|sbr_level|sbr_leaf|"
                   r"exhaustive\w*|init)", name)
-    return m.group(1) if m else name[:40]
+    if not m:
+        return name[:40]
+    return m.group(1)[:-3] if m.group(1).endswith("_rf") else m.group(1)  # bench.py kind names
 
 
 def load(rep: str):
