@@ -104,6 +104,13 @@ enum {
                                     same image)                                            */
 #define MANDEL_FLAG_SERIAL 16u   /* run every fill on the main stream after its level instead
                                     of as a concurrent graph branch (A/B; same image)       */
+/* Groups: the call's level-0 tiles are dealt round-robin (in the given order) to G independent
+ * ASK chains, each level-synchronous, captured as parallel graph branches, so one chain's
+ * level tails overlap another's work.  G in {1..8}, encoded in flag bits
+ * 8-11 as G-1; 0 there means 1 group.  Same image for every G.                           */
+#define MANDEL_FLAG_GROUPS(G) ((((uint32_t)(G)-1u) & 15u) << 8)
+#define MANDEL_FLAG_GROUPS_MASK (15u << 8)
+#define MANDEL_FLAG_GROUPS_OF(f) ((int)(((f) >> 8) & 15u) + 1)
 
 /* Kernel kinds reported by mandel_ask_kernel_times (value = kind * 100 + level). */
 enum {

@@ -18,6 +18,8 @@ from typing import List, Optional, Sequence
 from . import _lib
 
 SCHEMES = {"sbr": _lib.SCHEME_SBR, "b200": _lib.SCHEME_B200}
+# Independent ASK chains per call (MANDEL_FLAG_GROUPS); same image for any value.
+DEFAULT_GROUPS = 1
 
 
 def _torch():
@@ -74,12 +76,13 @@ def exhaustive(region: Sequence[float], n: int, maxdwell: int, out=None, stream=
 def ask(region: Sequence[float], n: int, maxdwell: int, g: int, r: int, B: int, out=None, ws=None,
         tiles: Optional[Sequence[int]] = None, scheme: str = "b200", stats: bool = False,
         timing: bool = False, tile_cost: bool = False, flat: bool = False, serial: bool = False,
-        stream=None):
+        groups: Optional[int] = None, stream=None):
     """ASK dwell image over all g*g level-0 regions, or only `tiles`.
     stats: accumulate per-level counters (ask_stats); timing: per-kernel events
     (kernel_times); flat: B200 scheme with the plain thread-per-pixel border/leaf kernels
     instead of the lane-refill ones; serial: fills on the main stream instead of concurrent
-    graph branches (A/B comparisons, same image)."""
+    graph branches (A/B comparisons, same image); groups: independent level-synchronous
+    chains over round-robin subsets of the tiles, run as parallel graph branches."""
     out = _image(n, out)
     if ws is None:
         ws = workspace(n, g, r, B, device=out.device)
@@ -89,7 +92,8 @@ def ask(region: Sequence[float], n: int, maxdwell: int, g: int, r: int, B: int, 
                                       (_lib.FLAG_STATS if stats else 0) | (_lib.FLAG_TIMING if timing else 0)
                                       | (_lib.FLAG_TILE_COST if tile_cost else 0)
                                       | (_lib.FLAG_FLAT if flat else 0)
-                                      | (_lib.FLAG_SERIAL if serial else 0),
+                                      | (_lib.FLAG_SERIAL if serial else 0)
+                                      | _lib.flag_groups(DEFAULT_GROUPS if groups is None else groups),
                                       out.data_ptr(), out.stride(0), ws.data_ptr(), ws.numel(),
                                       _stream_ptr(stream))
     _lib.check(rc, "mandel_ask_tiles")

@@ -23,6 +23,14 @@ FLAG_TIMING = 2
 FLAG_TILE_COST = 4
 FLAG_FLAT = 8
 FLAG_SERIAL = 16
+MAX_GROUPS = 8
+
+
+def flag_groups(g: int) -> int:
+    """MANDEL_FLAG_GROUPS(g) of include/mandel.h."""
+    if not 1 <= int(g) <= MAX_GROUPS:
+        raise ValueError(f"groups must be in [1, {MAX_GROUPS}]")
+    return ((int(g) - 1) & 15) << 8
 KIND_NAMES = {0: "init", 1: "b200_border", 2: "b200_classify", 3: "fill", 4: "b200_leaf",
               5: "sbr_level", 6: "sbr_leaf"}
 

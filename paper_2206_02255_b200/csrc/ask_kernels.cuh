@@ -8,6 +8,7 @@
 //   header  counters: subdivided / filled per level, leaves, optional iteration stats
 #pragma once
 #include <limits.h>
+#include <stddef.h>
 #include <stdint.h>
 
 #include "dwell.cuh"
@@ -16,6 +17,7 @@
 namespace mandel {
 
 constexpr int MAXL = 32;
+constexpr int MAXG = 8; // independent ASK chains (groups) per call
 constexpr uint32_t WS_MAGIC = 0x4d41534bu; // "MASK"
 constexpr int DWELL_K = 8;                 // iterations per escape test (dwell.cuh)
 // Lane-refill knobs (refill.cuh), tuned on B200 at C3/C5 (profiles/r01_tune_refill*.txt):
@@ -56,6 +58,7 @@ struct WsHeader {
     // ("cold") from the back, so the next kernel hands out hot work first.
     uint32_t n_sub_hot[MAXL], n_sub_cold[MAXL];
     uint32_t n_leaf_hot, n_leaf_cold;
+    uint32_t ngroups; // header of group 0: groups of the last call
     unsigned long long border_px[MAXL], border_iters[MAXL];
     unsigned long long leaf_px, leaf_iters;
     unsigned long long cursor[MAXL + 1]; // lane-refill work cursors: border level l, leaves
@@ -118,6 +121,7 @@ struct LevelArgs {
     FastDiv fd[4];           // lane-refill index maps (host-computed divisors)
     uint32_t capP;           // parent slots of an OLT buffer (= OLT entries / r^2)
     uint32_t capL;           // leaf list entries
+    int ngroups;
 };
 
 // Hot/cold list addressing: the q-th subdivided parent of level l-1 (q < hot count: front
@@ -226,8 +230,9 @@ __global__ void k_init(LevelArgs a)
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     constexpr int hdr_words = sizeof(WsHeader) / 4;
     uint32_t *hw = reinterpret_cast<uint32_t *>(a.hdr);
+    constexpr int ng_word = (int)(offsetof(WsHeader, ngroups) / 4);
     if (t >= 8 && t < hdr_words)
-        hw[t] = 0u;
+        hw[t] = (t == ng_word) ? (uint32_t)a.ngroups : 0u;
     if (t == 0) {
         a.hdr->magic = WS_MAGIC;
         a.hdr->levels = (uint32_t)a.levels;
@@ -240,12 +245,12 @@ __global__ void k_init(LevelArgs a)
     }
     if (t == 1)
         a.hdr->n = (uint32_t)(a.d * a.g);
-    if (a.tile_cost && t < a.g * a.g)
-        a.tile_cost[t] = 0ull;
     if (t < a.ntiles) {
         const int k = a.tiles ? a.tiles[t] : t;
         const int gx = k % a.g, gy = k / a.g;
         const_cast<uint32_t *>(a.olt_in)[t] = pack_xy(gx * a.d, gy * a.d);
+        if (a.tile_cost) // only this group's tiles (groups run concurrently)
+            a.tile_cost[k] = 0ull;
     }
 }
 

@@ -74,6 +74,7 @@ struct Layout {
     int u_log2; // log2 of the leaf side u = (n/g) / r^(L-1)
     size_t fill_off[MAXL]; // element offset of each level's fill segment
     size_t cap[MAXL];
+    size_t per_tile[MAXL]; // r^(2l): capacity per level-0 tile at level l
 };
 
 size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
@@ -88,6 +89,7 @@ bool make_layout(int64_t n, int32_t g, int32_t r, int32_t B, Layout &lay)
     size_t c = (size_t)g * g, fsum = 0;
     for (int l = 0; l < lay.L; ++l) {
         lay.cap[l] = c;
+        lay.per_tile[l] = c / ((size_t)g * g);
         lay.fill_off[l] = fsum;
         fsum += c;
         c *= (size_t)r * r;
@@ -95,7 +97,7 @@ bool make_layout(int64_t n, int32_t g, int32_t r, int32_t B, Layout &lay)
     const size_t capmax = lay.cap[lay.L - 1];
     size_t o = 0;
     lay.hdr = o;
-    o += 4096;
+    o += (size_t)MAXG * 4096; // one header per group
     lay.tiles = o;
     o = align256(o + (size_t)g * g * 4);
     lay.olt[0] = o;
@@ -142,9 +144,11 @@ PixMap make_map(const mandel_region &reg, int64_t n)
 
 struct DevInfo {
     int sms = 0;
-    cudaStream_t cap = nullptr;  // capture origin stream
-    cudaStream_t side = nullptr; // capture side stream (fill branches)
-    cudaEvent_t fork = nullptr;  // fork/join event used during capture
+    cudaStream_t cap = nullptr;        // capture origin stream
+    cudaStream_t grp[MAXG] = {};       // one capture stream per group chain
+    cudaStream_t side[MAXG] = {};      // per group: capture side stream (fill branches)
+    cudaEvent_t fork[MAXG] = {};       // per group: fill fork/join event used during capture
+    cudaEvent_t start = nullptr, join[MAXG] = {};
 };
 
 struct Key {
@@ -190,8 +194,13 @@ int dev_info(int dev, DevInfo *&out)
         CK(cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev));
         CK(cudaMemcpyToSymbol(c_num_sms, &di.sms, sizeof(int)));
         CK(cudaStreamCreateWithFlags(&di.cap, cudaStreamNonBlocking));
-        CK(cudaStreamCreateWithFlags(&di.side, cudaStreamNonBlocking));
-        CK(cudaEventCreateWithFlags(&di.fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&di.start, cudaEventDisableTiming));
+        for (int i = 0; i < MAXG; ++i) {
+            CK(cudaStreamCreateWithFlags(&di.grp[i], cudaStreamNonBlocking));
+            CK(cudaStreamCreateWithFlags(&di.side[i], cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&di.fork[i], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&di.join[i], cudaEventDisableTiming));
+        }
     }
     out = &di;
     return MANDEL_OK;
@@ -258,13 +267,24 @@ int t_end(Timing *tm, int kind, int level, cudaStream_t st)
             return m_;                                                                         \
     } while (0)
 
-// Enqueue the whole ASK call on `s` (called under stream capture).
+// One independent ASK chain over a subset of the level-0 tiles: its own
+// header, and slices of the OLT / fill / leaf buffers sized for its tiles.
+struct Group {
+    size_t hdr;               // byte offset of its header
+    size_t unit0;             // level-0 tiles of the groups before it (slice offset unit)
+    int ntiles;
+    const int32_t *tiles;     // device-visible tile ids (NULL: canonical 0..ntiles-1)
+};
+
+// Enqueue one group's whole ASK chain on `s` (called under stream capture).
 // Fills (HBM-bound) run on the side stream s2 as graph branches forked after each level's
 // classification and joined at the end, overlapping the ALU-bound dwell kernels; a fill
 // writes only the interior of regions that are terminal, which no later kernel reads.
-int enqueue_ask(const Key &k, const Layout &lay, const int32_t *d_tiles_visible, int ntiles, int sms,
-                cudaStream_t s, cudaStream_t s2, cudaEvent_t fork, Timing *tm)
+int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, int sms, cudaStream_t s,
+                cudaStream_t s2, cudaEvent_t fork, Timing *tm)
 {
+    const int ntiles = grp.ntiles;
+    const size_t Lm = (size_t)lay.L - 1;
     const bool overlap = (k.flags & MANDEL_FLAG_SERIAL) == 0;
     cudaStream_t sf = overlap ? s2 : s; // stream of the fill kernels
     char *ws = (char *)k.ws;
@@ -274,9 +294,10 @@ int enqueue_ask(const Key &k, const Layout &lay, const int32_t *d_tiles_visible,
     a.maxdwell = k.maxdwell;
     a.pitch = k.pitch;
     a.out = k.out;
-    a.hdr = (WsHeader *)(ws + lay.hdr);
-    a.leaf = (uint32_t *)(ws + lay.leaf);
-    a.tiles = d_tiles_visible;
+    a.hdr = (WsHeader *)(ws + grp.hdr);
+    a.leaf = (uint32_t *)(ws + lay.leaf) + grp.unit0 * lay.per_tile[Lm];
+    a.tiles = grp.tiles;
+    a.ngroups = ngroups;
     a.r = k.r;
     a.B = k.B;
     a.g = k.g;
@@ -284,8 +305,8 @@ int enqueue_ask(const Key &k, const Layout &lay, const int32_t *d_tiles_visible,
     a.levels = lay.L;
     a.scheme = k.scheme;
     a.d0 = (int)(k.n / k.g);
-    a.capL = (uint32_t)lay.cap[lay.L - 1];
-    a.capP = (uint32_t)(lay.cap[lay.L - 1] / ((size_t)k.r * k.r));
+    a.capL = (uint32_t)((size_t)ntiles * lay.per_tile[Lm]);
+    a.capP = (uint32_t)((size_t)ntiles * lay.per_tile[Lm] / ((size_t)k.r * k.r));
     a.tile_cost = (k.flags & MANDEL_FLAG_TILE_COST) ? (unsigned long long *)(ws + lay.tile_cost) : nullptr;
     const bool stats = (k.flags & (MANDEL_FLAG_STATS | MANDEL_FLAG_TILE_COST)) != 0;
     const bool flat = (k.flags & MANDEL_FLAG_FLAT) != 0;
@@ -300,7 +321,9 @@ int enqueue_ask(const Key &k, const Layout &lay, const int32_t *d_tiles_visible,
     // init: level-0 OLT + zeroed counters
     a.level = 0;
     a.d = d0;
-    a.olt_in = (const uint32_t *)(ws + lay.olt[0]);
+    uint32_t *olt_g[2] = {(uint32_t *)(ws + lay.olt[0]) + grp.unit0 * lay.per_tile[Lm],
+                          (uint32_t *)(ws + lay.olt[1]) + grp.unit0 * lay.per_tile[Lm]};
+    a.olt_in = olt_g[0];
     {
         int nthr = ntiles > 1024 ? ntiles : 1024;
         if (nthr < k.g * k.g)
@@ -315,9 +338,9 @@ int enqueue_ask(const Key &k, const Layout &lay, const int32_t *d_tiles_visible,
         a.level = l;
         a.d = d;
         a.subdivide = (d / k.r >= k.B) ? 1 : 0;
-        a.olt_in = (const uint32_t *)(ws + lay.olt[l & 1]);
-        a.olt_out = (uint32_t *)(ws + lay.olt[(l + 1) & 1]);
-        a.fill = (uint2 *)(ws + lay.fill) + lay.fill_off[l];
+        a.olt_in = olt_g[l & 1];
+        a.olt_out = olt_g[(l + 1) & 1];
+        a.fill = (uint2 *)(ws + lay.fill) + lay.fill_off[l] + grp.unit0 * lay.per_tile[l];
         // max regions at this level for this call
         size_t cap = (size_t)ntiles;
         for (int i = 0; i < l; ++i)
@@ -548,7 +571,8 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
         return rc;
     if (!valid_grb(n, g, r, B) || !d_ws || (scheme != MANDEL_SCHEME_SBR && scheme != MANDEL_SCHEME_B200) ||
         (flags & ~(MANDEL_FLAG_STATS | MANDEL_FLAG_TIMING | MANDEL_FLAG_TILE_COST | MANDEL_FLAG_FLAT |
-                   MANDEL_FLAG_SERIAL)) != 0)
+                   MANDEL_FLAG_SERIAL | MANDEL_FLAG_GROUPS_MASK)) != 0 ||
+        MANDEL_FLAG_GROUPS_OF(flags) > MAXG)
         return MANDEL_EINVAL;
     Layout lay;
     if (!make_layout(n, g, r, B, lay))
@@ -599,9 +623,28 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
         }
         Entry e;
         e.key = key;
-        if (h_tile_ids && ntiles > 0) {
-            CK(cudaHostAlloc((void **)&e.h_tiles, (size_t)ntiles * 4, cudaHostAllocMapped | cudaHostAllocPortable));
-            memcpy(e.h_tiles, tiles.data(), (size_t)ntiles * 4);
+        // groups: tiles dealt round-robin in the given order (LPT order is preserved)
+        int ngroups = MANDEL_FLAG_GROUPS_OF(flags);
+        if (ngroups > ntiles)
+            ngroups = ntiles > 0 ? ntiles : 1;
+        std::vector<int32_t> order;
+        std::vector<int> gcount((size_t)ngroups, 0);
+        if (ngroups > 1 || h_tile_ids) {
+            std::vector<int32_t> all(tiles);
+            if (!h_tile_ids)
+                for (int32_t t = 0; t < ntiles; ++t)
+                    all.push_back(t);
+            for (int gi = 0; gi < ngroups; ++gi)
+                for (int i = gi; i < ntiles; i += ngroups) {
+                    order.push_back(all[(size_t)i]);
+                    ++gcount[(size_t)gi];
+                }
+        } else {
+            gcount[0] = ntiles;
+        }
+        if (!order.empty()) {
+            CK(cudaHostAlloc((void **)&e.h_tiles, order.size() * 4, cudaHostAllocMapped | cudaHostAllocPortable));
+            memcpy(e.h_tiles, order.data(), order.size() * 4);
         }
         int32_t *d_tiles = nullptr;
         if (e.h_tiles) {
@@ -619,7 +662,28 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
         }
         Timing tm;
         tm.on = (flags & MANDEL_FLAG_TIMING) != 0;
-        int erc = enqueue_ask(key, lay, d_tiles, ntiles, di->sms, di->cap, di->side, di->fork, &tm);
+        int erc = MANDEL_OK;
+        if (ngroups == 1) {
+            Group grp{lay.hdr, 0, ntiles, d_tiles};
+            erc = enqueue_ask(key, lay, grp, 1, di->sms, di->cap, di->side[0], di->fork[0], &tm);
+        } else { // fork one branch per group off the origin stream, join them at the end
+            cudaError_t fe = cudaEventRecord(di->start, di->cap);
+            size_t unit0 = 0;
+            for (int gi = 0; gi < ngroups && !erc && fe == cudaSuccess; ++gi) {
+                fe = cudaStreamWaitEvent(di->grp[gi], di->start, 0);
+                if (fe != cudaSuccess)
+                    break;
+                Group grp{lay.hdr + (size_t)gi * 4096, unit0, gcount[(size_t)gi], d_tiles + unit0};
+                erc = enqueue_ask(key, lay, grp, ngroups, di->sms, di->grp[gi], di->side[gi], di->fork[gi], &tm);
+                if (!erc)
+                    fe = cudaEventRecord(di->join[gi], di->grp[gi]);
+                if (!erc && fe == cudaSuccess)
+                    fe = cudaStreamWaitEvent(di->cap, di->join[gi], 0);
+                unit0 += (size_t)gcount[(size_t)gi];
+            }
+            if (!erc && fe != cudaSuccess)
+                erc = cuda_fail(fe, "group fork/join");
+        }
         e.evs = tm.evs;
         e.kinds = tm.kinds;
         e.t_start = tm.start;
@@ -713,24 +777,34 @@ int mandel_ask_last_stats(const void *d_ws, mandel_level_stats *h_out, int32_t m
     CK(cudaStreamSynchronize((cudaStream_t)stream));
     WsHeader h;
     CK(cudaMemcpy(&h, d_ws, sizeof h, cudaMemcpyDeviceToHost));
-    if (h.magic != WS_MAGIC || h.levels < 1 || h.levels > (uint32_t)MAXL)
+    if (h.magic != WS_MAGIC || h.levels < 1 || h.levels > (uint32_t)MAXL || h.ngroups < 1 ||
+        h.ngroups > (uint32_t)MAXG)
         return -MANDEL_EINVAL;
+    // sum the counters of every group's header (group 0's header carries the group count)
+    std::vector<WsHeader> hs(h.ngroups);
+    CK(cudaMemcpy2D(hs.data(), sizeof(WsHeader), d_ws, 4096, sizeof(WsHeader), h.ngroups,
+                    cudaMemcpyDeviceToHost));
     const int L = (int)h.levels;
     int64_t d = (int64_t)h.n / h.g;
-    int64_t regions = h.ntiles;
+    int64_t regions = 0;
+    for (const auto &hg : hs)
+        regions += hg.ntiles;
     for (int l = 0; l < L && l < max_levels; ++l) {
         mandel_level_stats &s = h_out[l];
         s.level = l;
         s.side = (int32_t)d;
         s.regions_in = regions;
-        s.filled = h.n_fill[l];
-        s.subdivided = h.n_subdiv[l];
-        s.leaves = (l == L - 1) ? h.n_leaf : 0;
-        s.border_px = (int64_t)h.border_px[l];
-        s.border_iters = (int64_t)h.border_iters[l];
-        s.leaf_px = (l == L - 1) ? (int64_t)h.leaf_px : 0;
-        s.leaf_iters = (l == L - 1) ? (int64_t)h.leaf_iters : 0;
-        regions = (int64_t)h.n_subdiv[l] * h.r * h.r;
+        s.filled = s.subdivided = s.leaves = s.border_px = s.border_iters = s.leaf_px = s.leaf_iters = 0;
+        for (const auto &hg : hs) {
+            s.filled += hg.n_fill[l];
+            s.subdivided += hg.n_subdiv[l];
+            s.leaves += (l == L - 1) ? hg.n_leaf : 0;
+            s.border_px += (int64_t)hg.border_px[l];
+            s.border_iters += (int64_t)hg.border_iters[l];
+            s.leaf_px += (l == L - 1) ? (int64_t)hg.leaf_px : 0;
+            s.leaf_iters += (l == L - 1) ? (int64_t)hg.leaf_iters : 0;
+        }
+        regions = s.subdivided * h.r * h.r;
         d /= h.r;
     }
     return L;
@@ -781,10 +855,18 @@ void mandel_shutdown(void)
     for (auto &d : g_dev) {
         if (d.cap)
             cudaStreamDestroy(d.cap);
-        if (d.side)
-            cudaStreamDestroy(d.side);
-        if (d.fork)
-            cudaEventDestroy(d.fork);
+        if (d.start)
+            cudaEventDestroy(d.start);
+        for (int i = 0; i < MAXG; ++i) {
+            if (d.grp[i])
+                cudaStreamDestroy(d.grp[i]);
+            if (d.side[i])
+                cudaStreamDestroy(d.side[i]);
+            if (d.fork[i])
+                cudaEventDestroy(d.fork[i]);
+            if (d.join[i])
+                cudaEventDestroy(d.join[i]);
+        }
     }
     g_dev.clear();
 }

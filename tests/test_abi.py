@@ -101,6 +101,9 @@ def test_validation_before_any_launch(lib):
     assert lib.mandel_ask_tiles(*args, ctypes.cast(t, ctypes.c_void_p), 1, 1, 0, fake, 64, fake, ws_need, None) == 1
     assert lib.mandel_ask_tiles(*args, None, 0, 7, 0, fake, 64, fake, ws_need, None) == 1
     assert lib.mandel_ask_tiles(*args, None, 0, 1, 32, fake, 64, fake, ws_need, None) == 1
+    # more than 8 groups (MANDEL_FLAG_GROUPS bits 8-11 hold G-1)
+    assert lib.mandel_ask_tiles(*args, None, 0, 1, 8 << 8, fake, 64, fake, ws_need, None) == 1
+    assert _lib.flag_groups(1) == 0 and _lib.flag_groups(8) == 7 << 8
     assert lib.mandel_strerror(2) == b"workspace too small"
 
 

@@ -238,3 +238,22 @@ def test_ask_ab_variants(mb, w, flags):
     out = mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, **flags)
     A, _ = oracle.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B)
     assert np.array_equal(out.cpu().numpy(), A)
+
+
+@pytest.mark.parametrize("groups", [2, 3, 8])
+def test_ask_groups(mb, groups):
+    """Independent ASK chains over round-robin tile subsets (MANDEL_FLAG_GROUPS): same image
+    and the same summed level statistics as the oracle, with and without a tile subset."""
+    w = W.Workload("g", W.SEAHORSE_REGION, 1024, 900, 8, 2, 16)
+    ws = mb.workspace(w.n, w.g, w.r, w.B)
+    out = mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, ws=ws, groups=groups, stats=True)
+    A, st = oracle.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B)
+    assert np.array_equal(out.cpu().numpy(), A)
+    _cmp_stats(mb.ask_stats(ws), st, "b200")
+    tiles = [5, 17, 2, 40, 63, 33, 9]
+    buf = torch.full((w.n, w.n), -3, dtype=torch.int32, device="cuda")
+    mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=buf, ws=ws, tiles=tiles, groups=groups, stats=True)
+    At, stt = oracle.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, tiles=tiles)
+    mine = At != -1
+    assert np.array_equal(buf.cpu().numpy()[mine], At[mine]) and np.all(buf.cpu().numpy()[~mine] == -3)
+    _cmp_stats(mb.ask_stats(ws), stt, "b200")

@@ -23,8 +23,12 @@ import workloads as W  # noqa: E402
 from paper_2206_02255_b200 import deal  # noqa: E402
 
 
+GROUPS = None
+
+
 def time_tiles(w, out, ws, tiles, flush, reps):
-    f = lambda: mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, tiles=tiles)  # noqa: E731
+    f = lambda: mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, tiles=tiles,  # noqa: E731
+                       groups=GROUPS)
     f()
     torch.cuda.synchronize()
     ts = []
@@ -45,7 +49,10 @@ def main():
     ap.add_argument("--ranks", default="1,2,4,8")
     ap.add_argument("--deals", default="costrank,cyclic,diagonal")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--groups", type=int, default=None)
     a = ap.parse_args()
+    global GROUPS
+    GROUPS = a.groups
     w = W.CONFIGS[a.workload]
     out = torch.empty((w.n, w.n), dtype=torch.int32, device="cuda")
     ws = mb.workspace(w.n, w.g, w.r, w.B)
@@ -59,7 +66,7 @@ def main():
     mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, tile_cost=True)
     exact = mb.tile_costs(ws, w.g)
     t1 = time_tiles(w, out, ws, None, flush, a.reps)
-    res = {"workload": w.name, "t1_ms": t1, "preview_ms": preview_ms, "deals": {}}
+    res = {"workload": w.name, "groups": GROUPS, "t1_ms": t1, "preview_ms": preview_ms, "deals": {}}
     for dname in a.deals.split(","):
         for P in [int(x) for x in a.ranks.split(",")]:
             parts = deal.deal(dname, w.g, P, costs if dname == "costrank" else None)
@@ -72,16 +79,14 @@ def main():
     # per-kernel breakdown of the heaviest rank at the largest P (costrank deal)
     P = max(int(x) for x in a.ranks.split(","))
     parts = deal.deal("costrank", w.g, P, costs)
-    worst = max(range(P), key=lambda r: deal.imbalance([parts[r]], exact))
     heavy = max(parts, key=lambda p: sum(exact[k] for k in p))
     for _ in range(2):
-        mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, tiles=heavy, timing=True)
+        mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, tiles=heavy, timing=True, groups=GROUPS)
     torch.cuda.synchronize()
     res["heavy_rank_kernels"] = [dict(k) for k in mb.kernel_times()]
     mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, timing=True)
     torch.cuda.synchronize()
     res["full_kernels"] = [dict(k) for k in mb.kernel_times()]
-    del worst
     print(json.dumps(res), flush=True)
 
 
