@@ -42,6 +42,12 @@ constexpr int DWELL_K = 8;                 // iterations per escape test (dwell.
 #ifndef MANDEL_RFL_CH
 #define MANDEL_RFL_CH 128
 #endif
+#ifndef MANDEL_RF_WPS
+#define MANDEL_RF_WPS 4 // border: max working warps per SM sub-partition
+#endif
+#ifndef MANDEL_RFL_WPS
+#define MANDEL_RFL_WPS 12 // leaf
+#endif
 #ifndef MANDEL_RF_MINB
 #define MANDEL_RF_MINB 6
 #endif
@@ -507,14 +513,24 @@ __global__ void __launch_bounds__(256) k_b200_classify(LevelArgs a)
         const int x0 = unpack_x(off), y0 = unpack_y(off);
         int lo = INT_MAX, hi = INT_MIN;
         if (valid) {
-#pragma unroll 4
-            for (int b = t; b < ring; b += TPR) {
-                int x, y;
-                ring_pixel(b, d, x0, y0, x, y);
-                const int v = (a.colT && b >= 2 * d) ? __ldcg(a.colT + colT_index(a, x, y))
-                                                     : __ldcg(a.out + (long long)y * a.pitch + x);
-                lo = min(lo, v);
-                hi = max(hi, v);
+            // batches of 8 independent loads in flight per thread (the ring of a level-0
+            // region is 8188 pixels: latency, not bandwidth, bounds this loop)
+            for (int b0 = t; b0 < ring; b0 += 8 * TPR) {
+                int v[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int b = b0 + j * TPR;
+                    int x, y;
+                    ring_pixel(b < ring ? b : 0, d, x0, y0, x, y);
+                    const int *src = (a.colT && b >= 2 * d) ? a.colT + colT_index(a, x, y)
+                                                            : a.out + (long long)y * a.pitch + x;
+                    v[j] = b < ring ? __ldcg(src) : v[0];
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    lo = min(lo, v[j]);
+                    hi = max(hi, v[j]);
+                }
             }
         }
         lo = __reduce_min_sync(0xffffffffu, lo);
@@ -688,9 +704,9 @@ __global__ void __launch_bounds__(256, RF_MINB) k_b200_border_rf(LevelArgs a)
                                     : *((volatile uint32_t *)&a.hdr->n_subdiv[a.level - 1]);
     const uint32_t total = map.fper.d * count;
     StoreSink<STATS, true> sink{&a, 0ull, 0ull};
-    refill_loop<MANDEL_RFB_K, MANDEL_RFB_T, MANDEL_RFB_CH>(a.map, a.maxdwell, total, &a.hdr->cursor[a.level],
+    refill_loop<MANDEL_RFB_K, MANDEL_RFB_T, MANDEL_RFB_CH, MANDEL_RF_WPS>(a.map, a.maxdwell, total, &a.hdr->cursor[a.level],
                                                            map, sink,
-                                   s_q[threadIdx.x >> 5]);
+                                   s_q[threadIdx.x >> 5], a.level);
     sink_flush<STATS, true>(sink, &a.hdr->border_iters[a.level], &a.hdr->border_px[a.level]);
 }
 
@@ -707,9 +723,9 @@ __global__ void __launch_bounds__(256, RF_MINB) k_b200_leaf_rf(LevelArgs a)
     const uint32_t total = map.fI.d * *((volatile uint32_t *)&a.hdr->n_leaf);
     StoreSink<STATS, false> sink{&a, 0ull, 0ull};
     if (map.fI.d > 0)
-        refill_loop<MANDEL_RFL_K, MANDEL_RFL_T, MANDEL_RFL_CH>(a.map, a.maxdwell, total, &a.hdr->cursor[MAXL],
+        refill_loop<MANDEL_RFL_K, MANDEL_RFL_T, MANDEL_RFL_CH, MANDEL_RFL_WPS>(a.map, a.maxdwell, total, &a.hdr->cursor[MAXL],
                                                                map, sink,
-                                       s_q[threadIdx.x >> 5]);
+                                       s_q[threadIdx.x >> 5], 15);
     sink_flush<STATS, false>(sink, &a.hdr->leaf_iters, &a.hdr->leaf_px);
 }
 

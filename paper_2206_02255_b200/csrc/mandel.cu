@@ -846,6 +846,23 @@ const char *mandel_strerror(int code)
 
 const char *mandel_last_cuda_error(void) { return g_cuda_err; }
 
+#ifdef MANDEL_RF_TRACE
+// Debug builds only (not part of include/mandel.h): copy the refill trace of the last
+// traced launch ({start, exhausted, end, pixels | active << 40} per warp) to host memory.
+int mandel_debug_rf_trace(unsigned long long *h) // 16 x 8192 x 4 u64
+{
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpyFromSymbol(h, g_rf_trace, sizeof(g_rf_trace)));
+    return MANDEL_OK;
+}
+int mandel_debug_rf_trace_clear(void)
+{
+    static unsigned long long z[16][8192][4];
+    CK(cudaMemcpyToSymbol(g_rf_trace, z, sizeof z));
+    return MANDEL_OK;
+}
+#endif
+
 void mandel_shutdown(void)
 {
     std::lock_guard<std::mutex> lk(g_mu);

@@ -77,6 +77,18 @@ constexpr int RF_QCAP = 64; // per-warp queue entries (< 32 left over + < 32 new
 // SM count of the device the kernels run on (set by the host before capture).
 __constant__ int c_num_sms;
 
+#ifdef MANDEL_RF_TRACE
+// Debug build only (tools/trace_refill.py): per active warp of the last traced launch,
+// {start, cursor exhausted, end} in globaltimer ns and the pixels it computed.
+__device__ unsigned long long g_rf_trace[16][8192][4]; // [launch slot][warp rank]
+__device__ __forceinline__ unsigned long long rf_now()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
 // Replay the queued points q[0..cnt) (cnt <= 32), one per lane, and store their dwells.
 // A parked point escaped (or reached maxdwell) within the K steps after its chunk start, so
 // its dwell is sit + j* with j* the first j in [1, K] where P(j) = "escaped at step j, or
@@ -121,10 +133,10 @@ __device__ __forceinline__ void replay_batch(const ParkedPoint *q, int cnt, cons
 // The grab size adapts to the launch: at most CH, but small enough that every warp of the
 // grid gets about 4 grabs (small levels -- e.g. one rank's share of a multi-GPU run -- would
 // otherwise leave most warps idle while a few run whole grabs of maxdwell pixels), and >= 8.
-template <int K, int T, int CH, class Map, class Sink>
+template <int K, int T, int CH, int WPS, class Map, class Sink>
 __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint32_t total,
                                             unsigned long long *cursor, const Map &map, Sink &sink,
-                                            ParkedPoint *q)
+                                            ParkedPoint *q, int tslot = 0)
 {
     // Active warps: a launch with few pixels per lane runs like a thread-per-pixel kernel
     // (every warp waits for its slowest lane and there is nothing to refill from), so only
@@ -132,14 +144,30 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
     // B200), below which one warp per scheduler is latency-bound.  Warp w of block b has
     // rank w*gridDim+b, so the active warps spread over all SMs.  (Idle warps return here and
     // still reach the caller's block-wide reductions.)
-    constexpr uint32_t PPL = 8;
+    // At most WPS warps per sub-partition work at all: the chunk loop has two independent
+    // 12-cycle dependency chains per step, so ~3 warps already saturate a scheduler's issue
+    // slot, while every extra resident warp stretches the latency of a long (maxdwell) pixel
+    // -- and a level ends only when its last long pixel does.
+#ifndef MANDEL_RF_PPL
+#define MANDEL_RF_PPL 8
+#endif
+#ifndef MANDEL_RF_MINW
+#define MANDEL_RF_MINW 2
+#endif
+    constexpr uint32_t PPL = MANDEL_RF_PPL;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    const uint32_t min_active = 8u * (uint32_t)c_num_sms;
+    const uint32_t min_active = (uint32_t)(4 * MANDEL_RF_MINW) * (uint32_t)c_num_sms;
+    const uint32_t max_active = (uint32_t)(4 * WPS) * (uint32_t)c_num_sms;
     uint32_t active = total / (32u * PPL);
     active = active < min_active ? min_active : active;
+    active = active > max_active ? max_active : active;
     active = active > nwarps ? nwarps : active;
-    if ((threadIdx.x >> 5) * gridDim.x + blockIdx.x >= active)
+    const uint32_t wrank = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+    if (wrank >= active)
         return;
+#ifdef MANDEL_RF_TRACE
+    unsigned long long tr_start = rf_now(), tr_ex = 0, tr_px = 0;
+#endif
     uint32_t grab = total / (4u * active);
     grab = grab < 8u ? 8u : (grab > (uint32_t)CH ? (uint32_t)CH : grab);
     const unsigned FULL = 0xffffffffu;
@@ -180,16 +208,28 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
         unsigned need = __ballot_sync(FULL, !has);
         while (need && !exhausted) {
             if (pos >= end) {
+                // guided self-scheduling: a grab is a quarter of the remaining work's fair
+                // share (so the last windows are small and the level ends together)
                 unsigned long long b = 0;
-                if (lane == 0)
-                    b = atomicAdd(cursor, (unsigned long long)grab);
+                uint32_t gsz = 0;
+                if (lane == 0) {
+                    const unsigned long long cur = *((volatile unsigned long long *)cursor);
+                    const uint32_t rem = cur < total ? (uint32_t)(total - cur) : 0u;
+                    gsz = rem / (4u * active);
+                    gsz = gsz < 8u ? 8u : (gsz > grab ? grab : gsz);
+                    b = atomicAdd(cursor, (unsigned long long)gsz);
+                }
                 b = __shfl_sync(FULL, b, 0);
+                gsz = __shfl_sync(FULL, gsz, 0);
                 if (b >= total) {
                     exhausted = true;
+#ifdef MANDEL_RF_TRACE
+                    tr_ex = rf_now();
+#endif
                     break;
                 }
                 pos = (uint32_t)b;
-                end = (uint32_t)min(b + (unsigned long long)grab, (unsigned long long)total);
+                end = (uint32_t)min(b + (unsigned long long)gsz, (unsigned long long)total);
             }
             const unsigned cnt = __popc(need);
             const unsigned avail = end - pos;
@@ -209,6 +249,9 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
                 }
             }
             pos += take;
+#ifdef MANDEL_RF_TRACE
+            tr_px += take;
+#endif
             need = __ballot_sync(FULL, !has);
         }
         const unsigned active = __ballot_sync(FULL, has);
@@ -238,6 +281,14 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
     // drain the queue
     if (qn > 0)
         replay_batch<K>(q, qn, pm, md, sink);
+#ifdef MANDEL_RF_TRACE
+    if (lane == 0 && wrank < 8192 && tslot >= 0 && tslot < 16) {
+        g_rf_trace[tslot][wrank][0] = tr_start;
+        g_rf_trace[tslot][wrank][1] = tr_ex;
+        g_rf_trace[tslot][wrank][2] = rf_now();
+        g_rf_trace[tslot][wrank][3] = tr_px | ((unsigned long long)active << 40);
+    }
+#endif
 }
 
 } // namespace mandel
