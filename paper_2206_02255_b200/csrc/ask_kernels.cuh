@@ -42,16 +42,14 @@ constexpr int DWELL_K = 8;                 // iterations per escape test (dwell.
 #ifndef MANDEL_RFL_CH
 #define MANDEL_RFL_CH 128
 #endif
-#ifndef MANDEL_RF_WPS
-#define MANDEL_RF_WPS 4 // border: max working warps per SM sub-partition
-#endif
-#ifndef MANDEL_RFL_WPS
-#define MANDEL_RFL_WPS 12 // leaf
-#endif
 #ifndef MANDEL_RF_MINB
 #define MANDEL_RF_MINB 6
 #endif
-constexpr int RF_MINB = MANDEL_RF_MINB; // resident 256-thread blocks per SM (register cap)
+#ifndef MANDEL_RF_TPB
+#define MANDEL_RF_TPB 256
+#endif
+constexpr int RF_TPB = MANDEL_RF_TPB;                    // threads per refill block
+constexpr int RF_MINB = MANDEL_RF_MINB * (256 / RF_TPB); // resident blocks per SM (register cap)
 
 struct WsHeader {
     uint32_t magic, levels, n, g, r, B, ntiles, scheme; // written by k_init
@@ -675,19 +673,19 @@ __device__ __forceinline__ void sink_flush(const StoreSink<STATS, RING> &sk, uns
 {
     if (!STATS)
         return;
-    __shared__ unsigned long long s_sum[8];
-    const unsigned long long it = block_sum_u64<256>(sk.iters, s_sum);
+    __shared__ unsigned long long s_sum[RF_TPB / 32];
+    const unsigned long long it = block_sum_u64<RF_TPB>(sk.iters, s_sum);
     if (threadIdx.x == 0 && it)
         atomicAdd(it_dst, it);
-    const unsigned long long px = block_sum_u64<256>(sk.px, s_sum);
+    const unsigned long long px = block_sum_u64<RF_TPB>(sk.px, s_sum);
     if (threadIdx.x == 0 && px)
         atomicAdd(px_dst, px);
 }
 
 template <bool STATS>
-__global__ void __launch_bounds__(256, RF_MINB) k_b200_border_rf(LevelArgs a)
+__global__ void __launch_bounds__(RF_TPB, RF_MINB) k_b200_border_rf(LevelArgs a)
 {
-    __shared__ ParkedPoint s_q[8][RF_QCAP];
+    __shared__ ParkedPoint s_q[RF_TPB / 32][RF_QCAP];
     BorderMap map;
     map.olt = a.olt_in;
     map.nh = sub_hot(a);
@@ -704,16 +702,15 @@ __global__ void __launch_bounds__(256, RF_MINB) k_b200_border_rf(LevelArgs a)
                                     : *((volatile uint32_t *)&a.hdr->n_subdiv[a.level - 1]);
     const uint32_t total = map.fper.d * count;
     StoreSink<STATS, true> sink{&a, 0ull, 0ull};
-    refill_loop<MANDEL_RFB_K, MANDEL_RFB_T, MANDEL_RFB_CH, MANDEL_RF_WPS>(a.map, a.maxdwell, total, &a.hdr->cursor[a.level],
-                                                           map, sink,
-                                   s_q[threadIdx.x >> 5], a.level);
+    refill_loop<MANDEL_RFB_K, MANDEL_RFB_T, MANDEL_RFB_CH>(a.map, a.maxdwell, total, &a.hdr->cursor[a.level], map,
+                                                           sink, s_q[threadIdx.x >> 5], a.level);
     sink_flush<STATS, true>(sink, &a.hdr->border_iters[a.level], &a.hdr->border_px[a.level]);
 }
 
 template <bool STATS>
-__global__ void __launch_bounds__(256, RF_MINB) k_b200_leaf_rf(LevelArgs a)
+__global__ void __launch_bounds__(RF_TPB, RF_MINB) k_b200_leaf_rf(LevelArgs a)
 {
-    __shared__ ParkedPoint s_q[8][RF_QCAP];
+    __shared__ ParkedPoint s_q[RF_TPB / 32][RF_QCAP];
     LeafMap map;
     map.leaf = a.leaf;
     map.nh = leaf_hot(a);
@@ -723,9 +720,8 @@ __global__ void __launch_bounds__(256, RF_MINB) k_b200_leaf_rf(LevelArgs a)
     const uint32_t total = map.fI.d * *((volatile uint32_t *)&a.hdr->n_leaf);
     StoreSink<STATS, false> sink{&a, 0ull, 0ull};
     if (map.fI.d > 0)
-        refill_loop<MANDEL_RFL_K, MANDEL_RFL_T, MANDEL_RFL_CH, MANDEL_RFL_WPS>(a.map, a.maxdwell, total, &a.hdr->cursor[MAXL],
-                                                               map, sink,
-                                       s_q[threadIdx.x >> 5], 15);
+        refill_loop<MANDEL_RFL_K, MANDEL_RFL_T, MANDEL_RFL_CH>(a.map, a.maxdwell, total, &a.hdr->cursor[MAXL], map,
+                                                               sink, s_q[threadIdx.x >> 5], 15);
     sink_flush<STATS, false>(sink, &a.hdr->leaf_iters, &a.hdr->leaf_px);
 }
 

@@ -383,18 +383,18 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
                     k_b200_border<false><<<gsz, 256, 0, s>>>(a);
                 }
             } else { // lane refill: persistent warps, one per 32 pixels of work at most
-                const size_t rf_blocks = (work + 255) / 256;
+                const size_t rf_blocks = (work + RF_TPB - 1) / RF_TPB;
                 const uint32_t per = (l == 0) ? (uint32_t)(4 * d - 4) : new_border_px_per_parent(d * k.r, k.r);
                 a.fd[0] = fastdiv_nz(per);
                 a.fd[1] = fastdiv_nz((uint32_t)(d * k.r - 2));
                 a.fd[2] = fastdiv_nz((uint32_t)(d - 2));
                 a.fd[3] = fastdiv_nz((uint32_t)(k.r * (d - 2)));
                 if (stats) {
-                    int gsz = resident_grid(k_b200_border_rf<true>, 256, sms, rf_blocks);
-                    k_b200_border_rf<true><<<gsz, 256, 0, s>>>(a);
+                    int gsz = resident_grid(k_b200_border_rf<true>, RF_TPB, sms, rf_blocks);
+                    k_b200_border_rf<true><<<gsz, RF_TPB, 0, s>>>(a);
                 } else {
-                    int gsz = resident_grid(k_b200_border_rf<false>, 256, sms, rf_blocks);
-                    k_b200_border_rf<false><<<gsz, 256, 0, s>>>(a);
+                    int gsz = resident_grid(k_b200_border_rf<false>, RF_TPB, sms, rf_blocks);
+                    k_b200_border_rf<false><<<gsz, RF_TPB, 0, s>>>(a);
                 }
             }
             CK(cudaGetLastError());
@@ -478,11 +478,11 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
                 a.fd[0] = fastdiv_nz((uint32_t)((d - 2) * (d - 2)));
                 a.fd[1] = fastdiv_nz((uint32_t)(d - 2));
                 if (stats) {
-                    int gsz = resident_grid(k_b200_leaf_rf<true>, 256, sms, blocks);
-                    k_b200_leaf_rf<true><<<gsz, 256, 0, s>>>(a);
+                    int gsz = resident_grid(k_b200_leaf_rf<true>, RF_TPB, sms, blocks * (256 / RF_TPB));
+                    k_b200_leaf_rf<true><<<gsz, RF_TPB, 0, s>>>(a);
                 } else {
-                    int gsz = resident_grid(k_b200_leaf_rf<false>, 256, sms, blocks);
-                    k_b200_leaf_rf<false><<<gsz, 256, 0, s>>>(a);
+                    int gsz = resident_grid(k_b200_leaf_rf<false>, RF_TPB, sms, blocks * (256 / RF_TPB));
+                    k_b200_leaf_rf<false><<<gsz, RF_TPB, 0, s>>>(a);
                 }
             }
         }

@@ -133,7 +133,7 @@ __device__ __forceinline__ void replay_batch(const ParkedPoint *q, int cnt, cons
 // The grab size adapts to the launch: at most CH, but small enough that every warp of the
 // grid gets about 4 grabs (small levels -- e.g. one rank's share of a multi-GPU run -- would
 // otherwise leave most warps idle while a few run whole grabs of maxdwell pixels), and >= 8.
-template <int K, int T, int CH, int WPS, class Map, class Sink>
+template <int K, int T, int CH, class Map, class Sink>
 __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint32_t total,
                                             unsigned long long *cursor, const Map &map, Sink &sink,
                                             ParkedPoint *q, int tslot = 0)
@@ -144,23 +144,11 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
     // B200), below which one warp per scheduler is latency-bound.  Warp w of block b has
     // rank w*gridDim+b, so the active warps spread over all SMs.  (Idle warps return here and
     // still reach the caller's block-wide reductions.)
-    // At most WPS warps per sub-partition work at all: the chunk loop has two independent
-    // 12-cycle dependency chains per step, so ~3 warps already saturate a scheduler's issue
-    // slot, while every extra resident warp stretches the latency of a long (maxdwell) pixel
-    // -- and a level ends only when its last long pixel does.
-#ifndef MANDEL_RF_PPL
-#define MANDEL_RF_PPL 8
-#endif
-#ifndef MANDEL_RF_MINW
-#define MANDEL_RF_MINW 2
-#endif
-    constexpr uint32_t PPL = MANDEL_RF_PPL;
+    constexpr uint32_t PPL = 8;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    const uint32_t min_active = (uint32_t)(4 * MANDEL_RF_MINW) * (uint32_t)c_num_sms;
-    const uint32_t max_active = (uint32_t)(4 * WPS) * (uint32_t)c_num_sms;
+    const uint32_t min_active = 8u * (uint32_t)c_num_sms;
     uint32_t active = total / (32u * PPL);
     active = active < min_active ? min_active : active;
-    active = active > max_active ? max_active : active;
     active = active > nwarps ? nwarps : active;
     const uint32_t wrank = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
     if (wrank >= active)
@@ -208,19 +196,10 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
         unsigned need = __ballot_sync(FULL, !has);
         while (need && !exhausted) {
             if (pos >= end) {
-                // guided self-scheduling: a grab is a quarter of the remaining work's fair
-                // share (so the last windows are small and the level ends together)
                 unsigned long long b = 0;
-                uint32_t gsz = 0;
-                if (lane == 0) {
-                    const unsigned long long cur = *((volatile unsigned long long *)cursor);
-                    const uint32_t rem = cur < total ? (uint32_t)(total - cur) : 0u;
-                    gsz = rem / (4u * active);
-                    gsz = gsz < 8u ? 8u : (gsz > grab ? grab : gsz);
-                    b = atomicAdd(cursor, (unsigned long long)gsz);
-                }
+                if (lane == 0)
+                    b = atomicAdd(cursor, (unsigned long long)grab);
                 b = __shfl_sync(FULL, b, 0);
-                gsz = __shfl_sync(FULL, gsz, 0);
                 if (b >= total) {
                     exhausted = true;
 #ifdef MANDEL_RF_TRACE
@@ -229,7 +208,7 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
                     break;
                 }
                 pos = (uint32_t)b;
-                end = (uint32_t)min(b + (unsigned long long)gsz, (unsigned long long)total);
+                end = (uint32_t)min(b + (unsigned long long)grab, (unsigned long long)total);
             }
             const unsigned cnt = __popc(need);
             const unsigned avail = end - pos;
