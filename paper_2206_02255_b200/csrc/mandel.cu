@@ -555,7 +555,15 @@ int mandel_exhaustive(mandel_region reg, int64_t n, int32_t maxdwell, int32_t *d
     a.maxdwell = maxdwell;
     a.pitch = out_pitch;
     a.out = d_out;
-    constexpr int BX = 16, BY = 16;
+    // block shape of the flat Ex kernel (tuned on the box like the paper's Table 2 search,
+    // P:459-468; profiles/r01_tune_ex.txt)
+#ifndef MANDEL_EX_BX
+#define MANDEL_EX_BX 16
+#endif
+#ifndef MANDEL_EX_BY
+#define MANDEL_EX_BY 16
+#endif
+    constexpr int BX = MANDEL_EX_BX, BY = MANDEL_EX_BY;
     dim3 grid((unsigned)((n + BX - 1) / BX), (unsigned)((n + BY - 1) / BY));
     k_exhaustive<BX, BY><<<grid, dim3(BX, BY), 0, (cudaStream_t)stream>>>(a);
     CK(cudaGetLastError());

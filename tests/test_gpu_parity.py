@@ -166,7 +166,7 @@ def _sample_tiles(g, k, seed):
     return sorted(rng.choice(g * g, size=k, replace=False).tolist())
 
 
-@pytest.mark.parametrize("wname", ["C3", "C5"])
+@pytest.mark.parametrize("wname", ["C3", "C5", "C4"])
 def test_full_size_ask_sampled_tiles(mb, wname):
     """BASELINE C3 / C5 at full size in bench.py's launch configuration (all g*g tiles, B200
     scheme): sampled level-0 tiles equal the oracle's recursion on those tiles."""
@@ -176,7 +176,7 @@ def test_full_size_ask_sampled_tiles(mb, wname):
     torch.cuda.synchronize()
     st = mb.ask_stats(ws)
     d0 = w.n // w.g
-    tiles = _sample_tiles(w.g, 3, W.SEED + (3 if wname == "C3" else 5))
+    tiles = _sample_tiles(w.g, 2 if wname == "C4" else 3, W.SEED + int(wname[1]))
     for t in tiles:
         gy, gx = divmod(t, w.g)
         A, _ = oracle.ask_tile(w.region, w.n, w.maxdwell, w.g, w.r, w.B, t)
@@ -190,7 +190,7 @@ def test_full_size_ask_sampled_tiles(mb, wname):
         assert s["regions_in"] == s["filled"] + s["subdivided"] + s["leaves"]
 
 
-@pytest.mark.parametrize("wname", ["C3", "C5"])
+@pytest.mark.parametrize("wname", ["C3", "C5", "C4"])
 def test_full_size_exhaustive_sampled_pixels(mb, wname):
     w = W.CONFIGS[wname]
     out = mb.exhaustive(w.region, w.n, w.maxdwell)
