@@ -45,11 +45,30 @@ constexpr int DWELL_K = 8;                 // iterations per escape test (dwell.
 #ifndef MANDEL_RF_MINB
 #define MANDEL_RF_MINB 6
 #endif
+// Packed engine (refill_loop2, two pixels per lane on FMUL2/FADD2): on/off per kernel, T out
+// of 64 slots, resident blocks per SM.
+#ifndef MANDEL_RFB_PACK
+#define MANDEL_RFB_PACK 1
+#endif
+#ifndef MANDEL_RFL_PACK
+#define MANDEL_RFL_PACK 1
+#endif
+#ifndef MANDEL_RFB2_T
+#define MANDEL_RFB2_T 8
+#endif
+#ifndef MANDEL_RFL2_T
+#define MANDEL_RFL2_T 16
+#endif
+#ifndef MANDEL_RF2_MINB
+#define MANDEL_RF2_MINB 3
+#endif
 #ifndef MANDEL_RF_TPB
 #define MANDEL_RF_TPB 256
 #endif
 constexpr int RF_TPB = MANDEL_RF_TPB;                    // threads per refill block
 constexpr int RF_MINB = MANDEL_RF_MINB * (256 / RF_TPB); // resident blocks per SM (register cap)
+constexpr int RFB_MINB = MANDEL_RFB_PACK ? MANDEL_RF2_MINB * (256 / RF_TPB) : RF_MINB;
+constexpr int RFL_MINB = MANDEL_RFL_PACK ? MANDEL_RF2_MINB * (256 / RF_TPB) : RF_MINB;
 
 struct WsHeader {
     uint32_t magic, levels, n, g, r, B, ntiles, scheme; // written by k_init
@@ -683,9 +702,9 @@ __device__ __forceinline__ void sink_flush(const StoreSink<STATS, RING> &sk, uns
 }
 
 template <bool STATS>
-__global__ void __launch_bounds__(RF_TPB, RF_MINB) k_b200_border_rf(LevelArgs a)
+__global__ void __launch_bounds__(RF_TPB, RFB_MINB) k_b200_border_rf(LevelArgs a)
 {
-    __shared__ ParkedPoint s_q[RF_TPB / 32][RF_QCAP];
+    __shared__ ParkedPoint s_q[RF_TPB / 32][MANDEL_RFB_PACK ? RF2_QCAP : RF_QCAP];
     BorderMap map;
     map.olt = a.olt_in;
     map.nh = sub_hot(a);
@@ -702,15 +721,20 @@ __global__ void __launch_bounds__(RF_TPB, RF_MINB) k_b200_border_rf(LevelArgs a)
                                     : *((volatile uint32_t *)&a.hdr->n_subdiv[a.level - 1]);
     const uint32_t total = map.fper.d * count;
     StoreSink<STATS, true> sink{&a, 0ull, 0ull};
+#if MANDEL_RFB_PACK
+    refill_loop2<MANDEL_RFB_K, MANDEL_RFB2_T, MANDEL_RFB_CH>(a.map, a.maxdwell, total, &a.hdr->cursor[a.level], map,
+                                                             sink, s_q[threadIdx.x >> 5], a.level);
+#else
     refill_loop<MANDEL_RFB_K, MANDEL_RFB_T, MANDEL_RFB_CH>(a.map, a.maxdwell, total, &a.hdr->cursor[a.level], map,
                                                            sink, s_q[threadIdx.x >> 5], a.level);
+#endif
     sink_flush<STATS, true>(sink, &a.hdr->border_iters[a.level], &a.hdr->border_px[a.level]);
 }
 
 template <bool STATS>
-__global__ void __launch_bounds__(RF_TPB, RF_MINB) k_b200_leaf_rf(LevelArgs a)
+__global__ void __launch_bounds__(RF_TPB, RFL_MINB) k_b200_leaf_rf(LevelArgs a)
 {
-    __shared__ ParkedPoint s_q[RF_TPB / 32][RF_QCAP];
+    __shared__ ParkedPoint s_q[RF_TPB / 32][MANDEL_RFL_PACK ? RF2_QCAP : RF_QCAP];
     LeafMap map;
     map.leaf = a.leaf;
     map.nh = leaf_hot(a);
@@ -720,8 +744,13 @@ __global__ void __launch_bounds__(RF_TPB, RF_MINB) k_b200_leaf_rf(LevelArgs a)
     const uint32_t total = map.fI.d * *((volatile uint32_t *)&a.hdr->n_leaf);
     StoreSink<STATS, false> sink{&a, 0ull, 0ull};
     if (map.fI.d > 0)
+#if MANDEL_RFL_PACK
+        refill_loop2<MANDEL_RFL_K, MANDEL_RFL2_T, MANDEL_RFL_CH>(a.map, a.maxdwell, total, &a.hdr->cursor[MAXL],
+                                                                 map, sink, s_q[threadIdx.x >> 5], 15);
+#else
         refill_loop<MANDEL_RFL_K, MANDEL_RFL_T, MANDEL_RFL_CH>(a.map, a.maxdwell, total, &a.hdr->cursor[MAXL], map,
                                                                sink, s_q[threadIdx.x >> 5], 15);
+#endif
     sink_flush<STATS, false>(sink, &a.hdr->leaf_iters, &a.hdr->leaf_px);
 }
 

@@ -270,4 +270,294 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
 #endif
 }
 
+
+// ============================================================================ packed engine
+// Two pixels per lane on the packed FP32 instructions of sm_100 (FMUL2 / FADD2: one issue
+// slot drives the FP32 pipe for two lanes' worth of work).  The scalar engine above is
+// issue-bound (ncu: 95% of issue slots busy, 27% of them non-FP32 bookkeeping), so halving
+// the FP32 issue count lets the bookkeeping of one warp issue while the pipe works on
+// another's packed steps.  Each lane owns two independent slots (pixels) whose state lives
+// in the two halves of 64-bit register pairs; per slot the algorithm is exactly the scalar
+// engine's (same chunked test, parking, bisection replay), with 64 slots per warp.
+// mul.rn.f32x2 / add.rn.f32x2 / sub.rn.f32x2 are IEEE RN per half: bit-identical to the
+// scalar __fmul_rn / __fadd_rn / __fsub_rn sequence (R4).
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t f2_pack(float lo, float hi)
+{
+    f2_t d;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
+    return d;
+}
+__device__ __forceinline__ void f2_unpack(f2_t v, float &lo, float &hi)
+{
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b)
+{
+    f2_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f2_t f2_sub(f2_t a, f2_t b)
+{
+    f2_t d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+// Products are fma.rn.f32x2(a, b, -0) = RN(a*b) exactly (x*y + -0 == x*y for every x*y,
+// including +-0), with the -0 pair read from constant memory so ptxas cannot see it: ptxas
+// 12.9 contracts mul.rn.f32x2 followed by add/sub.rn.f32x2 into FFMA2 even under
+// --fmad=false (observed: x*x - y2 fused), which changes the rounding and the dwells.
+__constant__ f2_t c_f2_negzero = 0x8000000080000000ull;
+__device__ __forceinline__ f2_t f2_mul(f2_t a, f2_t b)
+{
+    f2_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c_f2_negzero));
+    return d;
+}
+// The dwell step of dwell.cuh on both halves (same operation order).
+#define MANDEL_STEP2(X, Y, X2, Y2, CR, CI)                                                    \
+    do {                                                                                       \
+        const f2_t xy_ = f2_mul((X), (Y));                                                     \
+        (X) = f2_add(f2_sub((X2), (Y2)), (CR));                                                \
+        (Y) = f2_add(f2_add(xy_, xy_), (CI));                                                  \
+        (X2) = f2_mul((X), (X));                                                               \
+        (Y2) = f2_mul((Y), (Y));                                                               \
+    } while (0)
+
+constexpr int RF2_QCAP = 128; // per-warp queue entries (< 64 left over + <= 64 new)
+
+// replay_batch on up to 64 queued points, two per lane (q[lane] low half, q[lane+32] high).
+template <int K, class Sink>
+__device__ __forceinline__ void replay_batch2(const ParkedPoint *q, int cnt, const PixMap &pm, unsigned md,
+                                              Sink &sink)
+{
+    static_assert((K & (K - 1)) == 0, "K must be a power of two");
+    const int lane = threadIdx.x & 31;
+    const bool v0 = lane < cnt, v1 = lane + 32 < cnt;
+    if (v0) {
+        ParkedPoint p0 = q[lane], p1 = p0;
+        if (v1)
+            p1 = q[lane + 32];
+        const f2_t CR = f2_pack(pix_re(pm, p0.px), pix_re(pm, p1.px));
+        const f2_t CI = f2_pack(pix_im(pm, p0.py), pix_im(pm, p1.py));
+        f2_t BX = f2_pack(p0.x, p1.x), BY = f2_pack(p0.y, p1.y);
+        f2_t BX2 = f2_mul(BX, BX), BY2 = f2_mul(BY, BY); // as the chunk start had them
+        unsigned lo0 = p0.it, lo1 = p1.it;
+#pragma unroll
+        for (int h = K / 2; h >= 1; h /= 2) {
+            f2_t X = BX, Y = BY, X2 = BX2, Y2 = BY2;
+#pragma unroll
+            for (int k = 0; k < h; ++k)
+                MANDEL_STEP2(X, Y, X2, Y2, CR, CI);
+            float m0, m1;
+            f2_unpack(f2_add(X2, Y2), m0, m1);
+            const bool hit0 = !(m0 <= 4.0f) || lo0 + (unsigned)h >= md;
+            const bool hit1 = !(m1 <= 4.0f) || lo1 + (unsigned)h >= md;
+            float a0, a1, b0, b1;
+            // advance the halves whose first hit lies beyond lo + h
+            f2_unpack(X, a0, a1);
+            f2_unpack(BX, b0, b1);
+            BX = f2_pack(hit0 ? b0 : a0, hit1 ? b1 : a1);
+            f2_unpack(Y, a0, a1);
+            f2_unpack(BY, b0, b1);
+            BY = f2_pack(hit0 ? b0 : a0, hit1 ? b1 : a1);
+            f2_unpack(X2, a0, a1);
+            f2_unpack(BX2, b0, b1);
+            BX2 = f2_pack(hit0 ? b0 : a0, hit1 ? b1 : a1);
+            f2_unpack(Y2, a0, a1);
+            f2_unpack(BY2, b0, b1);
+            BY2 = f2_pack(hit0 ? b0 : a0, hit1 ? b1 : a1);
+            lo0 += hit0 ? 0u : (unsigned)h;
+            lo1 += hit1 ? 0u : (unsigned)h;
+        }
+        sink(p0.px, p0.py, (int)(lo0 + 1u));
+        if (v1)
+            sink(p1.px, p1.py, (int)(lo1 + 1u));
+    }
+    __syncwarp();
+}
+
+// Fetch flat index t into one slot: pixel, c, and the zero orbit; pixels with |c|^2 > 3.9
+// run the per-step loop here and leave the slot empty.
+template <int K, class Map, class Sink>
+__device__ __forceinline__ bool rf2_fetch(uint32_t t, const PixMap &pm, int maxdwell, const Map &map, Sink &sink,
+                                          int &px, int &py, float &cr, float &ci)
+{
+    map(t, px, py);
+    cr = pix_re(pm, px);
+    ci = pix_im(pm, py);
+    const float c2 = __fadd_rn(__fmul_rn(cr, cr), __fmul_rn(ci, ci));
+    if (c2 <= 3.9f)
+        return true;
+    sink(px, py, dwell_per_step<K>(cr, ci, maxdwell));
+    return false;
+}
+
+// Same contract as refill_loop (Map, Sink, cursor, launch shape); q: RF2_QCAP entries.
+// T counts parked slots out of the warp's 64.
+template <int K, int T, int CH, class Map, class Sink>
+__device__ __forceinline__ void refill_loop2(const PixMap &pm, int maxdwell, uint32_t total,
+                                             unsigned long long *cursor, const Map &map, Sink &sink,
+                                             ParkedPoint *q, int tslot = 0)
+{
+    constexpr uint32_t PPL = 8; // pixels per slot before a warp is worth activating
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t min_active = 8u * (uint32_t)c_num_sms;
+    uint32_t active = total / (64u * PPL);
+    active = active < min_active ? min_active : active;
+    active = active > nwarps ? nwarps : active;
+    const uint32_t wrank = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+    if (wrank >= active)
+        return;
+#ifdef MANDEL_RF_TRACE
+    unsigned long long tr_start = rf_now(), tr_ex = 0, tr_px = 0;
+#endif
+    uint32_t grab = total / (4u * active);
+    grab = grab < 8u ? 8u : (grab > (uint32_t)CH ? (uint32_t)CH : grab);
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned md = (unsigned)maxdwell;
+
+    uint32_t pos = 0, end = 0;
+    bool exhausted = false;
+    int qn = 0;
+
+    bool has0 = false, has1 = false, fin0 = false, fin1 = false;
+    int px0 = 0, py0 = 0, px1 = 0, py1 = 0;
+    unsigned it0 = 0, it1 = 0, sit0 = 0, sit1 = 0;
+    float sx0 = 0.f, sy0 = 0.f, sx1 = 0.f, sy1 = 0.f;
+    f2_t X = 0, Y = 0, X2 = 0, Y2 = 0, CR = 0, CI = 0;
+
+    while (true) {
+        // ---------------------------------------------------------------- park + refill
+        const unsigned f0 = __ballot_sync(FULL, fin0), f1 = __ballot_sync(FULL, fin1);
+        if (f0 | f1) {
+            const int n0 = __popc(f0);
+            if (fin0) {
+                ParkedPoint &e = q[qn + __popc(f0 & lt)];
+                e.px = px0;
+                e.py = py0;
+                e.x = sx0;
+                e.y = sy0;
+                e.it = sit0;
+                has0 = false;
+                fin0 = false;
+            }
+            if (fin1) {
+                ParkedPoint &e = q[qn + n0 + __popc(f1 & lt)];
+                e.px = px1;
+                e.py = py1;
+                e.x = sx1;
+                e.y = sy1;
+                e.it = sit1;
+                has1 = false;
+                fin1 = false;
+            }
+            qn += n0 + __popc(f1);
+            __syncwarp();
+            if (qn >= 64) {
+                qn -= 64;
+                replay_batch2<K>(q + qn, 64, pm, md, sink);
+            }
+        }
+        unsigned need0 = __ballot_sync(FULL, !has0), need1 = __ballot_sync(FULL, !has1);
+        while ((need0 | need1) && !exhausted) {
+            if (pos >= end) {
+                unsigned long long b = 0;
+                if (lane == 0)
+                    b = atomicAdd(cursor, (unsigned long long)grab);
+                b = __shfl_sync(FULL, b, 0);
+                if (b >= total) {
+                    exhausted = true;
+#ifdef MANDEL_RF_TRACE
+                    tr_ex = rf_now();
+#endif
+                    break;
+                }
+                pos = (uint32_t)b;
+                end = (uint32_t)min(b + (unsigned long long)grab, (unsigned long long)total);
+            }
+            const unsigned c0 = __popc(need0);
+            const unsigned cnt = c0 + __popc(need1);
+            const unsigned avail = end - pos;
+            const unsigned take = avail < cnt ? avail : cnt;
+            const unsigned r0 = __popc(need0 & lt), r1 = c0 + __popc(need1 & lt);
+            float cr0, ci0, cr1, ci1;
+            f2_unpack(CR, cr0, cr1);
+            f2_unpack(CI, ci0, ci1);
+            bool new0 = false, new1 = false;
+            if (!has0 && r0 < take)
+                new0 = has0 = rf2_fetch<K>(pos + r0, pm, maxdwell, map, sink, px0, py0, cr0, ci0);
+            if (!has1 && r1 < take)
+                new1 = has1 = rf2_fetch<K>(pos + r1, pm, maxdwell, map, sink, px1, py1, cr1, ci1);
+            if (new0 | new1) {
+                CR = f2_pack(cr0, cr1);
+                CI = f2_pack(ci0, ci1);
+                float a0, a1;
+#define RF2_ZERO(V)                                                                            \
+    f2_unpack(V, a0, a1);                                                                      \
+    V = f2_pack(new0 ? 0.0f : a0, new1 ? 0.0f : a1);
+                RF2_ZERO(X)
+                RF2_ZERO(Y)
+                RF2_ZERO(X2)
+                RF2_ZERO(Y2)
+#undef RF2_ZERO
+                it0 = new0 ? 0u : it0;
+                it1 = new1 ? 0u : it1;
+            }
+            pos += take;
+#ifdef MANDEL_RF_TRACE
+            tr_px += take;
+#endif
+            need0 = __ballot_sync(FULL, !has0);
+            need1 = __ballot_sync(FULL, !has1);
+        }
+        const unsigned a0m = __ballot_sync(FULL, has0), a1m = __ballot_sync(FULL, has1);
+        if (!(a0m | a1m))
+            break; // cursor exhausted and every slot idle
+        // ---------------------------------------------------------------- compute
+        const int thresh = exhausted ? 64 : T;
+        const bool live0 = has0, live1 = has1;
+        while (true) {
+            float xl, xh, yl, yh;
+            f2_unpack(X, xl, xh);
+            f2_unpack(Y, yl, yh);
+            const bool keep0 = fin0 || !live0, keep1 = fin1 || !live1;
+            sx0 = keep0 ? sx0 : xl;
+            sy0 = keep0 ? sy0 : yl;
+            sit0 = keep0 ? sit0 : it0;
+            sx1 = keep1 ? sx1 : xh;
+            sy1 = keep1 ? sy1 : yh;
+            sit1 = keep1 ? sit1 : it1;
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+                MANDEL_STEP2(X, Y, X2, Y2, CR, CI);
+            it0 += K;
+            it1 += K;
+            float m0, m1;
+            f2_unpack(f2_add(X2, Y2), m0, m1);
+            fin0 = live0 && (fin0 || !(m0 <= 4.0f) || it0 >= md);
+            fin1 = live1 && (fin1 || !(m1 <= 4.0f) || it1 >= md);
+            const unsigned g0 = __ballot_sync(FULL, fin0), g1 = __ballot_sync(FULL, fin1);
+            if ((g0 == a0m && g1 == a1m) || __popc(g0) + __popc(g1) >= thresh)
+                break;
+        }
+    }
+    while (qn > 0) { // drain the queue
+        const int c = qn < 64 ? qn : 64;
+        qn -= c;
+        replay_batch2<K>(q + qn, c, pm, md, sink);
+    }
+#ifdef MANDEL_RF_TRACE
+    if (lane == 0 && wrank < 8192 && tslot >= 0 && tslot < 16) {
+        g_rf_trace[tslot][wrank][0] = tr_start;
+        g_rf_trace[tslot][wrank][1] = tr_ex;
+        g_rf_trace[tslot][wrank][2] = rf_now();
+        g_rf_trace[tslot][wrank][3] = tr_px | ((unsigned long long)active << 40);
+    }
+#endif
+}
+
 } // namespace mandel

@@ -46,8 +46,16 @@ def test_no_fma_in_dwell_kernels():
     for f in funcs[1:]:
         name = f.split("\n", 1)[0]
         if any(k in name for k in ("k_exhaustive", "k_sbr_level", "k_sbr_leaf", "k_b200_border", "k_b200_leaf")):
-            assert "FFMA" not in f, name
-            assert "FMUL" in f and "FADD" in f, name
+            # no scalar FFMA at all
+            assert re.search(r"\bFFMA\b", f) is None, name
+            # packed engine: every FFMA2 is a product fma(a, b, -0) whose addend is the
+            # -0 pair from constant memory (a uniform register), never a fused x*x - y2
+            ffma2 = re.findall(r"FFMA2 ([^;]*);", f)
+            for ins in ffma2:
+                addend = ins.split(",")[-1].strip()
+                assert addend.startswith("UR") and not addend.startswith("-"), (name, ins)
+            assert "FMUL2" not in f, name  # products only through the opaque -0 fma
+            assert ("FMUL" in f and "FADD" in f) or (ffma2 and "FADD2" in f), name
             checked += 1
     assert checked >= 5
 
