@@ -174,7 +174,7 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="C3", choices=sorted(W.CONFIGS))
-    ap.add_argument("--scheme", default="b200", choices=["b200", "sbr"])
+    ap.add_argument("--scheme", default="b200", choices=["b200", "sbr", "mbr"])
     ap.add_argument("--deal", default="costrank", choices=["costrank", "cyclic", "diagonal"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -349,7 +349,7 @@ def main():
     kt_sum = {k: sum(v) / args.steps for k, v in ktime.items()}
     kt_launches = {k: len(v) / args.steps for k, v in ktime.items()}
     dwell_kinds = {"b200_border": border_iters, "b200_leaf": leaf_iters, "sbr_level": border_iters,
-                   "sbr_leaf": leaf_iters}
+                   "sbr_leaf": leaf_iters, "mbr_leaf": leaf_iters}
     dom = max((k for k in kt_sum if k in dwell_kinds), key=lambda k: kt_sum[k])
     achieved = FLOPS_PER_ITER * dwell_kinds[dom] / (kt_sum[dom] / 1e3) / 1e12
     traffic = None

@@ -77,20 +77,28 @@ enum {
     MANDEL_ECUDA = 3
 };
 
-/* Scheme of the subdivision kernels.  Both produce bit-identical images.
- *   MANDEL_SCHEME_SBR   the paper's ASK-SBR: per level one CUDA
- *                       block per region computes the region's whole border (split across
- *                       its warps, reduced with warp reductions), then appends to the fill
- *                       list / next-level offset list / leaf list; leaves: one block each.
+/* Scheme of the subdivision kernels.  All produce bit-identical images.
+ *   MANDEL_SCHEME_SBR   the paper's ASK-SBR, "single block per region" (P:296-302,
+ *                       P:366-377): per level one CUDA kernel in which one block per region
+ *                       computes the region's whole border (query Q, split across its
+ *                       warps, reduced with warp reductions), appends to the next-level
+ *                       offset list or the leaf list (PS), and fills the region itself when
+ *                       the border is uniform (Delta[T]); leaves: one block each (Delta[L]).
+ *                       1 + L + 1 kernels per call.
  *   MANDEL_SCHEME_B200  B200 re-design: border dwells are written to the
  *                       image and reused -- a child only computes the new internal division
  *                       lines of its parent -- by a flat, load-balanced kernel over all new
  *                       border pixels of the level; a warp per region then decides
  *                       uniformity from the image with warp reductions; leaf interiors run
- *                       as one flat pixel-parallel kernel.                                */
+ *                       as one flat pixel-parallel kernel.  1 + 3L + 1 kernels.
+ *   MANDEL_SCHEME_MBR   the paper's ASK-MBR, "multiple blocks per region": Q and
+ *                       PS as in SBR (block per region), terminal work T and leaf work L as
+ *                       flat multi-block kernels over all regions of the level (nabla[T],
+ *                       nabla[L]), one thread per pixel.  1 + 2L + 1 kernels.          */
 enum {
     MANDEL_SCHEME_SBR = 0,
-    MANDEL_SCHEME_B200 = 1
+    MANDEL_SCHEME_B200 = 1,
+    MANDEL_SCHEME_MBR = 2
 };
 
 /* flags */
@@ -119,8 +127,9 @@ enum {
     MANDEL_KIND_B200_CLASSIFY = 2, /* warp-per-region uniformity test + list appends          */
     MANDEL_KIND_FILL = 3,          /* fill of the level's uniform regions                     */
     MANDEL_KIND_B200_LEAF = 4,     /* leaf interiors, flat                                    */
-    MANDEL_KIND_SBR_LEVEL = 5,     /* paper SBR: block-per-region border + decision           */
-    MANDEL_KIND_SBR_LEAF = 6       /* paper SBR: block-per-leaf interior                      */
+    MANDEL_KIND_SBR_LEVEL = 5,     /* paper SBR/MBR: block-per-region border + decision       */
+    MANDEL_KIND_SBR_LEAF = 6,      /* paper SBR: block-per-leaf interior                      */
+    MANDEL_KIND_MBR_LEAF = 7       /* paper MBR: leaf interiors, flat multi-block             */
 };
 
 /* Bytes of workspace mandel_ask / mandel_ask_tiles need for these parameters (worst case

@@ -132,6 +132,7 @@ struct LevelArgs {
     int level, d, r, B, g, ntiles, levels, scheme;
     int subdivide;           // d / r >= B
     int log2_q4, log2_row4;  // fill: log2(d*d/4), log2(d/4)
+    int fill_vec;            // SBR in-block fill: rows 16-byte aligned and d % 4 == 0
     unsigned long long *tile_cost; // MANDEL_FLAG_TILE_COST: iterations per level-0 tile
     int d0;                  // level-0 side
     // Column lines, transposed (B200 scheme, leaf side u >= 8): every pixel
@@ -283,11 +284,14 @@ __global__ void k_init(LevelArgs a)
 // level's count (compact concurrent insertion; hot parents from the front of the
 // buffer, cold ones from the back); else -> leaf list.
 // Returns the reserved parent slot (or UINT_MAX) to the caller's lane/thread.
-__device__ __forceinline__ uint32_t decide(const LevelArgs &a, uint32_t off, int lo, int hi)
+// fill_list = false: the caller fills the region itself (ASK-SBR's Delta[T]) and
+// only the count is kept.
+__device__ __forceinline__ uint32_t decide(const LevelArgs &a, uint32_t off, int lo, int hi, bool fill_list = true)
 {
     if (lo == hi) {
         const uint32_t e = atomicAdd(&a.hdr->n_fill[a.level], 1u);
-        a.fill[e] = make_uint2(off, (uint32_t)lo);
+        if (fill_list)
+            a.fill[e] = make_uint2(off, (uint32_t)lo);
         return UINT_MAX;
     }
     const bool hot = 2 * hi >= a.maxdwell;
@@ -305,17 +309,41 @@ __device__ __forceinline__ uint32_t decide(const LevelArgs &a, uint32_t off, int
     return UINT_MAX;
 }
 
-// --------------------------------------------------------------------------- SBR scheme
-// ASK-SBR level kernel: one block of TPB threads per region
-// (persistent, grid-stride over the level's OLT).  The block's warps split the region's
-// 4d-4 border pixels, write their dwells to the image (they are final values), and reduce
-// (min, max) with warp reductions + shared memory; uniform iff min == max.
-template <int TPB, bool STATS>
+// --------------------------------------------------------------------------- SBR / MBR
+// The block of TPB threads that decided region (x0, y0, d) uniform writes v to all its d*d
+// pixels (the ring already holds v): 128-bit stores when the rows are 16-byte aligned.
+template <int TPB>
+__device__ __forceinline__ void block_fill_region(const LevelArgs &a, int x0, int y0, int d, int v, bool vec)
+{
+    if (vec) {
+        const int q = d >> 2; // int4 per row
+        const int4 v4 = make_int4(v, v, v, v);
+        for (int t = threadIdx.x; t < d * q; t += TPB) {
+            const int row = t / q, c = t - row * q;
+            __stcs(reinterpret_cast<int4 *>(a.out + (long long)(y0 + row) * a.pitch + x0) + c, v4);
+        }
+    } else {
+        for (int t = threadIdx.x; t < d * d; t += TPB) {
+            const int row = t / d, c = t - row * d;
+            a.out[(long long)(y0 + row) * a.pitch + x0 + c] = v;
+        }
+    }
+}
+
+// ASK level kernel of the paper's two schemes: one block of TPB
+// threads per region (persistent, grid-stride over the level's OLT).  The block's warps
+// split the region's 4d-4 border pixels (query Q), write their dwells to the image (they
+// are final values), and reduce (min, max) with warp reductions + shared memory; uniform
+// iff min == max; thread 0 appends (PS).  FILL (ASK-SBR, Delta[(1-P) T]): the same block
+// then fills a uniform region.  !FILL (ASK-MBR, nabla[(1-P) T]): uniform regions go to the
+// level's fill list for the flat multi-block k_fill.
+template <int TPB, bool STATS, bool FILL = false>
 __global__ void __launch_bounds__(TPB) k_sbr_level(LevelArgs a)
 {
     __shared__ int s_lo[TPB / 32], s_hi[TPB / 32];
     __shared__ unsigned long long s_sum[TPB / 32];
     __shared__ uint32_t s_base;
+    __shared__ int s_fillv;
     const uint32_t count = level_count(a);
     const int d = a.d, ring = 4 * d - 4, s = d / a.r, rr = a.r * a.r;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -351,7 +379,8 @@ __global__ void __launch_bounds__(TPB) k_sbr_level(LevelArgs a)
                 lo = min(lo, s_lo[i]);
                 hi = max(hi, s_hi[i]);
             }
-            s_base = decide(a, off, lo, hi);
+            s_base = decide(a, off, lo, hi, !FILL);
+            s_fillv = (lo == hi) ? lo : INT_MIN;
             if (STATS) {
                 atomicAdd(&a.hdr->border_px[a.level], (unsigned long long)ring);
                 atomicAdd(&a.hdr->border_iters[a.level], it);
@@ -362,6 +391,8 @@ __global__ void __launch_bounds__(TPB) k_sbr_level(LevelArgs a)
         if (base != UINT_MAX)
             for (int t = threadIdx.x; t < rr; t += TPB)
                 a.olt_out[(size_t)base * rr + t] = pack_xy(x0 + (t % a.r) * s, y0 + (t / a.r) * s);
+        if (FILL && s_fillv != INT_MIN)
+            block_fill_region<TPB>(a, x0, y0, d, s_fillv, a.fill_vec != 0);
         __syncthreads();
     }
 }

@@ -285,7 +285,8 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
 {
     const int ntiles = grp.ntiles;
     const size_t Lm = (size_t)lay.L - 1;
-    const bool overlap = (k.flags & MANDEL_FLAG_SERIAL) == 0;
+    // (ASK-SBR has no fill kernels: nothing to overlap)
+    const bool overlap = (k.flags & MANDEL_FLAG_SERIAL) == 0 && k.scheme != MANDEL_SCHEME_SBR;
     cudaStream_t sf = overlap ? s2 : s; // stream of the fill kernels
     char *ws = (char *)k.ws;
     LevelArgs a;
@@ -345,11 +346,22 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
         size_t cap = (size_t)ntiles;
         for (int i = 0; i < l; ++i)
             cap *= (size_t)k.r * k.r;
-        if (k.scheme == MANDEL_SCHEME_SBR) {
+        const bool paper = k.scheme == MANDEL_SCHEME_SBR || k.scheme == MANDEL_SCHEME_MBR;
+        const bool sbr_fill = k.scheme == MANDEL_SCHEME_SBR; // Delta[T]: the level kernel fills
+        a.fill_vec = (vec_ok && d % 4 == 0) ? 1 : 0;
+        if (paper) {
             const int ring = 4 * d - 4;
 #define SBR_LAUNCH(TPB)                                                                        \
     do {                                                                                       \
-        if (stats) {                                                                           \
+        if (sbr_fill) {                                                                        \
+            if (stats) {                                                                       \
+                int gsz = resident_grid(k_sbr_level<TPB, true, true>, TPB, sms, cap);          \
+                k_sbr_level<TPB, true, true><<<gsz, TPB, 0, s>>>(a);                            \
+            } else {                                                                           \
+                int gsz = resident_grid(k_sbr_level<TPB, false, true>, TPB, sms, cap);         \
+                k_sbr_level<TPB, false, true><<<gsz, TPB, 0, s>>>(a);                           \
+            }                                                                                  \
+        } else if (stats) {                                                                    \
             int gsz = resident_grid(k_sbr_level<TPB, true>, TPB, sms, cap);                    \
             k_sbr_level<TPB, true><<<gsz, TPB, 0, s>>>(a);                                      \
         } else {                                                                               \
@@ -410,8 +422,9 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
             CK(cudaGetLastError());
             TEND(MANDEL_KIND_B200_CLASSIFY, l, s);
         }
-        // fill (terminal work) of this level's uniform regions
-        {
+        // fill (terminal work) of this level's uniform regions: flat over all of them
+        // (B200, MBR); ASK-SBR filled them inside its level kernel
+        if (!sbr_fill) {
             const bool vec = vec_ok && d >= 4;
             a.log2_q4 = vec ? ilog2((int64_t)d * d / 4) : 0;
             a.log2_row4 = vec ? ilog2(d / 4) : 0;
@@ -443,7 +456,16 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
         for (int i = 0; i < lay.L - 1; ++i)
             cap *= (size_t)k.r * k.r;
         TBEGIN(s);
-        if (k.scheme == MANDEL_SCHEME_SBR) {
+        if (k.scheme == MANDEL_SCHEME_MBR) { // nabla[L]: multiple blocks per leaf, flat
+            size_t blocks = (cap * (size_t)(d - 2) * (d - 2) + 255) / 256;
+            if (stats) {
+                int gsz = resident_grid(k_b200_leaf<true>, 256, sms, blocks);
+                k_b200_leaf<true><<<gsz, 256, 0, s>>>(a);
+            } else {
+                int gsz = resident_grid(k_b200_leaf<false>, 256, sms, blocks);
+                k_b200_leaf<false><<<gsz, 256, 0, s>>>(a);
+            }
+        } else if (k.scheme == MANDEL_SCHEME_SBR) {
             const int I = (d - 2) * (d - 2);
 #define LEAF_LAUNCH(TPB)                                                                       \
     do {                                                                                       \
@@ -487,7 +509,10 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
             }
         }
         CK(cudaGetLastError());
-        TEND(k.scheme == MANDEL_SCHEME_SBR ? MANDEL_KIND_SBR_LEAF : MANDEL_KIND_B200_LEAF, lay.L - 1, s);
+        TEND(k.scheme == MANDEL_SCHEME_SBR   ? MANDEL_KIND_SBR_LEAF
+             : k.scheme == MANDEL_SCHEME_MBR ? MANDEL_KIND_MBR_LEAF
+                                             : MANDEL_KIND_B200_LEAF,
+             lay.L - 1, s);
     }
     if (overlap) { // join the fill branches
         CK(cudaEventRecord(fork, sf));
@@ -540,7 +565,7 @@ int32_t mandel_ask_kernel_count(int64_t n, int32_t g, int32_t r, int32_t B, int3
     if (!valid_grb(n, g, r, B))
         return 0;
     const int L = levels_of(n, g, r, B);
-    return 1 + L * (scheme == MANDEL_SCHEME_SBR ? 2 : 3) + 1;
+    return 1 + L * (scheme == MANDEL_SCHEME_SBR ? 1 : scheme == MANDEL_SCHEME_MBR ? 2 : 3) + 1;
 }
 
 int mandel_exhaustive(mandel_region reg, int64_t n, int32_t maxdwell, int32_t *d_out, int64_t out_pitch,
@@ -577,7 +602,7 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
     int rc = validate_common(reg, n, maxdwell, d_out, out_pitch);
     if (rc)
         return rc;
-    if (!valid_grb(n, g, r, B) || !d_ws || (scheme != MANDEL_SCHEME_SBR && scheme != MANDEL_SCHEME_B200) ||
+    if (!valid_grb(n, g, r, B) || !d_ws || (scheme != MANDEL_SCHEME_SBR && scheme != MANDEL_SCHEME_B200 && scheme != MANDEL_SCHEME_MBR) ||
         (flags & ~(MANDEL_FLAG_STATS | MANDEL_FLAG_TIMING | MANDEL_FLAG_TILE_COST | MANDEL_FLAG_FLAT |
                    MANDEL_FLAG_SERIAL | MANDEL_FLAG_GROUPS_MASK)) != 0 ||
         MANDEL_FLAG_GROUPS_OF(flags) > MAXG)

@@ -77,7 +77,8 @@ def test_levels_and_workspace(lib):
     M4 = (1024 // 4) ** 2
     assert mb.workspace_bytes(1024, 4, 2, 4) < 3 * 4 * M4 + 8 * M4 * 4 // 3 + 2 * 1024 * 1024
     assert mb.kernel_count(32768, 16, 2, 32, "b200") == 1 + 7 * 3 + 1
-    assert mb.kernel_count(32768, 16, 2, 32, "sbr") == 1 + 7 * 2 + 1
+    assert mb.kernel_count(32768, 16, 2, 32, "sbr") == 1 + 7 * 1 + 1   # fills inside the level kernel
+    assert mb.kernel_count(32768, 16, 2, 32, "mbr") == 1 + 7 * 2 + 1   # + flat fill per level
 
 
 @pytest.mark.parametrize("n,g,r,B", [(1000, 4, 2, 32), (1024, 3, 2, 32), (1024, 4, 1, 32),

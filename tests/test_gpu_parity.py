@@ -11,7 +11,7 @@ import workloads as W
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-SCHEMES = ("b200", "sbr")
+SCHEMES = ("b200", "sbr", "mbr")
 
 
 @pytest.fixture(scope="module")
@@ -35,7 +35,7 @@ def _cmp_stats(gpu, orc, scheme):
     for a, b in zip(gpu, orc):
         for k in ("regions_in", "filled", "subdivided", "leaves", "leaf_px", "leaf_iters"):
             assert a[k] == b[k], (k, a, b)
-        if scheme == "sbr":  # the paper's scheme recomputes every region's full border
+        if scheme in ("sbr", "mbr"):  # the paper's schemes recompute every region's full border
             assert a["border_px"] == b["border_px"] and a["border_iters"] == b["border_iters"]
         else:                # the B200 scheme computes each border pixel once
             assert a["border_px"] <= b["border_px"] and a["border_iters"] <= b["border_iters"]
