@@ -223,11 +223,21 @@ def fit_dimension(level_regions: Sequence[int], r: int) -> float:
     return sxy / sxx
 
 
-def fit_lambda(t_ask: float, t_unit: float, p: ModelParams, tau_mode: str = "leaf") -> float:
-    """Solve T_SBR(lam) * t_unit = t_ask for lam.  T_SBR is affine in lam."""
+def scheme_time(p: ModelParams, scheme: str = "sbr", tau_mode: str = "literal") -> float:
+    """T_SBR or T_MBR by name."""
+    if scheme == "sbr":
+        return sbr_time(p, tau_mode)
+    if scheme == "mbr":
+        return mbr_time(p, tau_mode)
+    raise ValueError(scheme)
+
+
+def fit_lambda(t_ask: float, t_unit: float, p: ModelParams, tau_mode: str = "leaf",
+               scheme: str = "sbr") -> float:
+    """Solve T_scheme(lam) * t_unit = t_ask for lam.  T_SBR and T_MBR are affine in lam."""
     p0 = dataclasses.replace(p, lam=0.0)
     p1 = dataclasses.replace(p, lam=1.0)
-    a0, a1 = sbr_time(p0, tau_mode), sbr_time(p1, tau_mode)
+    a0, a1 = scheme_time(p0, scheme, tau_mode), scheme_time(p1, scheme, tau_mode)
     slope = a1 - a0
     if slope <= 0:
         return 0.0
@@ -243,26 +253,27 @@ class Calibration:
     q: int
     c: int
     tau_mode: str
+    scheme: str = "sbr"
 
     def P(self, r: int) -> float:
         return min(1.0, max(0.0, r ** (self.D - 2.0)))
 
     def predict_time(self, n: int, g: int, r: int, B: int) -> float:
         p = ModelParams(n, g, r, B, self.P(r), self.A, self.lam, self.q, self.c)
-        return sbr_time(p, self.tau_mode) * self.t_unit
+        return scheme_time(p, self.scheme, self.tau_mode) * self.t_unit
 
 
 def calibrate(n: int, A: float, t_ex: float, ref: Tuple[int, int, int], ref_level_regions:
               Sequence[int], t_ref: float, q: int = B200_Q, c: int = B200_C,
-              tau_mode: str = "leaf") -> Calibration:
+              tau_mode: str = "leaf", scheme: str = "sbr") -> Calibration:
     """SURVEY.md c-6 protocol: t_unit from the exhaustive run alone, D (hence P) from the
-    reference run's level sizes, lam from the reference run's time."""
+    reference run's level sizes, lam from the reference run's time (T_SBR or T_MBR)."""
     t_unit = t_ex / exhaustive_time(n, q, c, A)
     g, r, B = ref
     D = fit_dimension(ref_level_regions, r)
     P = min(1.0, max(0.0, r ** (D - 2.0)))
-    lam = fit_lambda(t_ref, t_unit, ModelParams(n, g, r, B, P, A, 0.0, q, c), tau_mode)
-    return Calibration(t_unit, D, lam, A, q, c, tau_mode)
+    lam = fit_lambda(t_ref, t_unit, ModelParams(n, g, r, B, P, A, 0.0, q, c), tau_mode, scheme)
+    return Calibration(t_unit, D, lam, A, q, c, tau_mode, scheme)
 
 
 def spearman(a: Sequence[float], b: Sequence[float]) -> float:

@@ -96,10 +96,13 @@ def analyse(report):
     A_modes = {"A=maxdwell": float(md)}
     if report.get("sum_dwell_ex"):
         A_modes["A=mean_dwell"] = report["sum_dwell_ex"] / float(n * n)
+    # the model of the scheme that ran (the B200 scheme has no model of its own: T_SBR)
+    model_scheme = "mbr" if report.get("scheme") == "mbr" else "sbr"
+    report["model_scheme"] = model_scheme
     for a_name, A in A_modes.items():
         for tau_mode in ("literal", "leaf"):
             cal = cm.calibrate(n, A, t_ex / 1e3, (16, 2, 32), ref["regions"], ref["ms"] / 1e3,
-                               tau_mode=tau_mode)
+                               tau_mode=tau_mode, scheme=model_scheme)
             pred = {k: 1e3 * cal.predict_time(n, *k) for k in meas}
             others = [k for k in meas if k != (16, 2, 32)]
             best_pred = min(others, key=pred.get)
