@@ -10,6 +10,8 @@ libmandel_b200.so's CUDA kernels through the C ABI of include/mandel.h):
     ask_stats(ws)                                               -> per-level dict list
     ask_to_host(region, n, maxdwell, g, r, B, h_out, out, ws)   -> h_out (pinned host)
     workspace(n, g, r, B)                                       -> uint8 cuda tensor
+    dp(region, n, maxdwell, g, r, B, out=None)                  -> int32 (n, n) cuda tensor
+                                       (Dynamic Parallelism baseline, libmandel_dp.so)
 """
 from __future__ import annotations
 
@@ -70,6 +72,16 @@ def exhaustive(region: Sequence[float], n: int, maxdwell: int, out=None, stream=
     rc = _lib.load().mandel_exhaustive(_lib.region(region), n, maxdwell, out.data_ptr(),
                                        out.stride(0), _stream_ptr(stream))
     _lib.check(rc, "mandel_exhaustive")
+    return out
+
+
+def dp(region: Sequence[float], n: int, maxdwell: int, g: int, r: int, B: int, out=None, stream=None):
+    """The paper's Dynamic Parallelism baseline (include/mandel_dp.h, libmandel_dp.so):
+    recursive Mariani-Silver, one child grid per subdividing node.  Same image as ask()."""
+    out = _image(n, out)
+    rc = _lib.load_dp().mandel_dp(_lib.region(region), n, maxdwell, g, r, B, out.data_ptr(), out.stride(0),
+                                  _stream_ptr(stream))
+    _lib.check_dp(rc, "mandel_dp")
     return out
 
 

@@ -102,6 +102,44 @@ def load() -> ctypes.CDLL:
     return _lib
 
 
+# ---------------------------------------------------------------- Dynamic Parallelism library
+# libmandel_dp.so (include/mandel_dp.h): the paper's recursive DP baseline, built separately
+# with relocatable device code.
+DP_LIB_PATH = os.environ.get("MANDEL_DP_LIB") or os.path.join(HERE, "libmandel_dp.so")
+_DP_SIGS = [
+    ("mandel_dp_pending_launches", ctypes.c_int64, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
+    ("mandel_dp", ctypes.c_int, [MandelRegion, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                 ctypes.c_int32, _P, ctypes.c_int64, _P]),
+    ("mandel_dp_last_cuda_error", ctypes.c_char_p, []),
+]
+DP_EXPORTED = [s[0] for s in _DP_SIGS]
+_dp_lib: Optional[ctypes.CDLL] = None
+
+
+def load_dp() -> ctypes.CDLL:
+    global _dp_lib
+    with _lock:
+        if _dp_lib is None:
+            if not os.path.exists(DP_LIB_PATH):
+                raise RuntimeError(f"{DP_LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                                   "g.build()'` (no CPU fallback)")
+            lib = ctypes.CDLL(DP_LIB_PATH)
+            for name, res, args in _DP_SIGS:
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _dp_lib = lib
+    return _dp_lib
+
+
+def check_dp(code: int, what: str) -> None:
+    if code != MANDEL_OK:
+        msg = load().mandel_strerror(code).decode()
+        if code == MANDEL_ECUDA:
+            msg += ": " + load_dp().mandel_dp_last_cuda_error().decode()
+        raise RuntimeError(f"{what}: {msg} (code {code})")
+
+
 def region(r: Sequence[float]) -> MandelRegion:
     return MandelRegion(*[float(v) for v in r])
 

@@ -53,6 +53,30 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
     return target
 
 
+# The Dynamic Parallelism comparison library (include/mandel_dp.h): device-side kernel
+# launches need relocatable device code and the device runtime (-rdc=true -lcudadevrt), kept
+# out of libmandel_b200.so so the ASK kernels are compiled exactly as before.
+DP_LIB = os.path.join(HERE, "libmandel_dp.so")
+DP_DEPS = ["mandel_dp.cu", "dwell.cuh", os.path.join("..", "..", "include", "mandel_dp.h"),
+           os.path.join("..", "..", "include", "mandel.h")]
+
+
+def build_dp(force: bool = False) -> str:
+    if not force and os.path.exists(DP_LIB) and not any(
+            os.path.getmtime(os.path.join(SRC_DIR, d)) > os.path.getmtime(DP_LIB) for d in DP_DEPS):
+        return DP_LIB
+    tmp = DP_LIB + f".tmp{os.getpid()}"
+    flags = [f for f in NVCC_FLAGS if f not in ("-Xptxas", "-v")]
+    cmd = [NVCC, *flags, "-rdc=true", "-o", tmp, os.path.join(SRC_DIR, "mandel_dp.cu"), "-lcudadevrt"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("nvcc failed building libmandel_dp.so")
+    os.replace(tmp, DP_LIB)
+    return DP_LIB
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    build_dp(force="--force" in sys.argv)
+    print(LIB, DP_LIB)

@@ -32,6 +32,31 @@ def test_exports_every_declared_symbol(lib):
     assert sorted(_lib.EXPORTED) == declared
 
 
+def test_dp_library_exports_every_declared_symbol():
+    """libmandel_dp.so (include/mandel_dp.h): loads, exports every declared function, and the
+    host-only entry points validate before touching CUDA."""
+    build.build_dp()
+    src = open(os.path.join(ROOT, "include", "mandel_dp.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    declared = sorted(set(re.findall(r"\b(mandel_[a-z_0-9]+)\s*\(", src)))
+    dl = _lib.load_dp()
+    assert declared == sorted(_lib.DP_EXPORTED)
+    for name in declared:
+        assert hasattr(dl, name), name
+    # sum_{l < L-1} g^2 r^(2l): C3 (7 levels) -> 256 (1 + 4 + ... + 4^5)
+    assert dl.mandel_dp_pending_launches(32768, 16, 2, 32) == 256 * (4 ** 6 - 1) // 3
+    assert dl.mandel_dp_pending_launches(1024, 4, 2, 32) == 16 * (1 + 4 + 16)
+    assert dl.mandel_dp_pending_launches(1024, 4, 3, 32) == 0
+    reg = _lib.region((-1.5, 0.5, -1.0, 1.0))
+    fake = ctypes.c_void_p(256)
+    assert dl.mandel_dp(reg, 1024, 0, 4, 2, 32, fake, 1024, None) == 1
+    assert dl.mandel_dp(reg, 1024, 10, 4, 2, 512, fake, 1024, None) == 1
+    assert dl.mandel_dp(reg, 1024, 10, 4, 2, 32, None, 1024, None) == 1
+    assert dl.mandel_dp(_lib.region((0.5, -1.5, -1, 1)), 1024, 10, 4, 2, 32, fake, 1024, None) == 1
+    out = os.popen(f"/usr/local/cuda/bin/cuobjdump --list-elf {_lib.DP_LIB_PATH} 2>&1").read()
+    assert "sm_100a" in out
+
+
 def test_sass_is_sm100a():
     so = _lib.LIB_PATH
     out = os.popen(f"/usr/local/cuda/bin/cuobjdump --list-elf {so} 2>&1").read()
@@ -40,12 +65,15 @@ def test_sass_is_sm100a():
 
 def test_no_fma_in_dwell_kernels():
     """-fmad=false + __f*_rn: the dwell loops must not contain FFMA (R4)."""
+    build.build_dp()
     sass = os.popen(f"/usr/local/cuda/bin/cuobjdump -sass {_lib.LIB_PATH} 2>&1").read()
+    sass += os.popen(f"/usr/local/cuda/bin/cuobjdump -sass {_lib.DP_LIB_PATH} 2>&1").read()
     funcs = re.split(r"\n\s*Function : ", sass)
     checked = 0
     for f in funcs[1:]:
         name = f.split("\n", 1)[0]
-        if any(k in name for k in ("k_exhaustive", "k_sbr_level", "k_sbr_leaf", "k_b200_border", "k_b200_leaf")):
+        if any(k in name for k in ("k_exhaustive", "k_sbr_level", "k_sbr_leaf", "k_b200_border", "k_b200_leaf",
+                                   "k_dp")):
             # no scalar FFMA at all
             assert re.search(r"\bFFMA\b", f) is None, name
             # packed engine: every FFMA2 is a product fma(a, b, -0) whose addend is the

@@ -257,3 +257,42 @@ def test_ask_groups(mb, groups):
     mine = At != -1
     assert np.array_equal(buf.cpu().numpy()[mine], At[mine]) and np.all(buf.cpu().numpy()[~mine] == -3)
     _cmp_stats(mb.ask_stats(ws), stt, "b200")
+
+
+# ----------------------------------------------------------------------------- DP baseline
+# libmandel_dp.so (include/mandel_dp.h): recursive Dynamic Parallelism, same decisions per
+# region as ASK, hence the same image as the oracle's ASK recursion.
+@pytest.mark.parametrize("w", [W.C1] + list(W.random_small_workloads(12, seed=W.SEED + 21, max_n=512)),
+                         ids=lambda w: w.name)
+def test_dp_parity(mb, w):
+    out = mb.dp(w.region, w.n, w.maxdwell, w.g, w.r, w.B)
+    A, _ = oracle.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B)
+    assert np.array_equal(out.cpu().numpy(), A)
+
+
+@pytest.mark.parametrize("n,g,r,B,md,region", [
+    (1024, 2, 4, 32, 700, W.DEFAULT_REGION),    # non-exact tiling
+    (512, 1, 2, 4, 1000, W.SEAHORSE_REGION),    # g = 1, 8 levels of recursion
+    (256, 4, 2, 8, 64, W.INTERIOR_REGION),      # closed form: all maxdwell (no launches)
+])
+def test_dp_edge_cases(mb, n, g, r, B, md, region):
+    buf = torch.full((n, n + 3), -1, dtype=torch.int32, device="cuda")  # unaligned pitch: scalar fill
+    mb.dp(region, n, md, g, r, B, out=buf)
+    A, _ = oracle.ask(region, n, md, g, r, B)
+    got = buf.cpu().numpy()
+    assert np.array_equal(got[:, :n], A) and np.all(got[:, n:] == -1)
+
+
+def test_dp_full_size_c3_equals_ask(mb):
+    """C3 at full size: the DP tree's image equals mandel_ask's (bit-exact, every pixel), and
+    sampled tiles equal the oracle."""
+    w = W.C3
+    a = mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B)
+    d = mb.dp(w.region, w.n, w.maxdwell, w.g, w.r, w.B)
+    torch.cuda.synchronize()
+    assert torch.equal(a, d)
+    d0 = w.n // w.g
+    t = _sample_tiles(w.g, 1, W.SEED + 31)[0]
+    gy, gx = divmod(t, w.g)
+    A, _ = oracle.ask_tile(w.region, w.n, w.maxdwell, w.g, w.r, w.B, t)
+    assert np.array_equal(d[gy * d0:(gy + 1) * d0, gx * d0:(gx + 1) * d0].cpu().numpy(), A)

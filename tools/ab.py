@@ -44,6 +44,20 @@ def main():
             s.record(); mb.exhaustive(w.region, w.n, w.maxdwell, out=out); e.record(); e.synchronize()
             res["ex_ms"] = s.elapsed_time(e)
         for v in a.variants.split(","):
+            if v == "dp":  # Dynamic Parallelism baseline (libmandel_dp.so): device time only
+                mb.dp(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out)
+                torch.cuda.synchronize()
+                same = True if ref is None else bool(torch.equal(ref, out))
+                ts = []
+                for _ in range(a.reps):
+                    flush.zero_()
+                    s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+                    s.record()
+                    mb.dp(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out)
+                    e.record(); e.synchronize()
+                    ts.append(s.elapsed_time(e))
+                res[v] = {"ms_mean": sum(ts) / len(ts), "ms_min": min(ts), "same_image": same}
+                continue
             kw = VARIANTS[v]
             mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, stats=True, **kw)
             st = mb.ask_stats(ws)
