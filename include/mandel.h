@@ -94,11 +94,18 @@ enum {
  *   MANDEL_SCHEME_MBR   the paper's ASK-MBR, "multiple blocks per region": Q and
  *                       PS as in SBR (block per region), terminal work T and leaf work L as
  *                       flat multi-block kernels over all regions of the level (nabla[T],
- *                       nabla[L]), one thread per pixel.  1 + 2L + 1 kernels.          */
+ *                       nabla[L]), one thread per pixel.  1 + 2L + 1 kernels.
+ *   MANDEL_SCHEME_FLOW  the B200 scheme's work (border reuse, lane refill, warp
+ *                       classification, fills) as ONE persistent dataflow kernel: a region's
+ *                       successors start as soon as its own ring is complete instead of at
+ *                       the next level barrier; decisions are region-local,
+ *                       so the image is the same.  MANDEL_FLAG_GROUPS is ignored.  3 kernels.
+ */
 enum {
     MANDEL_SCHEME_SBR = 0,
     MANDEL_SCHEME_B200 = 1,
-    MANDEL_SCHEME_MBR = 2
+    MANDEL_SCHEME_MBR = 2,
+    MANDEL_SCHEME_FLOW = 3
 };
 
 /* flags */
@@ -129,7 +136,9 @@ enum {
     MANDEL_KIND_B200_LEAF = 4,     /* leaf interiors, flat                                    */
     MANDEL_KIND_SBR_LEVEL = 5,     /* paper SBR/MBR: block-per-region border + decision       */
     MANDEL_KIND_SBR_LEAF = 6,      /* paper SBR: block-per-leaf interior                      */
-    MANDEL_KIND_MBR_LEAF = 7       /* paper MBR: leaf interiors, flat multi-block             */
+    MANDEL_KIND_MBR_LEAF = 7,      /* paper MBR: leaf interiors, flat multi-block             */
+    MANDEL_KIND_FLOW_INIT = 8,     /* flow scheme: level-0 tasks + per-level divisors         */
+    MANDEL_KIND_FLOW = 9           /* flow scheme: the persistent dataflow kernel             */
 };
 
 /* Bytes of workspace mandel_ask / mandel_ask_tiles need for these parameters (worst case

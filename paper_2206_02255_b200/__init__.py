@@ -19,7 +19,7 @@ from typing import List, Optional, Sequence
 
 from . import _lib
 
-SCHEMES = {"sbr": _lib.SCHEME_SBR, "b200": _lib.SCHEME_B200, "mbr": _lib.SCHEME_MBR}
+SCHEMES = {"sbr": _lib.SCHEME_SBR, "b200": _lib.SCHEME_B200, "mbr": _lib.SCHEME_MBR, "flow": _lib.SCHEME_FLOW}
 # Independent ASK chains per call (MANDEL_FLAG_GROUPS); same image for any value.
 DEFAULT_GROUPS = 1
 

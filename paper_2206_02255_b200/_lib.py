@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("MANDEL_B200_LIB") or os.path.join(HERE, "libmandel_b200.so")
 
 MANDEL_OK, MANDEL_EINVAL, MANDEL_EWORKSPACE, MANDEL_ECUDA = 0, 1, 2, 3
-SCHEME_SBR, SCHEME_B200, SCHEME_MBR = 0, 1, 2
+SCHEME_SBR, SCHEME_B200, SCHEME_MBR, SCHEME_FLOW = 0, 1, 2, 3
 FLAG_STATS = 1
 FLAG_TIMING = 2
 FLAG_TILE_COST = 4
@@ -32,7 +32,8 @@ def flag_groups(g: int) -> int:
         raise ValueError(f"groups must be in [1, {MAX_GROUPS}]")
     return ((int(g) - 1) & 15) << 8
 KIND_NAMES = {0: "init", 1: "b200_border", 2: "b200_classify", 3: "fill", 4: "b200_leaf",
-              5: "sbr_level", 6: "sbr_leaf", 7: "mbr_leaf"}
+              5: "sbr_level", 6: "sbr_leaf", 7: "mbr_leaf",
+              8: "flow_init", 9: "flow"}
 
 _lock = threading.Lock()
 _lib: Optional[ctypes.CDLL] = None

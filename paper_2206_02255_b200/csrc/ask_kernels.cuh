@@ -85,6 +85,9 @@ struct WsHeader {
     unsigned long long border_px[MAXL], border_iters[MAXL];
     unsigned long long leaf_px, leaf_iters;
     unsigned long long cursor[MAXL + 1]; // lane-refill work cursors: border level l, leaves
+    // MANDEL_SCHEME_FLOW (flow.cuh): task / unit / fill allocation, publication watermark,
+    // consumer cursor, tasks not yet retired
+    uint32_t f_task_alloc, f_unit_alloc, f_cursor, f_fill_alloc, f_pending, f_exited;
 };
 static_assert(sizeof(WsHeader) <= 4096, "header");
 
@@ -146,6 +149,13 @@ struct LevelArgs {
     uint32_t capP;           // parent slots of an OLT buffer (= OLT entries / r^2)
     uint32_t capL;           // leaf list entries
     int ngroups;
+    // MANDEL_SCHEME_FLOW (flow.cuh)
+    struct FlowTask *ftask;
+    uint4 *funit;
+    uint2 *ffill;
+    FastDiv *ffd; // 4 per level
+    uint32_t *fmark; // FLOW_CLEAN: the unit array is all zero (survives k_init)
+    int r_log2;
 };
 
 // Hot/cold list addressing: the q-th subdivided parent of level l-1 (q < hot count: front

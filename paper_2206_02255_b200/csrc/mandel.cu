@@ -14,6 +14,7 @@
 
 #include "../../include/mandel.h"
 #include "ask_kernels.cuh"
+#include "flow.cuh"
 
 using namespace mandel;
 
@@ -71,6 +72,8 @@ int levels_of(int64_t n, int32_t g, int32_t r, int32_t B)
 struct Layout {
     int L;
     size_t hdr, tiles, olt[2], fill, leaf, tile_cost, colT, colT_bytes, total;
+    size_t ftask, funit, ffill, ffd, fmark; // MANDEL_SCHEME_FLOW (flow.cuh)
+    size_t ftask_cap, funit_cap, ffill_cap;
     int u_log2; // log2 of the leaf side u = (n/g) / r^(L-1)
     size_t fill_off[MAXL]; // element offset of each level's fill segment
     size_t cap[MAXL];
@@ -118,6 +121,26 @@ bool make_layout(int64_t n, int32_t g, int32_t r, int32_t B, Layout &lay)
     lay.colT = o;
     lay.colT_bytes = (u >= 8) ? (size_t)(2 * (n / u)) * (size_t)n * 4 : 0;
     o = align256(o + lay.colT_bytes);
+    // flow scheme: every region yields at most one task (kind 1 or 2) or one fill, plus the
+    // g^2 level-0 ring tasks; pixel units <= n^2/FLOW_U + tasks (each pixel is computed at
+    // most once, each task has at most one partial unit); fill units <= n^2/FLOW_PIECE + fills
+    size_t regions = 0;
+    for (int l = 0; l < lay.L; ++l)
+        regions += lay.cap[l];
+    lay.ftask_cap = regions + (size_t)g * g;
+    lay.ffill_cap = regions;
+    lay.funit_cap = (size_t)n * (size_t)n / FLOW_U + (size_t)n * (size_t)n / FLOW_PIECE + lay.ftask_cap +
+                    lay.ffill_cap;
+    lay.ftask = o;
+    o = align256(o + lay.ftask_cap * sizeof(FlowTask));
+    lay.funit = o;
+    o = align256(o + lay.funit_cap * 16);
+    lay.ffill = o;
+    o = align256(o + lay.ffill_cap * 8);
+    lay.ffd = o;
+    o = align256(o + (size_t)4 * MAXL * sizeof(FastDiv));
+    lay.fmark = o;
+    o = align256(o + 4);
     lay.total = o;
     return true;
 }
@@ -286,7 +309,8 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
     const int ntiles = grp.ntiles;
     const size_t Lm = (size_t)lay.L - 1;
     // (ASK-SBR has no fill kernels: nothing to overlap)
-    const bool overlap = (k.flags & MANDEL_FLAG_SERIAL) == 0 && k.scheme != MANDEL_SCHEME_SBR;
+    const bool overlap = (k.flags & MANDEL_FLAG_SERIAL) == 0 && k.scheme != MANDEL_SCHEME_SBR &&
+                         k.scheme != MANDEL_SCHEME_FLOW;
     cudaStream_t sf = overlap ? s2 : s; // stream of the fill kernels
     char *ws = (char *)k.ws;
     LevelArgs a;
@@ -311,7 +335,7 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
     a.tile_cost = (k.flags & MANDEL_FLAG_TILE_COST) ? (unsigned long long *)(ws + lay.tile_cost) : nullptr;
     const bool stats = (k.flags & (MANDEL_FLAG_STATS | MANDEL_FLAG_TILE_COST)) != 0;
     const bool flat = (k.flags & MANDEL_FLAG_FLAT) != 0;
-    if (k.scheme == MANDEL_SCHEME_B200 && lay.colT_bytes) {
+    if ((k.scheme == MANDEL_SCHEME_B200 || k.scheme == MANDEL_SCHEME_FLOW) && lay.colT_bytes) {
         a.colT = (int *)(ws + lay.colT);
         a.u_log2 = lay.u_log2;
         a.colT_pitch = k.n;
@@ -333,6 +357,37 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
         k_init<<<(nthr + 255) / 256, 256, 0, s>>>(a);
         CK(cudaGetLastError());
         TEND(MANDEL_KIND_INIT, 0, s);
+    }
+    if (k.scheme == MANDEL_SCHEME_FLOW) { // one persistent dataflow kernel (flow.cuh)
+        a.ftask = (FlowTask *)(ws + lay.ftask);
+        a.funit = (uint4 *)(ws + lay.funit);
+        a.ffill = (uint2 *)(ws + lay.ffill);
+        a.ffd = (FastDiv *)(ws + lay.ffd);
+        a.fmark = (uint32_t *)(ws + lay.fmark);
+        a.r_log2 = ilog2(k.r);
+        a.fill_vec = vec_ok ? 1 : 0;
+        a.level = 0;
+        a.d = d0;
+        {
+            int gsz = resident_grid(k_flow_clear, 256, sms, (lay.funit_cap + 255) / 256);
+            k_flow_clear<<<gsz, 256, 0, s>>>(a, lay.funit_cap);
+            CK(cudaGetLastError());
+        }
+        TBEGIN(s);
+        k_flow_init<<<(ntiles * 32 + 255) / 256 > 0 ? (ntiles * 32 + 255) / 256 : 1, 256, 0, s>>>(a);
+        CK(cudaGetLastError());
+        TEND(MANDEL_KIND_FLOW_INIT, 0, s);
+        TBEGIN(s);
+        if (stats) {
+            int gsz = resident_grid(k_flow<true>, RF_TPB, sms, (size_t)1 << 30);
+            k_flow<true><<<gsz, RF_TPB, 0, s>>>(a);
+        } else {
+            int gsz = resident_grid(k_flow<false>, RF_TPB, sms, (size_t)1 << 30);
+            k_flow<false><<<gsz, RF_TPB, 0, s>>>(a);
+        }
+        CK(cudaGetLastError());
+        TEND(MANDEL_KIND_FLOW, 0, s);
+        return MANDEL_OK;
     }
     int d = d0;
     for (int l = 0; l < lay.L; ++l) {
@@ -565,6 +620,8 @@ int32_t mandel_ask_kernel_count(int64_t n, int32_t g, int32_t r, int32_t B, int3
     if (!valid_grb(n, g, r, B))
         return 0;
     const int L = levels_of(n, g, r, B);
+    if (scheme == MANDEL_SCHEME_FLOW)
+        return 4; // init, unit-array clear, flow init, flow
     return 1 + L * (scheme == MANDEL_SCHEME_SBR ? 1 : scheme == MANDEL_SCHEME_MBR ? 2 : 3) + 1;
 }
 
@@ -602,7 +659,8 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
     int rc = validate_common(reg, n, maxdwell, d_out, out_pitch);
     if (rc)
         return rc;
-    if (!valid_grb(n, g, r, B) || !d_ws || (scheme != MANDEL_SCHEME_SBR && scheme != MANDEL_SCHEME_B200 && scheme != MANDEL_SCHEME_MBR) ||
+    if (!valid_grb(n, g, r, B) || !d_ws || (scheme != MANDEL_SCHEME_SBR && scheme != MANDEL_SCHEME_B200 && scheme != MANDEL_SCHEME_MBR &&
+                                  scheme != MANDEL_SCHEME_FLOW) ||
         (flags & ~(MANDEL_FLAG_STATS | MANDEL_FLAG_TIMING | MANDEL_FLAG_TILE_COST | MANDEL_FLAG_FLAT |
                    MANDEL_FLAG_SERIAL | MANDEL_FLAG_GROUPS_MASK)) != 0 ||
         MANDEL_FLAG_GROUPS_OF(flags) > MAXG)
@@ -657,7 +715,7 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
         Entry e;
         e.key = key;
         // groups: tiles dealt round-robin in the given order (LPT order is preserved)
-        int ngroups = MANDEL_FLAG_GROUPS_OF(flags);
+        int ngroups = scheme == MANDEL_SCHEME_FLOW ? 1 : MANDEL_FLAG_GROUPS_OF(flags);
         if (ngroups > ntiles)
             ngroups = ntiles > 0 ? ntiles : 1;
         std::vector<int32_t> order;

@@ -97,16 +97,24 @@ def test_levels_and_workspace(lib):
     assert mb.levels(64, 8, 2, 8) == 1
     # worst case: 2 OLTs + leaf list of (n/B_last)^2 u32 + 4/3 of it as 8-byte fill entries,
     # plus the transposed column lines (2 n/u columns of n int32, leaf side u >= 8)
+    # plus the flow scheme's arrays: tasks (16 B, <= regions + g^2), pixel/fill units (16 B,
+    # <= n^2/64 + n^2/4096 + tasks + fills), fills (8 B, <= regions)
+    def flow_bytes(n, g, r, L):
+        regions = sum(g * g * r ** (2 * l) for l in range(L))
+        tasks = regions + g * g
+        return 16 * tasks + 16 * (n * n // 64 + n * n // 4096 + tasks + regions) + 8 * regions
     ws = mb.workspace_bytes(65536, 16, 2, 32)
     M = (65536 // 32) ** 2
     colT = 2 * (65536 // 32) * 65536 * 4
-    assert 3 * 4 * M + 8 * M + colT < ws < 3 * 4 * M + 8 * M * 4 // 3 + colT + 2 * 1024 * 1024
+    fb = flow_bytes(65536, 16, 2, 8)
+    assert 3 * 4 * M + 8 * M + colT + fb < ws < 3 * 4 * M + 8 * M * 4 // 3 + colT + fb + 2 * 1024 * 1024
     # leaf side 4 (< 8): no column copy
     M4 = (1024 // 4) ** 2
-    assert mb.workspace_bytes(1024, 4, 2, 4) < 3 * 4 * M4 + 8 * M4 * 4 // 3 + 2 * 1024 * 1024
+    assert mb.workspace_bytes(1024, 4, 2, 4) < 3 * 4 * M4 + 8 * M4 * 4 // 3 + flow_bytes(1024, 4, 2, 7) + 2 * 1024 * 1024
     assert mb.kernel_count(32768, 16, 2, 32, "b200") == 1 + 7 * 3 + 1
     assert mb.kernel_count(32768, 16, 2, 32, "sbr") == 1 + 7 * 1 + 1   # fills inside the level kernel
     assert mb.kernel_count(32768, 16, 2, 32, "mbr") == 1 + 7 * 2 + 1   # + flat fill per level
+    assert mb.kernel_count(32768, 16, 2, 32, "flow") == 4              # init, clear, flow init, flow
 
 
 @pytest.mark.parametrize("n,g,r,B", [(1000, 4, 2, 32), (1024, 3, 2, 32), (1024, 4, 1, 32),

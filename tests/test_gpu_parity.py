@@ -11,7 +11,7 @@ import workloads as W
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-SCHEMES = ("b200", "sbr", "mbr")
+SCHEMES = ("b200", "sbr", "mbr", "flow")
 
 
 @pytest.fixture(scope="module")
@@ -296,3 +296,18 @@ def test_dp_full_size_c3_equals_ask(mb):
     gy, gx = divmod(t, w.g)
     A, _ = oracle.ask_tile(w.region, w.n, w.maxdwell, w.g, w.r, w.B, t)
     assert np.array_equal(d[gy * d0:(gy + 1) * d0, gx * d0:(gx + 1) * d0].cpu().numpy(), A)
+
+
+@pytest.mark.parametrize("wname", ["C3", "C5"])
+def test_flow_full_size_equals_b200(mb, wname):
+    """The dataflow scheme at full size: same image and same per-level statistics as the
+    level-synchronous B200 scheme (every decision is region-local)."""
+    w = W.CONFIGS[wname]
+    ws = mb.workspace(w.n, w.g, w.r, w.B)
+    a = mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, ws=ws, stats=True)
+    sa = mb.ask_stats(ws)
+    f = mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, ws=ws, scheme="flow", stats=True)
+    sf = mb.ask_stats(ws)
+    torch.cuda.synchronize()
+    assert torch.equal(a, f)
+    assert sa == sf

@@ -17,7 +17,7 @@ import torch
 import paper_2206_02255_b200 as mb
 import workloads as W
 
-VARIANTS = {"b200": dict(scheme="b200"), "flat": dict(scheme="b200", flat=True), "sbr": dict(scheme="sbr"), "mbr": dict(scheme="mbr"),
+VARIANTS = {"b200": dict(scheme="b200"), "flow": dict(scheme="flow"), "flat": dict(scheme="b200", flat=True), "sbr": dict(scheme="sbr"), "mbr": dict(scheme="mbr"),
             "serial": dict(scheme="b200", serial=True), "mbr_serial": dict(scheme="mbr", serial=True),
             "g2": dict(scheme="b200", groups=2), "g4": dict(scheme="b200", groups=4),
             "g8": dict(scheme="b200", groups=8), "g1": dict(scheme="b200", groups=1)}

@@ -24,11 +24,12 @@ from paper_2206_02255_b200 import deal  # noqa: E402
 
 
 GROUPS = None
+SCHEME = "b200"
 
 
 def time_tiles(w, out, ws, tiles, flush, reps):
     f = lambda: mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, tiles=tiles,  # noqa: E731
-                       groups=GROUPS)
+                       groups=GROUPS, scheme=SCHEME)
     f()
     torch.cuda.synchronize()
     ts = []
@@ -50,9 +51,11 @@ def main():
     ap.add_argument("--deals", default="costrank,cyclic,diagonal")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--groups", type=int, default=None)
+    ap.add_argument("--scheme", default="b200")
     a = ap.parse_args()
-    global GROUPS
+    global GROUPS, SCHEME
     GROUPS = a.groups
+    SCHEME = a.scheme
     w = W.CONFIGS[a.workload]
     out = torch.empty((w.n, w.n), dtype=torch.int32, device="cuda")
     ws = mb.workspace(w.n, w.g, w.r, w.B)
@@ -66,7 +69,7 @@ def main():
     mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, tile_cost=True)
     exact = mb.tile_costs(ws, w.g)
     t1 = time_tiles(w, out, ws, None, flush, a.reps)
-    res = {"workload": w.name, "groups": GROUPS, "t1_ms": t1, "preview_ms": preview_ms, "deals": {}}
+    res = {"workload": w.name, "scheme": SCHEME, "groups": GROUPS, "t1_ms": t1, "preview_ms": preview_ms, "deals": {}}
     for dname in a.deals.split(","):
         for P in [int(x) for x in a.ranks.split(",")]:
             parts = deal.deal(dname, w.g, P, costs if dname == "costrank" else None)
@@ -81,7 +84,8 @@ def main():
     parts = deal.deal("costrank", w.g, P, costs)
     heavy = max(parts, key=lambda p: sum(exact[k] for k in p))
     for _ in range(2):
-        mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, tiles=heavy, timing=True, groups=GROUPS)
+        mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, tiles=heavy, timing=True, groups=GROUPS,
+               scheme=SCHEME)
     torch.cuda.synchronize()
     res["heavy_rank_kernels"] = [dict(k) for k in mb.kernel_times()]
     mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, timing=True)
