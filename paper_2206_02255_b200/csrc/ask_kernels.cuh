@@ -28,7 +28,7 @@ constexpr int DWELL_K = 8;                 // iterations per escape test (dwell.
 #define MANDEL_RFB_K 16
 #endif
 #ifndef MANDEL_RFB_T
-#define MANDEL_RFB_T 4
+#define MANDEL_RFB_T 8
 #endif
 #ifndef MANDEL_RFB_CH
 #define MANDEL_RFB_CH 64
@@ -43,12 +43,15 @@ constexpr int DWELL_K = 8;                 // iterations per escape test (dwell.
 #define MANDEL_RFL_CH 128
 #endif
 #ifndef MANDEL_RF_MINB
-#define MANDEL_RF_MINB 6
+#define MANDEL_RF_MINB 4
 #endif
-// Packed engine (refill_loop2, two pixels per lane on FMUL2/FADD2): on/off per kernel, T out
-// of 64 slots, resident blocks per SM.
+// Packed engine (refill_loop2, two pixels per lane on FFMA2/FADD2): on/off per kernel, T out
+// of 64 slots, resident blocks per SM.  Measured on B200 (profiles/r01_tune_refill_v3.txt):
+// packed for the leaves (fewer bookkeeping instructions per pixel), scalar for the border
+// levels (a level's tail is one long pixel's latency, and a scalar warp steps a pixel twice
+// as fast as a packed one when the SM has drained).
 #ifndef MANDEL_RFB_PACK
-#define MANDEL_RFB_PACK 1
+#define MANDEL_RFB_PACK 0
 #endif
 #ifndef MANDEL_RFL_PACK
 #define MANDEL_RFL_PACK 1

@@ -18,7 +18,8 @@ from paper_2206_02255_b200 import build  # noqa: E402
 
 SO = "/tmp/libmandel_trace.so"
 if os.environ.get("MANDEL_B200_LIB") != SO:
-    build.build(out=SO, defines=["MANDEL_RF_TRACE"])
+    extra = [d for d in os.environ.get("MANDEL_TRACE_DEFS", "").split(",") if d]
+    build.build(out=SO, defines=["MANDEL_RF_TRACE"] + extra)
     os.environ["MANDEL_B200_LIB"] = SO
     os.execv(sys.executable, [sys.executable] + sys.argv)
 
