@@ -167,7 +167,10 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
 /* End-to-end variant over HOST memory: runs mandel_ask_tiles into the device buffer d_out
  * and copies the n x n image (rows of n elements) into h_out (host; pinned for full
  * bandwidth), then synchronises `stream`.  For tile runs only the tiles' pixels are
- * meaningful.  h_out is written with row pitch n. */
+ * meaningful.  h_out is written with row pitch n.  For the whole image (h_tile_ids NULL) the
+ * call is pipelined: min(g, 4) bands of level-0 tile rows run as separate tile calls and the
+ * copy of each band overlaps the computation of the next (same image: level-0 regions are
+ * independent).  One call at a time per device. */
 int mandel_ask_to_host(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, int32_t r,
                        int32_t B, const int32_t *h_tile_ids, int32_t n_tiles, int32_t scheme,
                        int32_t *d_out, int64_t out_pitch, void *d_ws, size_t ws_bytes,

@@ -172,6 +172,8 @@ struct DevInfo {
     cudaStream_t side[MAXG] = {};      // per group: capture side stream (fill branches)
     cudaEvent_t fork[MAXG] = {};       // per group: fill fork/join event used during capture
     cudaEvent_t start = nullptr, join[MAXG] = {};
+    cudaStream_t copy = nullptr;       // mandel_ask_to_host: band copies
+    cudaEvent_t band[8] = {}, copied = nullptr;
 };
 
 struct Key {
@@ -224,6 +226,10 @@ int dev_info(int dev, DevInfo *&out)
             CK(cudaEventCreateWithFlags(&di.fork[i], cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&di.join[i], cudaEventDisableTiming));
         }
+        CK(cudaStreamCreateWithFlags(&di.copy, cudaStreamNonBlocking));
+        for (int i = 0; i < 8; ++i)
+            CK(cudaEventCreateWithFlags(&di.band[i], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&di.copied, cudaEventDisableTiming));
     }
     out = &di;
     return MANDEL_OK;
@@ -840,24 +846,63 @@ int mandel_ask_to_host(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g
 {
     if (!h_out)
         return MANDEL_EINVAL;
-    int rc = mandel_ask_tiles(reg, n, maxdwell, g, r, B, h_tile_ids, n_tiles, scheme, 0u, d_out, out_pitch, d_ws,
-                              ws_bytes, stream);
-    if (rc)
-        return rc;
+    cudaStream_t st = (cudaStream_t)stream;
     if (h_tile_ids) { // only the tiles' pixels: one 2-D copy per tile
+        int rc = mandel_ask_tiles(reg, n, maxdwell, g, r, B, h_tile_ids, n_tiles, scheme, 0u, d_out, out_pitch, d_ws,
+                                  ws_bytes, stream);
+        if (rc)
+            return rc;
         const int64_t d0 = n / g;
         for (int32_t i = 0; i < n_tiles; ++i) {
             const int64_t gy = h_tile_ids[i] / g, gx = h_tile_ids[i] % g;
             const size_t off_h = (size_t)(gy * d0) * (size_t)n + (size_t)(gx * d0);
             const size_t off_d = (size_t)(gy * d0) * (size_t)out_pitch + (size_t)(gx * d0);
             CK(cudaMemcpy2DAsync(h_out + off_h, (size_t)n * 4, d_out + off_d, (size_t)out_pitch * 4,
-                                 (size_t)d0 * 4, (size_t)d0, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+                                 (size_t)d0 * 4, (size_t)d0, cudaMemcpyDeviceToHost, st));
         }
-    } else {
-        CK(cudaMemcpy2DAsync(h_out, (size_t)n * 4, d_out, (size_t)out_pitch * 4, (size_t)n * 4, (size_t)n,
-                             cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+        CK(cudaStreamSynchronize(st));
+        return MANDEL_OK;
     }
-    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    // Whole image: bands of level-0 tile rows, each an independent mandel_ask_tiles call
+    // (level-0 regions never interact, so the image is the same); the device->host copy of
+    // band b runs on a copy stream while band b+1 computes, in chunks of <= 256 MB (the
+    // copy, ~55 GB/s over PCIe, dominates this call).
+    if (!valid_grb(n, g, r, B) || !valid_region(reg) || !d_out || out_pitch < n)
+        return MANDEL_EINVAL;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    DevInfo *di = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        int rc = dev_info(dev, di);
+        if (rc)
+            return rc;
+    }
+    const int K = g >= 4 ? 4 : g, rows_per_band = g / K;
+    const int64_t d0 = n / g;
+    const int64_t chunk_rows = ((int64_t)1 << 26) / n > 0 ? ((int64_t)1 << 26) / n : 1;
+    std::vector<int32_t> tiles;
+    for (int b = 0; b < K; ++b) {
+        tiles.clear();
+        for (int gy = b * rows_per_band; gy < (b + 1) * rows_per_band; ++gy)
+            for (int gx = 0; gx < g; ++gx)
+                tiles.push_back(gy * g + gx);
+        int rc = mandel_ask_tiles(reg, n, maxdwell, g, r, B, tiles.data(), (int32_t)tiles.size(), scheme, 0u, d_out,
+                                  out_pitch, d_ws, ws_bytes, stream);
+        if (rc)
+            return rc;
+        CK(cudaEventRecord(di->band[b], st));
+        CK(cudaStreamWaitEvent(di->copy, di->band[b], 0));
+        const int64_t y1 = (int64_t)(b + 1) * rows_per_band * d0;
+        for (int64_t y = (int64_t)b * rows_per_band * d0; y < y1; y += chunk_rows) {
+            const int64_t rows = y + chunk_rows <= y1 ? chunk_rows : y1 - y;
+            CK(cudaMemcpy2DAsync(h_out + (size_t)y * (size_t)n, (size_t)n * 4, d_out + (size_t)y * (size_t)out_pitch,
+                                 (size_t)out_pitch * 4, (size_t)n * 4, (size_t)rows, cudaMemcpyDeviceToHost, di->copy));
+        }
+    }
+    CK(cudaEventRecord(di->copied, di->copy));
+    CK(cudaStreamWaitEvent(st, di->copied, 0));
+    CK(cudaStreamSynchronize(st));
     return MANDEL_OK;
 }
 

@@ -160,6 +160,19 @@ def test_ask_to_host(mb):
     assert np.array_equal(h.numpy().reshape(w.n, w.n), A)
 
 
+@pytest.mark.parametrize("n,g,r,B,md", [(2048, 16, 2, 16, 700), (1024, 2, 4, 8, 300), (512, 8, 8, 4, 900)])
+def test_ask_to_host_banded(mb, n, g, r, B, md):
+    """The whole-image host call is pipelined over bands of tile rows (copy of one band
+    overlapping the next band's ASK): the host image equals the oracle's, every pixel, also
+    with a pitched device buffer."""
+    ws = mb.workspace(n, g, r, B)
+    out = torch.full((n, n + 4), -3, dtype=torch.int32, device="cuda")
+    h = torch.full((n * n,), -7, dtype=torch.int32).pin_memory()
+    mb.ask_to_host(W.SEAHORSE_REGION, n, md, g, r, B, h, out, ws)
+    A, _ = oracle.ask(W.SEAHORSE_REGION, n, md, g, r, B)
+    assert np.array_equal(h.numpy().reshape(n, n), A)
+
+
 # ----------------------------------------------------------------------------- full sizes
 def _sample_tiles(g, k, seed):
     rng = np.random.default_rng(seed)
