@@ -65,6 +65,10 @@ constexpr int DWELL_K = 8;                 // iterations per escape test (dwell.
 #ifndef MANDEL_RF2_MINB
 #define MANDEL_RF2_MINB 3
 #endif
+// Short-pixel prepass steps of the packed leaf engine (refill.cuh rf2_prepass; 0 = off).
+#ifndef MANDEL_RFL_PRE
+#define MANDEL_RFL_PRE 16
+#endif
 #ifndef MANDEL_RF_TPB
 #define MANDEL_RF_TPB 256
 #endif
@@ -779,6 +783,9 @@ template <bool STATS>
 __global__ void __launch_bounds__(RF_TPB, RFL_MINB) k_b200_leaf_rf(LevelArgs a)
 {
     __shared__ ParkedPoint s_q[RF_TPB / 32][MANDEL_RFL_PACK ? RF2_QCAP : RF_QCAP];
+#if MANDEL_RFL_PACK && MANDEL_RFL_PRE > 0
+    __shared__ SvPoint s_sv[RF_TPB / 32][MANDEL_RFL_CH];
+#endif
     LeafMap map;
     map.leaf = a.leaf;
     map.nh = leaf_hot(a);
@@ -789,8 +796,14 @@ __global__ void __launch_bounds__(RF_TPB, RFL_MINB) k_b200_leaf_rf(LevelArgs a)
     StoreSink<STATS, false> sink{&a, 0ull, 0ull};
     if (map.fI.d > 0)
 #if MANDEL_RFL_PACK
+#if MANDEL_RFL_PRE > 0
+        refill_loop2<MANDEL_RFL_K, MANDEL_RFL2_T, MANDEL_RFL_CH, LeafMap, StoreSink<STATS, false>, MANDEL_RFL_PRE>(
+            a.map, a.maxdwell, total, &a.hdr->cursor[MAXL], map, sink, s_q[threadIdx.x >> 5], 15,
+            s_sv[threadIdx.x >> 5]);
+#else
         refill_loop2<MANDEL_RFL_K, MANDEL_RFL2_T, MANDEL_RFL_CH>(a.map, a.maxdwell, total, &a.hdr->cursor[MAXL],
                                                                  map, sink, s_q[threadIdx.x >> 5], 15);
+#endif
 #else
         refill_loop<MANDEL_RFL_K, MANDEL_RFL_T, MANDEL_RFL_CH>(a.map, a.maxdwell, total, &a.hdr->cursor[MAXL], map,
                                                                sink, s_q[threadIdx.x >> 5], 15);

@@ -394,12 +394,88 @@ __device__ __forceinline__ bool rf2_fetch(uint32_t t, const PixMap &pm, int maxd
     return false;
 }
 
+#ifndef MANDEL_PRE_WINDOW
+#define MANDEL_PRE_WINDOW 0xffffffffu // prepass pixels per decision window (default: always on)
+#endif
+#ifndef MANDEL_PRE_MINFRAC
+#define MANDEL_PRE_MINFRAC 25u // keep the prepass while >= this % of its pixels escape in it
+#endif
+// A prepass survivor: pixel and its orbit after S steps (x2, y2 are x*x, y*y again).
+struct SvPoint {
+    uint32_t pxy; // x | y << 16
+    float x, y;
+    uint32_t pad;
+};
+
+// Short-pixel prepass (PRE = S > 0): every grab of raw indices is first run
+// warp-synchronously, one pixel per lane, for S steps with an escape test after EVERY step
+// (exact dwell, no replay); pixels that escape -- 70% of the C3 leaf pixels have dwell <= 16
+// -- are stored at once and never enter the refill machinery (fetch, parking, bisection
+// replay: ~20 dispatch cycles per pixel); the survivors go to a per-warp buffer sv (CH
+// entries) and are dealt to slots with their orbit state at iteration S.  The test
+// `!(x2+y2 <= 4)` after step k first fires at the pixel's dwell (escape happens before any
+// overflow), so the stored dwell is the per-step definition's.  A warp stops using the
+// prepass once fewer than a quarter of its first >= 512 prepass pixels escaped in it
+// (boundary-heavy windows such as C5, median leaf dwell 146).
+template <int S, class Map, class Sink>
+__device__ __forceinline__ int rf2_prepass(uint32_t b, uint32_t e, const PixMap &pm, int maxdwell, const Map &map,
+                                           Sink &sink, SvPoint *sv, int &n_esc)
+{
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    int m = 0, esc = 0;
+    for (uint32_t r0 = b; r0 < e; r0 += 32) {
+        const uint32_t t = r0 + (uint32_t)lane;
+        bool surv = false;
+        uint32_t pxy = 0;
+        float x = 0.f, y = 0.f;
+        if (t < e) {
+            int px, py;
+            map(t, px, py);
+            pxy = (uint32_t)px | ((uint32_t)py << 16);
+            const float cr = pix_re(pm, px), ci = pix_im(pm, py);
+            if (__fadd_rn(__fmul_rn(cr, cr), __fmul_rn(ci, ci)) <= 3.9f) {
+                float x2 = 0.f, y2 = 0.f;
+                int dw = 0;
+#pragma unroll
+                for (int k = 1; k <= S; ++k) {
+                    MANDEL_STEP(x, y, x2, y2, cr, ci);
+                    dw = (dw == 0 && !(__fadd_rn(x2, y2) <= 4.0f)) ? k : dw;
+                }
+                if (dw) {
+                    sink(px, py, dw);
+                    ++esc;
+                } else {
+                    surv = true;
+                }
+            } else { // per-step loop (escape permanence not guaranteed)
+                sink(px, py, dwell_per_step<S>(cr, ci, maxdwell));
+                ++esc;
+            }
+        }
+        const unsigned sm = __ballot_sync(FULL, surv);
+        if (surv) {
+            SvPoint &o = sv[m + __popc(sm & lt)];
+            o.pxy = pxy;
+            o.x = x;
+            o.y = y;
+        }
+        m += __popc(sm);
+    }
+    n_esc += __reduce_add_sync(FULL, (unsigned)esc);
+    __syncwarp();
+    return m;
+}
+
 // Same contract as refill_loop (Map, Sink, cursor, launch shape); q: RF2_QCAP entries.
-// T counts parked slots out of the warp's 64.
-template <int K, int T, int CH, class Map, class Sink>
+// T counts parked slots out of the warp's 64.  PRE > 0: short-pixel prepass of PRE steps
+// (rf2_prepass above) with the per-warp survivor buffer sv (CH entries; requires
+// maxdwell > PRE, else the prepass is off).
+template <int K, int T, int CH, class Map, class Sink, int PRE = 0>
 __device__ __forceinline__ void refill_loop2(const PixMap &pm, int maxdwell, uint32_t total,
                                              unsigned long long *cursor, const Map &map, Sink &sink,
-                                             ParkedPoint *q, int tslot = 0)
+                                             ParkedPoint *q, int tslot = 0, SvPoint *sv = nullptr)
 {
     constexpr uint32_t PPL = 8; // pixels per slot before a warp is worth activating
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -423,6 +499,10 @@ __device__ __forceinline__ void refill_loop2(const PixMap &pm, int maxdwell, uin
     uint32_t pos = 0, end = 0;
     bool exhausted = false;
     int qn = 0;
+    // prepass state (warp-uniform)
+    bool use_pre = PRE > 0 && maxdwell > PRE && sv != nullptr;
+    uint32_t sv_pos = 0, sv_end = 0, pre_tot = 0;
+    int pre_esc = 0;
 
     bool has0 = false, has1 = false, fin0 = false, fin1 = false;
     int px0 = 0, py0 = 0, px1 = 0, py1 = 0;
@@ -464,6 +544,78 @@ __device__ __forceinline__ void refill_loop2(const PixMap &pm, int maxdwell, uin
         }
         unsigned need0 = __ballot_sync(FULL, !has0), need1 = __ballot_sync(FULL, !has1);
         while ((need0 | need1) && !exhausted) {
+            if (PRE > 0 && use_pre && sv_pos >= sv_end) {
+                // prepass a fresh grab; its survivors refill the buffer
+                unsigned long long b = 0;
+                if (lane == 0)
+                    b = atomicAdd(cursor, (unsigned long long)grab);
+                b = __shfl_sync(FULL, b, 0);
+                if (b >= total) {
+                    exhausted = true;
+                    break;
+                }
+                const uint32_t e = (uint32_t)min(b + (unsigned long long)grab, (unsigned long long)total);
+                sv_pos = 0;
+                sv_end = (uint32_t)rf2_prepass<PRE>((uint32_t)b, e, pm, maxdwell, map, sink, sv, pre_esc);
+                pre_tot += e - (uint32_t)b;
+                if (pre_tot >= MANDEL_PRE_WINDOW) { // windowed: the list runs hot (long) leaves first
+                    use_pre = MANDEL_PRE_MINFRAC * pre_tot <= 100u * (uint32_t)pre_esc;
+                    pre_tot = 0;
+                    pre_esc = 0;
+                }
+                continue;
+            }
+            if (PRE > 0 && sv_pos < sv_end) { // deal survivors (orbit at iteration PRE)
+                const unsigned c0 = __popc(need0);
+                const unsigned cnt = c0 + __popc(need1);
+                const unsigned avail = sv_end - sv_pos;
+                const unsigned take = avail < cnt ? avail : cnt;
+                const unsigned r0 = __popc(need0 & lt), r1 = c0 + __popc(need1 & lt);
+                float cr0, ci0, cr1, ci1, xa0, xa1, ya0, ya1, qa0, qa1, wa0, wa1;
+                f2_unpack(CR, cr0, cr1);
+                f2_unpack(CI, ci0, ci1);
+                f2_unpack(X, xa0, xa1);
+                f2_unpack(Y, ya0, ya1);
+                f2_unpack(X2, qa0, qa1);
+                f2_unpack(Y2, wa0, wa1);
+                if (!has0 && r0 < take) {
+                    const SvPoint p = sv[sv_pos + r0];
+                    px0 = (int)(p.pxy & 0xffffu);
+                    py0 = (int)(p.pxy >> 16);
+                    cr0 = pix_re(pm, px0);
+                    ci0 = pix_im(pm, py0);
+                    xa0 = p.x;
+                    ya0 = p.y;
+                    qa0 = __fmul_rn(p.x, p.x);
+                    wa0 = __fmul_rn(p.y, p.y);
+                    it0 = (unsigned)PRE;
+                    has0 = true;
+                }
+                if (!has1 && r1 < take) {
+                    const SvPoint p = sv[sv_pos + r1];
+                    px1 = (int)(p.pxy & 0xffffu);
+                    py1 = (int)(p.pxy >> 16);
+                    cr1 = pix_re(pm, px1);
+                    ci1 = pix_im(pm, py1);
+                    xa1 = p.x;
+                    ya1 = p.y;
+                    qa1 = __fmul_rn(p.x, p.x);
+                    wa1 = __fmul_rn(p.y, p.y);
+                    it1 = (unsigned)PRE;
+                    has1 = true;
+                }
+                CR = f2_pack(cr0, cr1);
+                CI = f2_pack(ci0, ci1);
+                X = f2_pack(xa0, xa1);
+                Y = f2_pack(ya0, ya1);
+                X2 = f2_pack(qa0, qa1);
+                Y2 = f2_pack(wa0, wa1);
+                sv_pos += take;
+                __syncwarp();
+                need0 = __ballot_sync(FULL, !has0);
+                need1 = __ballot_sync(FULL, !has1);
+                continue;
+            }
             if (pos >= end) {
                 unsigned long long b = 0;
                 if (lane == 0)
@@ -511,6 +663,13 @@ __device__ __forceinline__ void refill_loop2(const PixMap &pm, int maxdwell, uin
 #ifdef MANDEL_RF_TRACE
             tr_px += take;
 #endif
+            if (PRE > 0 && !use_pre && sv != nullptr && maxdwell > PRE) { // retry the prepass later
+                pre_tot += take;
+                if (pre_tot >= MANDEL_PRE_WINDOW && pos >= end) {
+                    use_pre = true;
+                    pre_tot = 0;
+                }
+            }
             need0 = __ballot_sync(FULL, !has0);
             need1 = __ballot_sync(FULL, !has1);
         }
