@@ -69,6 +69,9 @@ constexpr int DWELL_K = 8;                 // iterations per escape test (dwell.
 #ifndef MANDEL_RFL_PRE
 #define MANDEL_RFL_PRE 16
 #endif
+#ifndef MANDEL_RFB_PRE
+#define MANDEL_RFB_PRE 16 // (packed border engine only)
+#endif
 #ifndef MANDEL_RF_TPB
 #define MANDEL_RF_TPB 256
 #endif
@@ -753,6 +756,9 @@ template <bool STATS>
 __global__ void __launch_bounds__(RF_TPB, RFB_MINB) k_b200_border_rf(LevelArgs a)
 {
     __shared__ ParkedPoint s_q[RF_TPB / 32][MANDEL_RFB_PACK ? RF2_QCAP : RF_QCAP];
+#if MANDEL_RFB_PACK && MANDEL_RFB_PRE > 0
+    __shared__ SvPoint s_sv[RF_TPB / 32][MANDEL_RFB_CH];
+#endif
     BorderMap map;
     map.olt = a.olt_in;
     map.nh = sub_hot(a);
@@ -769,7 +775,11 @@ __global__ void __launch_bounds__(RF_TPB, RFB_MINB) k_b200_border_rf(LevelArgs a
                                     : *((volatile uint32_t *)&a.hdr->n_subdiv[a.level - 1]);
     const uint32_t total = map.fper.d * count;
     StoreSink<STATS, true> sink{&a, 0ull, 0ull};
-#if MANDEL_RFB_PACK
+#if MANDEL_RFB_PACK && MANDEL_RFB_PRE > 0
+    refill_loop2<MANDEL_RFB_K, MANDEL_RFB2_T, MANDEL_RFB_CH, BorderMap, StoreSink<STATS, true>, MANDEL_RFB_PRE>(
+        a.map, a.maxdwell, total, &a.hdr->cursor[a.level], map, sink, s_q[threadIdx.x >> 5], a.level,
+        s_sv[threadIdx.x >> 5]);
+#elif MANDEL_RFB_PACK
     refill_loop2<MANDEL_RFB_K, MANDEL_RFB2_T, MANDEL_RFB_CH>(a.map, a.maxdwell, total, &a.hdr->cursor[a.level], map,
                                                              sink, s_q[threadIdx.x >> 5], a.level);
 #else

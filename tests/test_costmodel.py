@@ -2,6 +2,7 @@
 the paper's stated bounds (Omega <= A, S <= A) and a Monte-Carlo simulation of the
 subdivision tree (oracle/montecarlo.py)."""
 import math
+import os
 
 import numpy as np
 import pytest
@@ -163,3 +164,51 @@ def test_fit_lambda_roundtrip():
 def test_spearman():
     assert cm.spearman([1, 2, 3], [10, 20, 30]) == 1.0
     assert cm.spearman([1, 2, 3], [3, 2, 1]) == -1.0
+
+
+def test_mbr_time_special_cases():
+    """T_MBR at its two degenerate subdivision probabilities.  P = 0: every level-0
+    region is uniform, so one parallel border pass over the g^2 regions plus one flat fill of
+    the n^2 pixels.  P = 1: every region subdivides, so no fill at all and the last level
+    computes every pixel (A ceil(n^2/(qc))), plus per level the border pass and the
+    subdivision cost S = lam A per region."""
+    n, g, r, B, A, lam, q, c = 8192, 16, 2, 32, 512.0, 3.0, 148, 128
+    tau = cm.depth_tau(n, g, r, B)
+    assert tau >= 2
+    G = g * g
+    p0 = cm.ModelParams(n, g, r, B, 0.0, A, lam, q, c)
+    assert cm.mbr_time(p0) == math.ceil(4 * n / (g * c)) * math.ceil(G / q) * A + math.ceil(n * n / (q * c))
+    p1 = cm.ModelParams(n, g, r, B, 1.0, A, lam, q, c)
+    want = A * math.ceil(n * n / (q * c))
+    for i in range(tau - 1):
+        Gi = G * (r * r) ** i
+        want += math.ceil(4 * n / (g * r ** i * c)) * math.ceil(Gi / q) * A + math.ceil(Gi / q) * lam * A
+    assert math.isclose(cm.mbr_time(p1), want, rel_tol=1e-12)
+
+
+def test_fit_lambda_roundtrip_mbr():
+    """The per-scheme calibration (sweep_c2 fits lambda with the scheme's own model)."""
+    p = cm.ModelParams(8192, 16, 2, 32, 0.6, 2048, 11.0, 148, 128)
+    t_unit = 2e-9
+    t = cm.mbr_time(p, "leaf") * t_unit
+    assert abs(cm.fit_lambda(t, t_unit, p, "leaf", scheme="mbr") - 11.0) < 1e-6
+    cal = cm.calibrate(8192, 2048.0, cm.exhaustive_time(8192, 148, 128, 2048.0) * t_unit, (16, 2, 32),
+                       [256, 256 * 3, 256 * 9, 256 * 27], t, scheme="mbr")
+    assert cal.scheme == "mbr" and abs(cal.t_unit - t_unit) < 1e-18
+
+
+def test_landscapes_tool_runs():
+    """tools/landscapes.py (NEXT-2) evaluates the figure data; Omega stays below A and the
+    claims report is complete."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "landscapes", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "landscapes.py"))
+    L = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(L)
+    e1 = L.e1()
+    for A, ws in e1["omega_n_vs_A"].items():
+        assert all(w <= A * (1 + 1e-12) for w in ws)
+    e2 = L.e2(cm.B200_Q, cm.B200_C)
+    assert set(e2["S_param"]) == {"g", "r", "B"}
+    cl = L.claims(e1, e2)
+    assert cl["Omega <= A everywhere (P:244)"] and len(cl) >= 10
