@@ -68,6 +68,9 @@ typedef struct {
     int64_t border_iters; /* iterations counted for them (= sum of their dwells)            */
     int64_t leaf_px;      /* leaf interior pixels computed at this level                    */
     int64_t leaf_iters;   /* sum of their dwells                                           */
+    int64_t deferred;     /* MANDEL_FLAG_DEFER: border pixels of this level that reached the
+                             cap unescaped (parked, or computed on when the pool was full)  */
+    int64_t uncertain;    /* MANDEL_FLAG_DEFER: regions whose whole ring was unresolved      */
 } mandel_level_stats;
 
 enum {
@@ -126,6 +129,20 @@ enum {
 #define MANDEL_FLAG_GROUPS(G) ((((uint32_t)(G)-1u) & 15u) << 8)
 #define MANDEL_FLAG_GROUPS_MASK (15u << 8)
 #define MANDEL_FLAG_GROUPS_OF(f) ((int)(((f) >> 8) & 15u) + 1)
+/* Deferred long pixels -- experimental, measured slower on B200 than the default scheme
+ * (B200 scheme, lane-refill kernels, one group, no STATS/TILE_COST; ignored otherwise;
+ * DESIGN.md §4.12).  A border pixel still unescaped after C iterations is
+ * parked with its orbit state in a workspace pool and its image slot holds a marker until the
+ * dwell is finished; a region is decided from the resolved part of its ring when that
+ * suffices (two different values, or a value <= C beside a marker), and only regions whose
+ * whole ring is unresolved wait for their markers (2 extra kernels per level).  The other
+ * deferred pixels are finished by one kernel before the leaves.  Same decisions, same image.
+ * C = 16 * (flag bits 16-27), or MANDEL_DEFER_CAP_DEFAULT when those bits are 0; off when
+ * C >= maxdwell.                                                                           */
+#define MANDEL_FLAG_DEFER 32u
+#define MANDEL_FLAG_DEFER_CAP(C) ((((uint32_t)(C) / 16u) & 0xfffu) << 16)
+#define MANDEL_FLAG_DEFER_CAP_MASK (0xfffu << 16)
+#define MANDEL_DEFER_CAP_DEFAULT 256
 
 /* Kernel kinds reported by mandel_ask_kernel_times (value = kind * 100 + level). */
 enum {
@@ -138,7 +155,10 @@ enum {
     MANDEL_KIND_SBR_LEAF = 6,      /* paper SBR: block-per-leaf interior                      */
     MANDEL_KIND_MBR_LEAF = 7,      /* paper MBR: leaf interiors, flat multi-block             */
     MANDEL_KIND_FLOW_INIT = 8,     /* flow scheme: level-0 tasks + per-level divisors         */
-    MANDEL_KIND_FLOW = 9           /* flow scheme: the persistent dataflow kernel             */
+    MANDEL_KIND_FLOW = 9,          /* flow scheme: the persistent dataflow kernel             */
+    MANDEL_KIND_B200_RESOLVE = 10, /* MANDEL_FLAG_DEFER: finish the markers on the rings of a
+                                      level's uncertain regions, then re-classify them (2)   */
+    MANDEL_KIND_B200_RESUME = 11   /* MANDEL_FLAG_DEFER: finish every remaining marker       */
 };
 
 /* Bytes of workspace mandel_ask / mandel_ask_tiles need for these parameters (worst case
@@ -194,6 +214,9 @@ int mandel_ask_tile_costs(const void *d_ws, uint64_t *h_costs, int32_t max_tiles
 
 /* Number of kernel launches one mandel_ask_tiles call issues for these parameters. */
 int32_t mandel_ask_kernel_count(int64_t n, int32_t g, int32_t r, int32_t B, int32_t scheme);
+/* Same, for a call with these flags and maxdwell (MANDEL_FLAG_DEFER adds kernels). */
+int32_t mandel_ask_kernel_count_ex(int64_t n, int32_t g, int32_t r, int32_t B, int32_t scheme, uint32_t flags,
+                                   int32_t maxdwell);
 
 const char *mandel_strerror(int code);
 const char *mandel_last_cuda_error(void);

@@ -22,6 +22,8 @@ from . import _lib
 SCHEMES = {"sbr": _lib.SCHEME_SBR, "b200": _lib.SCHEME_B200, "mbr": _lib.SCHEME_MBR, "flow": _lib.SCHEME_FLOW}
 # Independent ASK chains per call (MANDEL_FLAG_GROUPS); same image for any value.
 DEFAULT_GROUPS = 1
+# Deferred long pixels (MANDEL_FLAG_DEFER); same image either way.
+DEFAULT_DEFER = False
 
 
 def _torch():
@@ -46,8 +48,13 @@ def workspace_bytes(n: int, g: int, r: int, B: int) -> int:
     return v
 
 
-def kernel_count(n: int, g: int, r: int, B: int, scheme: str = "b200") -> int:
-    return int(_lib.load().mandel_ask_kernel_count(n, g, r, B, SCHEMES[scheme]))
+def kernel_count(n: int, g: int, r: int, B: int, scheme: str = "b200", defer=None, maxdwell: int = 0) -> int:
+    """Kernel launches of one ask() call (defer / maxdwell as passed to ask())."""
+    if not _lib.flag_defer(DEFAULT_DEFER if defer is None else defer):
+        return int(_lib.load().mandel_ask_kernel_count(n, g, r, B, SCHEMES[scheme]))
+    return int(_lib.load().mandel_ask_kernel_count_ex(n, g, r, B, SCHEMES[scheme],
+                                                      _lib.flag_defer(DEFAULT_DEFER if defer is None else defer),
+                                                      max(1, int(maxdwell))))
 
 
 def workspace(n: int, g: int, r: int, B: int, device=None):
@@ -88,13 +95,14 @@ def dp(region: Sequence[float], n: int, maxdwell: int, g: int, r: int, B: int, o
 def ask(region: Sequence[float], n: int, maxdwell: int, g: int, r: int, B: int, out=None, ws=None,
         tiles: Optional[Sequence[int]] = None, scheme: str = "b200", stats: bool = False,
         timing: bool = False, tile_cost: bool = False, flat: bool = False, serial: bool = False,
-        groups: Optional[int] = None, stream=None):
+        groups: Optional[int] = None, defer=None, stream=None):
     """ASK dwell image over all g*g level-0 regions, or only `tiles`.
     stats: accumulate per-level counters (ask_stats); timing: per-kernel events
     (kernel_times); flat: B200 scheme with the plain thread-per-pixel border/leaf kernels
     instead of the lane-refill ones; serial: fills on the main stream instead of concurrent
     graph branches (A/B comparisons, same image); groups: independent level-synchronous
-    chains over round-robin subsets of the tiles, run as parallel graph branches."""
+    chains over round-robin subsets of the tiles, run as parallel graph branches; defer:
+    MANDEL_FLAG_DEFER (True: default cap, int: that iteration cap, False: off)."""
     out = _image(n, out)
     if ws is None:
         ws = workspace(n, g, r, B, device=out.device)
@@ -105,7 +113,8 @@ def ask(region: Sequence[float], n: int, maxdwell: int, g: int, r: int, B: int, 
                                       | (_lib.FLAG_TILE_COST if tile_cost else 0)
                                       | (_lib.FLAG_FLAT if flat else 0)
                                       | (_lib.FLAG_SERIAL if serial else 0)
-                                      | _lib.flag_groups(DEFAULT_GROUPS if groups is None else groups),
+                                      | _lib.flag_groups(DEFAULT_GROUPS if groups is None else groups)
+                                      | _lib.flag_defer(DEFAULT_DEFER if defer is None else defer),
                                       out.data_ptr(), out.stride(0), ws.data_ptr(), ws.numel(),
                                       _stream_ptr(stream))
     _lib.check(rc, "mandel_ask_tiles")

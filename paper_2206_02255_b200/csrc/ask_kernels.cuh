@@ -98,6 +98,13 @@ struct WsHeader {
     // MANDEL_SCHEME_FLOW (flow.cuh): task / unit / fill allocation, publication watermark,
     // consumer cursor, tasks not yet retired
     uint32_t f_task_alloc, f_unit_alloc, f_cursor, f_fill_alloc, f_pending, f_exited;
+    // deferred long pixels: pool entries taken; per level, regions whose
+    // whole ring was unresolved ("uncertain"); work cursors of the resolve kernels and of
+    // the final resume kernel
+    uint32_t n_defer;
+    uint32_t n_unc[MAXL];
+    uint32_t n_defer_snap[MAXL]; // n_defer after level l's border kernel (statistics)
+    unsigned long long cursor_res[MAXL + 1];
 };
 static_assert(sizeof(WsHeader) <= 4096, "header");
 
@@ -166,6 +173,11 @@ struct LevelArgs {
     FastDiv *ffd; // 4 per level
     uint32_t *fmark; // FLOW_CLEAN: the unit array is all zero (survives k_init)
     int r_log2;
+    // deferred long pixels: pool, iteration cap (0: off), uncertain list
+    DeferRec *pool;
+    uint32_t capD;
+    unsigned dcap;
+    uint32_t *unc;
 };
 
 // Hot/cold list addressing: the q-th subdivided parent of level l-1 (q < hot count: front
@@ -563,23 +575,32 @@ __global__ void __launch_bounds__(256) k_b200_border(LevelArgs a)
 // (children written by the region's lanes).  WPR warps per region: one warp for small rings;
 // the whole 256-thread block for large ones (d >= 256, i.e. the first levels, where a warp
 // per region would serialise ~d/8 dependent load rounds).
-template <int WPR>
+//
+// DEFER: ring values may be markers (< 0) of deferred pixels, whose dwell is
+// known only to exceed the cap C.  The region is non-uniform as soon as two resolved values
+// differ, or a resolved value <= C sits beside a marker; uniform when every value is resolved
+// and equal; otherwise ("uncertain": every resolved value equal and > C, with markers) it
+// goes to the level's uncertain list, whose markers k_b200_resolve finishes before
+// UNC = true re-classifies those regions from the list.
+template <int WPR, bool DEFER = false, bool UNC = false>
 __global__ void __launch_bounds__(256) k_b200_classify(LevelArgs a)
 {
     constexpr int TPR = 32 * WPR; // threads per region
-    __shared__ int s_lo[8], s_hi[8];
+    __shared__ int s_lo[8], s_hi[8], s_mn[8];
     __shared__ uint32_t s_base[8 / WPR];
-    const uint32_t count = level_count(a);
+    const uint32_t count = UNC ? *((volatile uint32_t *)&a.hdr->n_unc[a.level]) : level_count(a);
     const int d = a.d, ring = 4 * d - 4, s = d / a.r, rr = a.r * a.r;
     const int t = threadIdx.x % TPR, w = threadIdx.x >> 5, slot = threadIdx.x / TPR;
     const uint32_t per_block = 256 / TPR;
     const uint32_t nh = sub_hot(a);
+    if (DEFER && blockIdx.x == 0 && threadIdx.x == 0)
+        a.hdr->n_defer_snap[a.level] = *((volatile uint32_t *)&a.hdr->n_defer);
     for (uint32_t ri0 = blockIdx.x * per_block; ri0 < count; ri0 += gridDim.x * per_block) {
         const uint32_t ri = ri0 + slot;
         const bool valid = ri < count;
-        const uint32_t off = valid ? region_origin(a, ri, nh) : 0u;
+        const uint32_t off = valid ? (UNC ? a.unc[ri] : region_origin(a, ri, nh)) : 0u;
         const int x0 = unpack_x(off), y0 = unpack_y(off);
-        int lo = INT_MAX, hi = INT_MIN;
+        int lo = INT_MAX, hi = INT_MIN, mn = INT_MAX; // resolved min, max, raw min (markers < 0)
         if (valid) {
             // batches of 8 independent loads in flight per thread (the ring of a level-0
             // region is 8188 pixels: latency, not bandwidth, bounds this loop)
@@ -596,28 +617,47 @@ __global__ void __launch_bounds__(256) k_b200_classify(LevelArgs a)
                 }
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    lo = min(lo, v[j]);
+                    if (DEFER) {
+                        mn = min(mn, v[j]);
+                        lo = min(lo, v[j] < 0 ? INT_MAX : v[j]);
+                    } else {
+                        lo = min(lo, v[j]);
+                    }
                     hi = max(hi, v[j]);
                 }
             }
         }
         lo = __reduce_min_sync(0xffffffffu, lo);
         hi = __reduce_max_sync(0xffffffffu, hi);
+        if (DEFER)
+            mn = __reduce_min_sync(0xffffffffu, mn);
         if (WPR > 1) {
             if ((threadIdx.x & 31) == 0) {
                 s_lo[w] = lo;
                 s_hi[w] = hi;
+                s_mn[w] = mn;
             }
             __syncthreads();
             if (t == 0) {
                 for (int k = 1; k < WPR; ++k) {
                     lo = min(lo, s_lo[k]);
                     hi = max(hi, s_hi[k]);
+                    mn = min(mn, s_mn[k]);
                 }
             }
         }
-        if (t == 0)
-            s_base[slot] = valid ? decide(a, off, lo, hi) : UINT_MAX;
+        if (t == 0) {
+            uint32_t base = UINT_MAX;
+            if (valid) {
+                if (!DEFER || mn >= 0)
+                    base = decide(a, off, lo, hi);
+                else if (hi >= 0 && (lo != hi || lo <= (int)a.dcap))
+                    base = decide(a, off, -1, a.maxdwell); // surely non-uniform; long pixels: hot
+                else
+                    a.unc[atomicAdd(&a.hdr->n_unc[a.level], 1u)] = off;
+            }
+            s_base[slot] = base;
+        }
         if (WPR > 1)
             __syncthreads();
         else
@@ -752,9 +792,10 @@ __device__ __forceinline__ void sink_flush(const StoreSink<STATS, RING> &sk, uns
         atomicAdd(px_dst, px);
 }
 
-template <bool STATS>
+template <bool STATS, bool DEFER = false>
 __global__ void __launch_bounds__(RF_TPB, RFB_MINB) k_b200_border_rf(LevelArgs a)
 {
+    static_assert(!(STATS && DEFER), "statistics passes run every pixel to the end");
     __shared__ ParkedPoint s_q[RF_TPB / 32][MANDEL_RFB_PACK ? RF2_QCAP : RF_QCAP];
 #if MANDEL_RFB_PACK && MANDEL_RFB_PRE > 0
     __shared__ SvPoint s_sv[RF_TPB / 32][MANDEL_RFB_CH];
@@ -783,8 +824,14 @@ __global__ void __launch_bounds__(RF_TPB, RFB_MINB) k_b200_border_rf(LevelArgs a
     refill_loop2<MANDEL_RFB_K, MANDEL_RFB2_T, MANDEL_RFB_CH>(a.map, a.maxdwell, total, &a.hdr->cursor[a.level], map,
                                                              sink, s_q[threadIdx.x >> 5], a.level);
 #else
-    refill_loop<MANDEL_RFB_K, MANDEL_RFB_T, MANDEL_RFB_CH>(a.map, a.maxdwell, total, &a.hdr->cursor[a.level], map,
-                                                           sink, s_q[threadIdx.x >> 5], a.level);
+    if constexpr (DEFER) {
+        const DeferCtx dc{a.pool, a.capD, &a.hdr->n_defer, a.dcap};
+        refill_loop<MANDEL_RFB_K, MANDEL_RFB_T, MANDEL_RFB_CH, BorderMap, StoreSink<STATS, true>, true>(
+            a.map, a.maxdwell, total, &a.hdr->cursor[a.level], map, sink, s_q[threadIdx.x >> 5], a.level, &dc);
+    } else {
+        refill_loop<MANDEL_RFB_K, MANDEL_RFB_T, MANDEL_RFB_CH>(a.map, a.maxdwell, total, &a.hdr->cursor[a.level],
+                                                               map, sink, s_q[threadIdx.x >> 5], a.level);
+    }
 #endif
     sink_flush<STATS, true>(sink, &a.hdr->border_iters[a.level], &a.hdr->border_px[a.level]);
 }
@@ -819,6 +866,74 @@ __global__ void __launch_bounds__(RF_TPB, RFL_MINB) k_b200_leaf_rf(LevelArgs a)
                                                                sink, s_q[threadIdx.x >> 5], 15);
 #endif
     sink_flush<STATS, false>(sink, &a.hdr->leaf_iters, &a.hdr->leaf_px);
+}
+
+// ----------------------------------------------------------------------- deferred pixels
+// Markers on the rings of this level's uncertain regions: t = region * (4d-4) + ring pixel.
+// A pixel shared by two listed regions may be resumed twice; both write the same dwell.
+struct ResolveMap {
+    static constexpr bool kResume = true;
+    const uint32_t *unc;
+    const int *out;
+    long long pitch;
+    const DeferRec *pool;
+    int d;
+    FastDiv fring; // 4d-4
+    __device__ __forceinline__ bool state(uint32_t t, int &px, int &py, float &x, float &y, unsigned &it) const
+    {
+        const uint32_t u = fdiv(t, fring), b = t - u * fring.d;
+        const uint32_t off = unc[u];
+        ring_pixel((int)b, d, unpack_x(off), unpack_y(off), px, py);
+        const int v = __ldcg(out + (long long)py * pitch + px);
+        if (v >= 0)
+            return false;
+        const DeferRec e = pool[-1 - v];
+        x = e.x;
+        y = e.y;
+        it = e.it;
+        return true;
+    }
+};
+
+// Every pool entry whose marker is still in the image (not resolved above).
+struct ResumeMap {
+    static constexpr bool kResume = true;
+    const int *out;
+    long long pitch;
+    const DeferRec *pool;
+    __device__ __forceinline__ bool state(uint32_t t, int &px, int &py, float &x, float &y, unsigned &it) const
+    {
+        const DeferRec e = pool[t];
+        px = (int)(e.pxy & 0xffffu);
+        py = (int)(e.pxy >> 16);
+        if (__ldcg(out + (long long)py * pitch + px) != -1 - (int)t)
+            return false;
+        x = e.x;
+        y = e.y;
+        it = e.it;
+        return true;
+    }
+};
+
+__global__ void __launch_bounds__(RF_TPB, RF_MINB) k_b200_resolve(LevelArgs a)
+{
+    __shared__ ParkedPoint s_q[RF_TPB / 32][RF_QCAP];
+    ResolveMap map{a.unc, a.out, a.pitch, a.pool, a.d, a.fd[0]};
+    const uint32_t total = map.fring.d * *((volatile uint32_t *)&a.hdr->n_unc[a.level]);
+    StoreSink<false, true> sink{&a, 0ull, 0ull};
+    refill_loop<MANDEL_RFB_K, MANDEL_RFB_T, MANDEL_RFB_CH>(a.map, a.maxdwell, total, &a.hdr->cursor_res[a.level],
+                                                           map, sink, s_q[threadIdx.x >> 5], -1);
+}
+
+__global__ void __launch_bounds__(RF_TPB, RF_MINB) k_b200_resume(LevelArgs a)
+{
+    __shared__ ParkedPoint s_q[RF_TPB / 32][RF_QCAP];
+    ResumeMap map{a.out, a.pitch, a.pool};
+    const uint32_t nd = *((volatile uint32_t *)&a.hdr->n_defer);
+    const uint32_t total = nd < a.capD ? nd : a.capD;
+    StoreSink<false, false> sink{&a, 0ull, 0ull}; // image only: colT is not read any more
+    refill_loop<MANDEL_RFB_K, MANDEL_RFB_T, MANDEL_RFB_CH>(a.map, a.maxdwell, total, &a.hdr->cursor_res[MAXL], map,
+                                                           sink, s_q[threadIdx.x >> 5], -1);
 }
 
 } // namespace mandel

@@ -73,6 +73,7 @@ struct Layout {
     int L;
     size_t hdr, tiles, olt[2], fill, leaf, tile_cost, colT, colT_bytes, total;
     size_t ftask, funit, ffill, ffd, fmark; // MANDEL_SCHEME_FLOW (flow.cuh)
+    size_t pool, unc, capD;                 // MANDEL_FLAG_DEFER: deferred-pixel pool, uncertain list
     size_t ftask_cap, funit_cap, ffill_cap;
     int u_log2; // log2 of the leaf side u = (n/g) / r^(L-1)
     size_t fill_off[MAXL]; // element offset of each level's fill segment
@@ -141,6 +142,16 @@ bool make_layout(int64_t n, int32_t g, int32_t r, int32_t B, Layout &lay)
     o = align256(o + (size_t)4 * MAXL * sizeof(FastDiv));
     lay.fmark = o;
     o = align256(o + 4);
+    // deferred long pixels: n^2/64 entries (C3 defers ~1.5% of n^2 pixels at C = 256; a pixel
+    // that finds the pool full is simply computed to the end), and one uncertain-region list
+    // reused by every level
+    lay.capD = (size_t)n * (size_t)n / 64;
+    if (lay.capD < 65536)
+        lay.capD = 65536;
+    lay.pool = o;
+    o = align256(o + lay.capD * sizeof(DeferRec));
+    lay.unc = o;
+    o = align256(o + capmax * 4);
     lay.total = o;
     return true;
 }
@@ -309,6 +320,19 @@ struct Group {
 // Fills (HBM-bound) run on the side stream s2 as graph branches forked after each level's
 // classification and joined at the end, overlapping the ALU-bound dwell kernels; a fill
 // writes only the interior of regions that are terminal, which no later kernel reads.
+// Iteration cap of MANDEL_FLAG_DEFER for a call, 0 when deferral does not apply.
+unsigned defer_cap(uint32_t flags, int32_t scheme, int32_t maxdwell, int ngroups)
+{
+    if (!(flags & MANDEL_FLAG_DEFER) || scheme != MANDEL_SCHEME_B200 || ngroups > 1 ||
+        (flags & (MANDEL_FLAG_STATS | MANDEL_FLAG_TILE_COST | MANDEL_FLAG_FLAT)))
+        return 0u;
+    unsigned c = 16u * ((flags & MANDEL_FLAG_DEFER_CAP_MASK) >> 16);
+    if (c == 0u)
+        c = MANDEL_DEFER_CAP_DEFAULT;
+    c = (c + MANDEL_RFB_K - 1) / MANDEL_RFB_K * MANDEL_RFB_K; // chunk boundaries
+    return c < (unsigned)maxdwell ? c : 0u;
+}
+
 int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, int sms, cudaStream_t s,
                 cudaStream_t s2, cudaEvent_t fork, Timing *tm)
 {
@@ -348,6 +372,13 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
     }
     const bool vec_ok = ((uintptr_t)k.out % 16 == 0) && (k.pitch % 4 == 0);
     const int d0 = (int)(k.n / k.g);
+    a.dcap = defer_cap(k.flags, k.scheme, k.maxdwell, ngroups);
+    const bool defer = a.dcap != 0u;
+    if (defer) {
+        a.pool = (DeferRec *)(ws + lay.pool);
+        a.capD = (uint32_t)lay.capD;
+        a.unc = (uint32_t *)(ws + lay.unc);
+    }
 
     // init: level-0 OLT + zeroed counters
     a.level = 0;
@@ -465,6 +496,9 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
                 if (stats) {
                     int gsz = resident_grid(k_b200_border_rf<true>, RF_TPB, sms, rf_blocks);
                     k_b200_border_rf<true><<<gsz, RF_TPB, 0, s>>>(a);
+                } else if (defer) {
+                    int gsz = resident_grid(k_b200_border_rf<false, true>, RF_TPB, sms, rf_blocks);
+                    k_b200_border_rf<false, true><<<gsz, RF_TPB, 0, s>>>(a);
                 } else {
                     int gsz = resident_grid(k_b200_border_rf<false>, RF_TPB, sms, rf_blocks);
                     k_b200_border_rf<false><<<gsz, RF_TPB, 0, s>>>(a);
@@ -475,13 +509,40 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
             TBEGIN(s);
             if (d >= 256) {
                 int gsz = resident_grid(k_b200_classify<8>, 256, sms, cap);
-                k_b200_classify<8><<<gsz, 256, 0, s>>>(a);
+                if (defer)
+                    k_b200_classify<8, true><<<gsz, 256, 0, s>>>(a);
+                else
+                    k_b200_classify<8><<<gsz, 256, 0, s>>>(a);
             } else {
                 int gsz = resident_grid(k_b200_classify<1>, 256, sms, (cap + 7) / 8);
-                k_b200_classify<1><<<gsz, 256, 0, s>>>(a);
+                if (defer)
+                    k_b200_classify<1, true><<<gsz, 256, 0, s>>>(a);
+                else
+                    k_b200_classify<1><<<gsz, 256, 0, s>>>(a);
             }
             CK(cudaGetLastError());
             TEND(MANDEL_KIND_B200_CLASSIFY, l, s);
+            if (defer) { // finish the uncertain regions' markers, then decide those regions
+                a.fd[0] = fastdiv_nz((uint32_t)(4 * d - 4));
+                TBEGIN(s);
+                {
+                    const size_t rf_blocks = (cap * (size_t)(4 * d - 4) + RF_TPB - 1) / RF_TPB;
+                    int gsz = resident_grid(k_b200_resolve, RF_TPB, sms, rf_blocks);
+                    k_b200_resolve<<<gsz, RF_TPB, 0, s>>>(a);
+                    CK(cudaGetLastError());
+                }
+                TEND(MANDEL_KIND_B200_RESOLVE, l, s);
+                TBEGIN(s);
+                if (d >= 256) {
+                    int gsz = resident_grid(k_b200_classify<8, false, true>, 256, sms, cap);
+                    k_b200_classify<8, false, true><<<gsz, 256, 0, s>>>(a);
+                } else {
+                    int gsz = resident_grid(k_b200_classify<1, false, true>, 256, sms, (cap + 7) / 8);
+                    k_b200_classify<1, false, true><<<gsz, 256, 0, s>>>(a);
+                }
+                CK(cudaGetLastError());
+                TEND(MANDEL_KIND_B200_CLASSIFY, l, s);
+            }
         }
         // fill (terminal work) of this level's uniform regions: flat over all of them
         // (B200, MBR); ASK-SBR filled them inside its level kernel
@@ -508,6 +569,13 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
         }
         if (l + 1 < lay.L)
             d /= k.r;
+    }
+    if (defer) { // every deferred pixel not finished by a level's resolve pass
+        TBEGIN(s);
+        int gsz = resident_grid(k_b200_resume, RF_TPB, sms, (lay.capD + RF_TPB - 1) / RF_TPB);
+        k_b200_resume<<<gsz, RF_TPB, 0, s>>>(a);
+        CK(cudaGetLastError());
+        TEND(MANDEL_KIND_B200_RESUME, 0, s);
     }
     // leaves of the last level
     {
@@ -631,6 +699,17 @@ int32_t mandel_ask_kernel_count(int64_t n, int32_t g, int32_t r, int32_t B, int3
     return 1 + L * (scheme == MANDEL_SCHEME_SBR ? 1 : scheme == MANDEL_SCHEME_MBR ? 2 : 3) + 1;
 }
 
+int32_t mandel_ask_kernel_count_ex(int64_t n, int32_t g, int32_t r, int32_t B, int32_t scheme, uint32_t flags,
+                                   int32_t maxdwell)
+{
+    const int32_t base = mandel_ask_kernel_count(n, g, r, B, scheme);
+    if (base == 0 || maxdwell < 1)
+        return 0;
+    if (!defer_cap(flags, scheme, maxdwell, MANDEL_FLAG_GROUPS_OF(flags)))
+        return base;
+    return base + 2 * levels_of(n, g, r, B) + 1; // resolve + re-classify per level, resume
+}
+
 int mandel_exhaustive(mandel_region reg, int64_t n, int32_t maxdwell, int32_t *d_out, int64_t out_pitch,
                       void *stream)
 {
@@ -668,7 +747,8 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
     if (!valid_grb(n, g, r, B) || !d_ws || (scheme != MANDEL_SCHEME_SBR && scheme != MANDEL_SCHEME_B200 && scheme != MANDEL_SCHEME_MBR &&
                                   scheme != MANDEL_SCHEME_FLOW) ||
         (flags & ~(MANDEL_FLAG_STATS | MANDEL_FLAG_TIMING | MANDEL_FLAG_TILE_COST | MANDEL_FLAG_FLAT |
-                   MANDEL_FLAG_SERIAL | MANDEL_FLAG_GROUPS_MASK)) != 0 ||
+                   MANDEL_FLAG_SERIAL | MANDEL_FLAG_GROUPS_MASK | MANDEL_FLAG_DEFER |
+                   MANDEL_FLAG_DEFER_CAP_MASK)) != 0 ||
         MANDEL_FLAG_GROUPS_OF(flags) > MAXG)
         return MANDEL_EINVAL;
     Layout lay;
@@ -931,6 +1011,7 @@ int mandel_ask_last_stats(const void *d_ws, mandel_level_stats *h_out, int32_t m
         s.side = (int32_t)d;
         s.regions_in = regions;
         s.filled = s.subdivided = s.leaves = s.border_px = s.border_iters = s.leaf_px = s.leaf_iters = 0;
+        s.deferred = s.uncertain = 0;
         for (const auto &hg : hs) {
             s.filled += hg.n_fill[l];
             s.subdivided += hg.n_subdiv[l];
@@ -939,6 +1020,10 @@ int mandel_ask_last_stats(const void *d_ws, mandel_level_stats *h_out, int32_t m
             s.border_iters += (int64_t)hg.border_iters[l];
             s.leaf_px += (l == L - 1) ? (int64_t)hg.leaf_px : 0;
             s.leaf_iters += (l == L - 1) ? (int64_t)hg.leaf_iters : 0;
+            // snapshots are 0 for levels of a call without deferral
+            const uint32_t prev = l > 0 ? hg.n_defer_snap[l - 1] : 0u;
+            s.deferred += hg.n_defer_snap[l] >= prev ? (int64_t)(hg.n_defer_snap[l] - prev) : 0;
+            s.uncertain += hg.n_unc[l];
         }
         regions = s.subdivided * h.r * h.r;
         d /= h.r;

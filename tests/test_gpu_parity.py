@@ -324,3 +324,75 @@ def test_flow_full_size_equals_b200(mb, wname):
     torch.cuda.synchronize()
     assert torch.equal(a, f)
     assert sa == sf
+
+
+# ----------------------------------------------------------------------------- deferred pixels
+def _decisions(stats):
+    return [{k: s[k] for k in ("regions_in", "filled", "subdivided", "leaves")} for s in _trim(stats)]
+
+
+@pytest.mark.parametrize("cap", [16, 48, 128])
+@pytest.mark.parametrize("w", list(W.random_small_workloads(20, seed=W.SEED + 41, max_n=512)),
+                         ids=lambda w: w.name)
+def test_defer_random_small(mb, w, cap):
+    """MANDEL_FLAG_DEFER: border pixels parked at `cap` iterations, regions
+    decided from partial rings, uncertain regions resolved first: same image and the same
+    decisions as the oracle's recursion."""
+    ws = mb.workspace(w.n, w.g, w.r, w.B)
+    out = mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, ws=ws, defer=cap)
+    A, st = oracle.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B)
+    assert np.array_equal(out.cpu().numpy(), A)
+    assert _decisions(mb.ask_stats(ws)) == _decisions(st)
+
+
+@pytest.mark.parametrize("n,g,r,B,md,region", [
+    (256, 2, 2, 2, 300, W.DEFAULT_REGION),
+    (512, 4, 8, 2, 500, W.SEAHORSE_REGION),
+    (1024, 2, 4, 32, 700, W.DEFAULT_REGION),
+    (256, 128, 2, 2, 100, W.DEFAULT_REGION),
+    (512, 1, 2, 4, 1000, W.SEAHORSE_REGION),
+    (256, 4, 2, 8, 64, W.INTERIOR_REGION),      # every ring unresolved: all regions uncertain
+    (256, 4, 2, 8, 64, W.ESCAPE_REGION),        # nothing deferred
+    (2048, 8, 2, 16, 3000, (-0.75, -0.5, 0.0, 0.25)),
+    (256, 2, 2, 8, 700, (-2.25, -1.75, -0.25, 0.25)),  # |c| ~ 2: per-step pixels beside deferred ones
+])
+def test_defer_edge_cases(mb, n, g, r, B, md, region):
+    ws = mb.workspace(n, g, r, B)
+    out = mb.ask(region, n, md, g, r, B, ws=ws, defer=16)
+    A, st = oracle.ask(region, n, md, g, r, B)
+    assert np.array_equal(out.cpu().numpy(), A)
+    got = mb.ask_stats(ws)
+    assert _decisions(got) == _decisions(st)
+    if region == W.INTERIOR_REGION:
+        assert got[0]["uncertain"] == g * g and sum(s["deferred"] for s in got) > 0
+
+
+def test_defer_pool_overflow(mb):
+    """More pixels reach the cap than the pool holds (65536 entries at n <= 2048): the rest
+    are computed to the end in place; the image is unchanged."""
+    n, g, r, B, md = 2048, 4, 2, 16, 2000
+    region = W.SEAHORSE_REGION
+    ws = mb.workspace(n, g, r, B)
+    out = mb.ask(region, n, md, g, r, B, ws=ws, defer=16)
+    st = mb.ask_stats(ws)
+    assert sum(s["deferred"] for s in st) > 65536
+    A, _ = oracle.ask(region, n, md, g, r, B)
+    assert np.array_equal(out.cpu().numpy(), A)
+
+
+@pytest.mark.parametrize("wname", ["C3", "C5", "C4"])
+def test_defer_full_size_equals_plain(mb, wname):
+    """Full BASELINE sizes: the deferred scheme's image equals the plain B200 scheme's on every
+    pixel (and so the oracle wherever test_full_size_ask_sampled_tiles checks it), with the
+    same per-level decisions."""
+    w = W.CONFIGS[wname]
+    ws = mb.workspace(w.n, w.g, w.r, w.B)
+    a = mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, ws=ws, defer=False)
+    sa = _decisions(mb.ask_stats(ws))
+    b = mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, ws=ws, defer=True)
+    sb = mb.ask_stats(ws)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    assert _decisions(sb) == sa
+    assert sum(s["deferred"] for s in sb) > 0
+    del a, b

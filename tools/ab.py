@@ -58,7 +58,8 @@ def main():
                     ts.append(s.elapsed_time(e))
                 res[v] = {"ms_mean": sum(ts) / len(ts), "ms_min": min(ts), "same_image": same}
                 continue
-            kw = VARIANTS[v]
+            # dNNN: MANDEL_FLAG_DEFER with an iteration cap of NNN
+            kw = dict(scheme="b200", defer=int(v[1:])) if v[0] == "d" and v[1:].isdigit() else VARIANTS[v]
             mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, stats=True, **kw)
             st = mb.ask_stats(ws)
             iters = sum(x["border_iters"] + x["leaf_iters"] for x in st)
