@@ -11,8 +11,12 @@ it; an explicit 256 MiB L2 flush also runs between timed steps, outside the per-
 
 N > 1: one process per GPU (torchrun), NCCL process group; level-0 tiles are dealt
 cost-ranked cyclically (paper_2206_02255_b200.deal) from a preview run every rank computes
-redundantly (its time is part of the first step... and reported as preview_ms); no data-path
+redundantly before the timed steps (a per-region plan, reused by every step of the same view);
+its warm wall time is reported as preview_ms and folded into value_incl_preview; no data-path
 collective; the time is the max over ranks of the device time.
+MANDEL_DIST_BACKEND=gloo (test only): gloo process group with CPU-side collectives and every
+rank on cuda:(LOCAL_RANK mod device count), so the N > 1 control flow can be exercised on a
+one-GPU box (ranks then share the GPU: the times are not scaling numbers).
 
 --impl reference: the CPU oracle (oracle/) on the box's host cores on a bounded sample of
 the same workload (the reference arm of this tier), rank 0 only.
@@ -197,10 +201,19 @@ def main():
     from paper_2206_02255_b200 import deal as deal_mod
     from paper_2206_02255_b200 import multigpu
 
+    backend = os.environ.get("MANDEL_DIST_BACKEND", "nccl")
+    if backend not in ("nccl", "gloo"):
+        raise SystemExit(f"MANDEL_DIST_BACKEND={backend}: expected nccl or gloo")
+    if backend == "gloo":
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    cdev = dev if backend == "nccl" else torch.device("cpu")  # device of collective tensors
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     w = W.CONFIGS[args.workload]
     n = w.n
 
@@ -209,12 +222,13 @@ def main():
     parts = [list(range(w.g * w.g))]
     if world > 1:
         if args.deal == "costrank":
+            costs = mb.preview_costs(w.region, n, w.maxdwell, w.g, w.r, w.B)  # cold: captures its graph
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             costs = mb.preview_costs(w.region, n, w.maxdwell, w.g, w.r, w.B)
+            parts = deal_mod.deal("costrank", w.g, world, costs)
             torch.cuda.synchronize()
             preview_ms = 1e3 * (time.perf_counter() - t0)
-            parts = deal_mod.deal("costrank", w.g, world, costs)
         else:
             parts = deal_mod.deal(args.deal, w.g, world)
         tiles = parts[rank]
@@ -262,8 +276,9 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
     my_total = sum(step_ms)
-    total_ms = multigpu.max_over_ranks(my_total, device=dev)
-    exec_iters_all = multigpu.sum_over_ranks([float(exec_iters)], device=dev)[0]
+    total_ms = multigpu.max_over_ranks(my_total, device=cdev)
+    exec_iters_all = multigpu.sum_over_ranks([float(exec_iters)], device=cdev)[0]
+    preview_ms = multigpu.max_over_ranks(preview_ms, device=cdev)
 
     # ---- verification gather to rank 0 (N > 1 only; timed separately, not part of `value`)
     gather = None
@@ -271,15 +286,15 @@ def main():
         torch.cuda.synchronize()
         dist.barrier()
         t0 = time.perf_counter()
-        full = multigpu.gather_image(out, parts, w.g, rank)
+        full = multigpu.gather_image(out if backend == "nccl" else out.cpu(), parts, w.g, rank)
         torch.cuda.synchronize()
         g_ms = 1e3 * (time.perf_counter() - t0)
-        gather = {"ms": multigpu.max_over_ranks(g_ms, device=dev),
+        gather = {"ms": multigpu.max_over_ranks(g_ms, device=cdev), "backend": backend,
                   "bytes_to_rank0": 4 * (n * n - len(parts[0]) * (n // w.g) ** 2)}
         if rank == 0:
             ref = torch.empty_like(out)
             mb.ask(w.region, n, w.maxdwell, w.g, w.r, w.B, out=ref, scheme=args.scheme)
-            gather["bit_exact_vs_1gpu_ask"] = bool(torch.equal(full, ref))
+            gather["bit_exact_vs_1gpu_ask"] = bool(torch.equal(full.to(ref.device), ref))
             del ref
     ms_per_step = total_ms / args.steps
     value = n * n / (ms_per_step / 1e3) / 1e6  # Mpixel/s, whole job
@@ -327,7 +342,7 @@ def main():
             e_ms.append(1e3 * (time.perf_counter() - t0))
         mine = sum(e_ms)
         if world > 1:
-            tt = torch.tensor([mine], dtype=torch.float64, device=dev)
+            tt = torch.tensor([mine], dtype=torch.float64, device=cdev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             mine = float(tt.item())
         e_step = mine / args.steps
@@ -385,6 +400,7 @@ def main():
             "mismatch_fraction_vs_exhaustive": extra.get("mismatch_fraction_vs_exhaustive"),
             "executed_iters_per_step": exec_iters_all,
             "preview_ms": preview_ms,
+            "value_incl_preview": n * n / ((ms_per_step + preview_ms) / 1e3) / 1e6 if world > 1 else None,
             "verify_gather": gather,
             "kernel_ms_per_step": kt_sum,
             "clocks": clocks, "e2e": e2e,
