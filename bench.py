@@ -10,7 +10,7 @@ output image (4 GiB at n = 32768) is far larger than L2 and every step rewrites 
 it; an explicit 256 MiB L2 flush also runs between timed steps, outside the per-step events.
 
 N > 1: one process per GPU (torchrun), NCCL process group; level-0 tiles are dealt
-cost-ranked cyclically (paper_2206_02255_b200.deal) from a preview run every rank computes
+longest-first (LPT, paper_2206_02255_b200.deal) on costs from a preview run every rank computes
 redundantly before the timed steps (a per-region plan, reused by every step of the same view);
 its warm wall time is reported as preview_ms and folded into value_incl_preview; no data-path
 collective; the time is the max over ranks of the device time.
@@ -179,7 +179,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="C3", choices=sorted(W.CONFIGS))
     ap.add_argument("--scheme", default="b200", choices=["b200", "sbr", "mbr"])
-    ap.add_argument("--deal", default="costrank", choices=["costrank", "cyclic", "diagonal"])
+    ap.add_argument("--deal", default="lpt", choices=["lpt", "costrank", "cyclic", "diagonal"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -221,12 +221,12 @@ def main():
     preview_ms = 0.0
     parts = [list(range(w.g * w.g))]
     if world > 1:
-        if args.deal == "costrank":
+        if args.deal in ("costrank", "lpt"):
             costs = mb.preview_costs(w.region, n, w.maxdwell, w.g, w.r, w.B)  # cold: captures its graph
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             costs = mb.preview_costs(w.region, n, w.maxdwell, w.g, w.r, w.B)
-            parts = deal_mod.deal("costrank", w.g, world, costs)
+            parts = deal_mod.deal(args.deal, w.g, world, costs)
             torch.cuda.synchronize()
             preview_ms = 1e3 * (time.perf_counter() - t0)
         else:

@@ -144,10 +144,13 @@ def tile_costs(ws, g: int, stream=None) -> List[int]:
     return _lib.tile_costs(ws.data_ptr(), g, _stream_ptr(stream))
 
 
-def preview_costs(region, n: int, maxdwell: int, g: int, r: int, B: int, shrink: int = 16,
-                  dwell_shrink: int = 8, scheme: str = "b200") -> List[int]:
-    """Per-tile cost estimate for the cost-ranked deal: ASK itself on an
-    n/shrink preview with maxdwell/dwell_shrink and B/shrink (>= 2), same g and r."""
+def preview_costs(region, n: int, maxdwell: int, g: int, r: int, B: int, shrink: int = 8,
+                  dwell_shrink: int = 2, scheme: str = "b200") -> List[int]:
+    """Per-tile cost estimate for the cost-ranked deals: ASK itself on an
+    n/shrink preview with maxdwell/dwell_shrink and B/shrink (>= 2), same g and r.  Default
+    n/8, maxdwell/2: on the seahorse window (C5) the survey's n/16, maxdwell/8 preview misranks
+    the dwell-heavy tiles (8-way imbalance 1.21-1.31 in executed iterations vs 1.02-1.06;
+    profiles/r01_deals_*.jsonl)."""
     pn = max(g * 2, n // shrink)
     pB = max(2, B // shrink)
     while g * pB > pn:

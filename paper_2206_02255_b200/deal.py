@@ -10,6 +10,9 @@ Deals (tile id k = gy * g + gx, canonical order):
              boustrophedon 0..P-1, P-1..0, ...       (cost-ranked cyclic deal); each rank
              keeps its tiles in that descending order, which becomes its level-0 OLT order
              (longest-first: the level-0 kernel's tail is short work)
+  lpt        the same cost order, each tile to the currently least-loaded rank (ties: lowest
+             rank) -- Graham's longest-processing-time-first list schedule; balances better
+             than boustrophedon when a few tiles dominate (the seahorse window, C5)
 """
 from __future__ import annotations
 
@@ -33,6 +36,17 @@ def costrank(costs: Sequence[float], world: int) -> List[List[int]]:
     return out  # each rank's tiles in descending cost: its level-0 work starts with the longest
 
 
+def lpt(costs: Sequence[float], world: int) -> List[List[int]]:
+    order = sorted(range(len(costs)), key=lambda k: (-float(costs[k]), k))
+    out: List[List[int]] = [[] for _ in range(world)]
+    load = [0.0] * world
+    for k in order:
+        r = min(range(world), key=lambda q: (load[q], q))
+        out[r].append(k)
+        load[r] += float(costs[k])
+    return out  # descending cost within each rank, like costrank
+
+
 def deal(method: str, g: int, world: int, costs: Optional[Sequence[float]] = None) -> List[List[int]]:
     if method == "cyclic":
         return cyclic(g, world)
@@ -42,6 +56,10 @@ def deal(method: str, g: int, world: int, costs: Optional[Sequence[float]] = Non
         if costs is None:
             raise ValueError("costrank needs per-tile costs")
         return costrank(costs, world)
+    if method == "lpt":
+        if costs is None:
+            raise ValueError("lpt needs per-tile costs")
+        return lpt(costs, world)
     raise ValueError(method)
 
 

@@ -24,17 +24,17 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("method", ["cyclic", "diagonal", "costrank"])
+@pytest.mark.parametrize("method", ["cyclic", "diagonal", "costrank", "lpt"])
 @pytest.mark.parametrize("g,world", [(16, 2), (16, 8), (4, 3), (8, 8), (2, 8)])
 def test_deal_partitions(method, g, world):
     rng = np.random.default_rng(W.SEED)
-    costs = rng.pareto(1.5, g * g).tolist() if method == "costrank" else None
+    costs = rng.pareto(1.5, g * g).tolist() if method in ("costrank", "lpt") else None
     parts = deal.deal(method, g, world, costs)
     assert len(parts) == world
     flat = sorted(k for p in parts for k in p)
     assert flat == list(range(g * g))                       # disjoint and complete
     sizes = [len(p) for p in parts]
-    assert max(sizes) - min(sizes) <= 1 or method == "diagonal"
+    assert max(sizes) - min(sizes) <= 1 or method in ("diagonal", "lpt")
 
 
 def test_costrank_balances_skewed_costs():
@@ -47,6 +47,21 @@ def test_costrank_balances_skewed_costs():
     cyc = deal.imbalance(deal.cyclic(g, world), costs)
     cr = deal.imbalance(deal.costrank(costs, world), costs)
     assert cyc > 2.0 and cr < 1.1
+
+
+def test_lpt_list_schedule():
+    """Graham's LPT list schedule (tiles in descending cost, each to the least-loaded rank,
+    ties to the lowest rank), hand-traced on small cases, and never worse than the
+    boustrophedon deal on a heavy-tailed seeded cost map."""
+    assert deal.lpt([10, 6, 5, 5], 2) == [[0, 3], [1, 2]]
+    # 8 -> r0; 7 -> r1; 6 -> r1 (7 < 8); 5 -> r0 (8 < 13); 4 -> r0 (13 == 13: lowest rank)
+    assert deal.lpt([8, 7, 6, 5, 4], 2) == [[0, 3, 4], [1, 2]]
+    # one dominant tile: it sits alone, the rest fill the other ranks
+    parts = deal.lpt([100, 1, 1, 1, 1, 1, 1, 1, 1], 3)
+    assert parts[0] == [0] and sorted(parts[1] + parts[2]) == list(range(1, 9))
+    rng = np.random.default_rng(W.SEED + 3)
+    costs = (rng.pareto(1.2, 256) + 1).tolist()
+    assert deal.imbalance(deal.lpt(costs, 8), costs) <= deal.imbalance(deal.costrank(costs, 8), costs) + 1e-12
 
 
 def _worker(rank, world, port, q):

@@ -49,11 +49,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("workload", nargs="?", default="C3")
     ap.add_argument("--ranks", default="1,2,4,8")
-    ap.add_argument("--deals", default="costrank,cyclic,diagonal")
+    ap.add_argument("--deals", default="lpt,costrank,cyclic,diagonal")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--groups", type=int, default=None)
     ap.add_argument("--scheme", default="b200")
     ap.add_argument("--defer", type=int, default=None, help="MANDEL_FLAG_DEFER cap (0: off)")
+    ap.add_argument("--preview", default="8,2", help="preview shrink,dwell_shrink")
     a = ap.parse_args()
     global GROUPS, SCHEME, DEFER
     GROUPS = a.groups
@@ -65,17 +66,24 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    costs = mb.preview_costs(w.region, w.n, w.maxdwell, w.g, w.r, w.B)
+    sh, dsh = (int(x) for x in a.preview.split(","))
+    costs = mb.preview_costs(w.region, w.n, w.maxdwell, w.g, w.r, w.B, shrink=sh, dwell_shrink=dsh)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()  # warm (the first call captured the preview graph)
+    costs = mb.preview_costs(w.region, w.n, w.maxdwell, w.g, w.r, w.B, shrink=sh, dwell_shrink=dsh)
     torch.cuda.synchronize()
     preview_ms = 1e3 * (time.perf_counter() - t0)
     # exact per-tile costs (executed iterations) from one full-size counter pass
     mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, tile_cost=True)
     exact = mb.tile_costs(ws, w.g)
     t1 = time_tiles(w, out, ws, None, flush, a.reps)
-    res = {"workload": w.name, "scheme": SCHEME, "groups": GROUPS, "defer": DEFER, "t1_ms": t1, "preview_ms": preview_ms, "deals": {}}
+    res = {"workload": w.name, "preview": a.preview, "scheme": SCHEME, "groups": GROUPS, "defer": DEFER, "t1_ms": t1, "preview_ms": preview_ms, "deals": {}}
     for dname in a.deals.split(","):
         for P in [int(x) for x in a.ranks.split(",")]:
-            parts = deal.deal(dname, w.g, P, costs if dname == "costrank" else None)
+            # "<deal>_exact": dealt on the exact per-tile costs (the estimator's upper bound)
+            base = dname[:-6] if dname.endswith("_exact") else dname
+            est = exact if dname.endswith("_exact") else costs
+            parts = deal.deal(base, w.g, P, est if base in ("costrank", "lpt") else None)
             per = [time_tiles(w, out, ws, p, flush, a.reps) for p in parts]
             tmax = max(per)
             res["deals"][f"{dname}:{P}"] = {
