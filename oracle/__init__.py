@@ -23,6 +23,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "mandel_oracle.c")
+_SRC3 = os.path.join(_HERE, "mandel3d_oracle.c")  # k = 3 extension
 _LIB = os.path.join(_HERE, "liboracle.so")
 CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared"]
 
@@ -34,9 +35,10 @@ _lib: Optional[ctypes.CDLL] = None
 
 def build(force: bool = False) -> str:
     """Compile liboracle.so with contraction off (R4)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    newest = max(os.path.getmtime(_SRC), os.path.getmtime(_SRC3))
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < newest:
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC])
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, _SRC3])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -50,6 +52,10 @@ class LevelStats(ctypes.Structure):
     _fields_ = [(k, ctypes.c_int64) for k in (
         "regions_in", "filled", "subdivided", "leaves",
         "border_px", "border_iters", "leaf_px", "leaf_iters")]
+
+
+class Region3(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_double) for k in ("re_min", "re_max", "im_min", "im_max", "w_min", "w_max")]
 
 
 class RegionRec(ctypes.Structure):
@@ -89,6 +95,23 @@ def lib() -> ctypes.CDLL:
             L.oracle_ask_by_lookup.argtypes = [i32p, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                                ctypes.c_int, i32p, ctypes.c_int64, i32p,
                                                P(LevelStats), ctypes.c_int]
+            # k = 3 (mandel3d_oracle.c)
+            L.oracle3_dwell.restype = ctypes.c_int32
+            L.oracle3_dwell.argtypes = [ctypes.c_float, ctypes.c_float, ctypes.c_float, ctypes.c_int32]
+            L.oracle3_voxel_c.restype = None
+            L.oracle3_voxel_c.argtypes = [Region3, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                          P(ctypes.c_float), P(ctypes.c_float), P(ctypes.c_float)]
+            L.oracle3_exhaustive_slices.restype = None
+            L.oracle3_exhaustive_slices.argtypes = [Region3, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64,
+                                                    ctypes.c_int64, i32p]
+            L.oracle3_ask_window.restype = ctypes.c_int
+            L.oracle3_ask_window.argtypes = [Region3, ctypes.c_int64, ctypes.c_int32, ctypes.c_int, ctypes.c_int,
+                                             ctypes.c_int, i32p, ctypes.c_int64, i32p, ctypes.c_int64,
+                                             ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                             P(LevelStats), ctypes.c_int]
+            L.oracle3_ask_by_lookup.restype = ctypes.c_int
+            L.oracle3_ask_by_lookup.argtypes = [i32p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                                i32p, P(LevelStats), ctypes.c_int]
             _lib = L
     return _lib
 
@@ -199,4 +222,61 @@ def ask_by_lookup(E: np.ndarray, g: int, r: int, B: int, tiles: Optional[Sequenc
                                     0 if t_arr is None else t_arr.size, _i32(out), st, MAX_LEVELS)
     if rc != 0:
         raise ValueError(f"oracle_ask_by_lookup failed rc={rc}")
+    return out, _stats_list(st, MAX_LEVELS)
+
+
+# ------------------------------------------------------------------------ k = 3
+def dwell3(cr: float, ci: float, w: float, maxdwell: int) -> int:
+    """Dwell of c = cr + i ci from z_0 = w (R15; all three rounded to float32)."""
+    return int(lib().oracle3_dwell(cr, ci, w, maxdwell))
+
+
+def voxel_c(region3, n: int, x: int, y: int, z: int) -> Tuple[float, float, float]:
+    cr, ci, w = ctypes.c_float(), ctypes.c_float(), ctypes.c_float()
+    lib().oracle3_voxel_c(Region3(*region3), n, x, y, z, ctypes.byref(cr), ctypes.byref(ci), ctypes.byref(w))
+    return cr.value, ci.value, w.value
+
+
+def exhaustive3(region3, n: int, maxdwell: int, z0: int = 0, nz: Optional[int] = None) -> np.ndarray:
+    """Exhaustive 3-D dwell volume, z-slices [z0, z0+nz), as int32 (nz, n, n) indexed [z, y, x]."""
+    nz = n - z0 if nz is None else nz
+    out = np.empty((nz, n, n), dtype=np.int32)
+    lib().oracle3_exhaustive_slices(Region3(*region3), n, maxdwell, z0, nz, _i32(out))
+    return out
+
+
+def ask3(region3, n: int, maxdwell: int, g: int, r: int, B: int):
+    """Recursive 3-D ASK volume [z, y, x] and its per-level statistics."""
+    out = np.full((n, n, n), -1, dtype=np.int32)
+    st = (LevelStats * MAX_LEVELS)()
+    rc = lib().oracle3_ask_window(Region3(*region3), n, maxdwell, g, r, B, None, 0, _i32(out), 0, 0, 0, n, n,
+                                  st, MAX_LEVELS)
+    if rc != 0:
+        raise ValueError(f"oracle3_ask_window failed rc={rc}")
+    return out, _stats_list(st, MAX_LEVELS)
+
+
+def ask3_tile(region3, n: int, maxdwell: int, g: int, r: int, B: int, tile: int):
+    """3-D ASK of one level-0 cube (k = (gz*g + gy)*g + gx) into a (d0, d0, d0) array."""
+    d0 = n // g
+    gx, gy, gz = tile % g, (tile // g) % g, tile // (g * g)
+    out = np.full((d0, d0, d0), -1, dtype=np.int32)
+    st = (LevelStats * MAX_LEVELS)()
+    t_arr = np.array([tile], dtype=np.int32)
+    rc = lib().oracle3_ask_window(Region3(*region3), n, maxdwell, g, r, B, _i32(t_arr), 1, _i32(out),
+                                  gx * d0, gy * d0, gz * d0, d0, d0, st, MAX_LEVELS)
+    if rc != 0:
+        raise ValueError(f"oracle3_ask_window failed rc={rc}")
+    return out, _stats_list(st, MAX_LEVELS)
+
+
+def ask3_by_lookup(E: np.ndarray, g: int, r: int, B: int):
+    """3-D ASK decisions replayed over an exhaustive volume E [z, y, x]."""
+    E = np.ascontiguousarray(E, dtype=np.int32)
+    n = E.shape[0]
+    out = np.full((n, n, n), -1, dtype=np.int32)
+    st = (LevelStats * MAX_LEVELS)()
+    rc = lib().oracle3_ask_by_lookup(_i32(E), n, g, r, B, _i32(out), st, MAX_LEVELS)
+    if rc != 0:
+        raise ValueError(f"oracle3_ask_by_lookup failed rc={rc}")
     return out, _stats_list(st, MAX_LEVELS)

@@ -101,3 +101,54 @@ def random_small_workloads(count: int, seed: int = SEED, max_n: int = 512,
         maxdwell = rng.choice([1, 2, 7, 64, 100, 256, 512, 1000])
         yield Workload(f"rand{k}", rng.choice(list(regions)), n, maxdwell, g, r, B)
         k += 1
+
+
+# ------------------------------------------------------------------ k = 3 (NEXT-4)
+# The paper sketches ASK on k-orthotopes without a 3-D workload; R15-R17 fix one:
+# the (c_re, c_im, w) slice of the quadratic family's parameter space, z_0 = w (w = 0 is the
+# Mandelbrot set).  Regions are (re_min, re_max, im_min, im_max, w_min, w_max), dyadic so the
+# voxel centres are exact in FP32.
+Region3 = Tuple[float, float, float, float, float, float]
+
+DEFAULT_REGION3: Region3 = (-1.5, 0.5, -1.0, 1.0, -0.5, 0.5)
+INTERIOR_REGION3: Region3 = (-0.125, 0.125, -0.125, 0.125, -0.25, 0.25)  # |c| <= 1/4, |w| <= 1/2
+ESCAPE_REGION3: Region3 = (2.5, 3.5, 2.5, 3.5, -0.5, 0.5)                # dwell 1 everywhere
+
+
+@dataclasses.dataclass(frozen=True)
+class Workload3:
+    name: str
+    region: Region3
+    n: int
+    maxdwell: int
+    g: int
+    r: int
+    B: int
+
+    def as_dict(self) -> dict:
+        return dataclasses.asdict(self)
+
+
+# Measured 3-D configurations (tools/bench3d.py): a 512^3 (512 MiB) and a 1024^3 (4 GiB)
+# volume; leaves of side 8 (4 levels) and 16.
+V1 = Workload3("V1", DEFAULT_REGION3, 512, 512, 8, 2, 8)
+V2 = Workload3("V2", DEFAULT_REGION3, 1024, 1024, 8, 2, 16)
+CONFIGS3 = {w.name: w for w in (V1, V2)}
+
+
+def random_small_workloads3(count: int, seed: int = SEED, max_n: int = 64) -> Iterator[Workload3]:
+    """Seeded random small 3-D cases (powers of two, g*B <= n, r in {2, 4})."""
+    rng = random.Random(seed)
+    regions = [DEFAULT_REGION3, (-1.0, 0.0, 0.0, 1.0, -0.25, 0.25), (-0.875, -0.625, 0.0, 0.25, 0.0, 0.25),
+               (-1.5, -1.25, -0.125, 0.125, -0.5, 0.0), (0.25, 0.5, -0.125, 0.125, -0.0625, 0.0625)]
+    k = 0
+    while k < count:
+        n = rng.choice(_pow2s(4, max_n))
+        g = rng.choice(_pow2s(1, n // 2))
+        B = rng.choice(_pow2s(2, max(2, n // g)))
+        if g * B > n:
+            continue
+        r = rng.choice([2, 4])
+        maxdwell = rng.choice([1, 2, 7, 64, 100, 256])
+        yield Workload3(f"v{k}", rng.choice(regions), n, maxdwell, g, r, B)
+        k += 1
