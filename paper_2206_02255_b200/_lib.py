@@ -208,3 +208,59 @@ def tile_costs(ws_ptr: int, g: int, stream_ptr: int) -> List[int]:
     if rc < 0:
         raise MandelError(-rc, "mandel_ask_tile_costs")
     return [int(v) for v in buf]
+
+
+# ---------------------------------------------------------------- libmandel3d.so (k = 3)
+LIB3_PATH = os.environ.get("MANDEL3D_LIB") or os.path.join(HERE, "libmandel3d.so")
+
+
+class Mandel3dRegion(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_double) for k in ("re_min", "re_max", "im_min", "im_max", "w_min", "w_max")]
+
+
+class Mandel3dLevelStats(ctypes.Structure):
+    _fields_ = [("level", ctypes.c_int32), ("side", ctypes.c_int32)] + [
+        (k, ctypes.c_int64) for k in ("regions_in", "filled", "subdivided", "leaves",
+                                       "border_px", "border_iters", "leaf_px", "leaf_iters")]
+
+
+_SIGS3 = [
+    ("mandel3d_ask_workspace_bytes", ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                                       ctypes.c_int32]),
+    ("mandel3d_ask_levels", ctypes.c_int32, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
+    ("mandel3d_exhaustive", ctypes.c_int, [Mandel3dRegion, ctypes.c_int64, ctypes.c_int32, _P, _P]),
+    ("mandel3d_ask", ctypes.c_int, [Mandel3dRegion, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                    ctypes.c_int32, ctypes.c_uint32, _P, _P, ctypes.c_size_t, _P]),
+    ("mandel3d_ask_last_stats", ctypes.c_int, [_P, ctypes.POINTER(Mandel3dLevelStats), ctypes.c_int32, _P]),
+    ("mandel3d_last_cuda_error", ctypes.c_char_p, []),
+]
+EXPORTED3 = [s[0] for s in _SIGS3]
+_lib3: Optional[ctypes.CDLL] = None
+
+
+def load_3d() -> ctypes.CDLL:
+    global _lib3
+    with _lock:
+        if _lib3 is None:
+            if not os.path.exists(LIB3_PATH):
+                raise RuntimeError(f"{LIB3_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                                   "g.build()'` (no CPU fallback)")
+            lib = ctypes.CDLL(LIB3_PATH)
+            for name, res, args in _SIGS3:
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib3 = lib
+    return _lib3
+
+
+def check3(rc: int, what: str) -> None:
+    if rc != 0:
+        err = load_3d().mandel3d_last_cuda_error().decode()
+        raise MandelError3(rc, f"{what}: code {rc} ({'invalid argument' if rc == 1 else 'workspace too small' if rc == 2 else err})")
+
+
+class MandelError3(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code

@@ -76,7 +76,29 @@ def build_dp(force: bool = False) -> str:
     return DP_LIB
 
 
+# The k = 3 library (include/mandel3d.h; NEXT-4): same flags as libmandel_b200.so.
+LIB3 = os.path.join(HERE, "libmandel3d.so")
+DEPS3 = ["mandel3d.cu", "dwell.cuh", os.path.join("..", "..", "include", "mandel3d.h")]
+
+
+def build_3d(force: bool = False) -> str:
+    if not force and os.path.exists(LIB3) and not any(
+            os.path.getmtime(os.path.join(SRC_DIR, d)) > os.path.getmtime(LIB3) for d in DEPS3):
+        return LIB3
+    tmp = LIB3 + f".tmp{os.getpid()}"
+    cmd = [NVCC, *NVCC_FLAGS, "-o", tmp, os.path.join(SRC_DIR, "mandel3d.cu")]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("nvcc failed building libmandel3d.so")
+    with open(os.path.join(HERE, "ptxas_info_3d.txt"), "w") as f:
+        f.write(res.stderr)
+    os.replace(tmp, LIB3)
+    return LIB3
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)
     build_dp(force="--force" in sys.argv)
-    print(LIB, DP_LIB)
+    build_3d(force="--force" in sys.argv)
+    print(LIB, DP_LIB, LIB3)

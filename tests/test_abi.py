@@ -170,3 +170,40 @@ def test_product_has_no_oracle_dependency():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "mandel_oracle" not in txt and "liboracle" not in txt, f
+
+
+def test_3d_library_exports_and_validates():
+    """libmandel3d.so (include/mandel3d.h, NEXT-4): every declared function is exported, and
+    argument validation happens before any CUDA call."""
+    build.build_3d()
+    src = open(os.path.join(ROOT, "include", "mandel3d.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    declared = sorted(set(re.findall(r"\b(mandel3d_[a-z_0-9]+)\s*\(", src)))
+    assert declared == sorted(_lib.EXPORTED3)
+    l3 = _lib.load_3d()
+    for name in declared:
+        assert hasattr(l3, name), name
+    assert l3.mandel3d_ask_levels(512, 8, 2, 8) == 4        # 64, 32, 16, 8
+    assert l3.mandel3d_ask_levels(1024, 8, 2, 16) == 4      # 128, 64, 32, 16
+    assert l3.mandel3d_ask_levels(2048, 8, 2, 16) == 0      # n > 1024: u32 SFC scalar
+    assert l3.mandel3d_ask_levels(64, 4, 3, 4) == 0         # r not a power of two
+    # worst case: 2 OLTs + leaf list of (g r^(L-1))^3 u32 + fill lists (8 B per region)
+    M = (8 * 2 ** 3) ** 3
+    ws = l3.mandel3d_ask_workspace_bytes(512, 8, 2, 8)
+    assert 3 * 4 * M + 8 * M < ws < 3 * 4 * M + 8 * M * 8 // 7 + 8192
+    reg = _lib.Mandel3dRegion(-1.5, 0.5, -1.0, 1.0, -0.5, 0.5)
+    bad = _lib.Mandel3dRegion(-1.5, 0.5, -1.0, 1.0, 0.5, -0.5)
+    fake = ctypes.c_void_p(256)
+    assert l3.mandel3d_exhaustive(bad, 64, 10, fake, None) == 1
+    assert l3.mandel3d_exhaustive(reg, 63, 10, fake, None) == 1
+    assert l3.mandel3d_exhaustive(reg, 64, 0, fake, None) == 1
+    need = l3.mandel3d_ask_workspace_bytes(64, 2, 2, 4)
+    assert l3.mandel3d_ask(reg, 64, 10, 2, 2, 4, 0, fake, fake, need - 1, None) == 2
+    assert l3.mandel3d_ask(reg, 64, 10, 2, 2, 4, 2, fake, fake, need, None) == 1   # unknown flag
+    assert l3.mandel3d_ask(reg, 64, 10, 2, 2, 4, 0, None, fake, need, None) == 1
+    out = os.popen(f"/usr/local/cuda/bin/cuobjdump --list-elf {_lib.LIB3_PATH} 2>&1").read()
+    assert "sm_100a" in out
+    sass = os.popen(f"/usr/local/cuda/bin/cuobjdump -sass {_lib.LIB3_PATH} 2>&1").read()
+    for f in re.split(r"\n\s*Function : ", sass)[1:]:
+        if any(k in f.split("\n", 1)[0] for k in ("k3_surface", "k3_leaf", "k3_exhaustive")):
+            assert re.search(r"\bFFMA\b", f) is None and "FMUL" in f and "FADD" in f
