@@ -44,7 +44,7 @@ typedef struct {
     int64_t filled;       /* uniform surface -> filled                                       */
     int64_t subdivided;   /* -> r^3 regions at level + 1                                     */
     int64_t leaves;       /* -> every voxel computed                                         */
-    int64_t border_px;    /* surface voxels computed (MANDEL3D_FLAG_STATS)                   */
+    int64_t border_px;    /* surface voxels computed at this level (MANDEL3D_FLAG_STATS)     */
     int64_t border_iters; /* sum of their dwells (MANDEL3D_FLAG_STATS)                       */
     int64_t leaf_px;      /* leaf interior voxels computed (MANDEL3D_FLAG_STATS)             */
     int64_t leaf_iters;   /* sum of their dwells (MANDEL3D_FLAG_STATS)                       */
@@ -61,8 +61,10 @@ int32_t mandel3d_ask_levels(int64_t n, int32_t g, int32_t r, int32_t B);
 /* Exhaustive volume: one thread per voxel (the speedup denominator). */
 int mandel3d_exhaustive(mandel3d_region reg, int64_t n, int32_t maxdwell, int32_t *d_out, void *stream);
 
-/* 3-D ASK volume over all g^3 level-0 cubes: per level a flat surface kernel (dwell of every
- * surface voxel of every region), a block-per-region classification (min/max reduction;
+/* 3-D ASK volume over all g^3 level-0 cubes: per level a flat surface kernel (level 0: every
+ * surface voxel of every region; deeper levels: only the division-plane voxels of each
+ * subdivided parent, the rest of the children's surfaces being the parent's, already in the
+ * volume), a block-per-region classification (min/max reduction;
  * fill list / r^3 OLT slots by one atomicAdd / leaf list), a flat 128-bit fill of the
  * uniform cubes, and a flat kernel over the leaves' interior voxels at the end; region
  * counts stay in device memory (no host round trip). */

@@ -201,19 +201,65 @@ __global__ void k3_init(Args a)
     }
 }
 
+// Border reuse (as the 2-D B200 scheme): the surfaces of the r^3 children of
+// a subdivided parent (side D = r d) are the parent's surface -- already computed, with its
+// final dwells in the volume -- plus the interior voxels of the parent lying on a division
+// plane (relative coordinate k d - 1 or k d, k = 1..r-1, on some axis).  Per axis the
+// a = D-2 interior values split into M = 2(r-1) plane values and N = r(d-2) others, so the new
+// voxels are a^3 - N^3 = M a^2 + N M a + N^2 M: x on a plane; x off, y on; x, y off, z on.
+__host__ __device__ __forceinline__ long long new_surface_count(int d, int r)
+{
+    const long long a = (long long)r * d - 2, N = (long long)r * (d - 2);
+    return a * a * a - N * N * N;
+}
+__device__ __forceinline__ int plane_val(int i, int d) { return (i / 2 + 1) * d - 1 + (i & 1); }
+__device__ __forceinline__ int off_val(int j, int d) { return (j / (d - 2)) * d + 1 + j % (d - 2); }
+__device__ __forceinline__ void new_surface_voxel(long long t, int d, int r, int &x, int &y, int &z)
+{
+    const long long a = (long long)r * d - 2, M = 2 * (r - 1), N = (long long)r * (d - 2);
+    if (t < M * a * a) { // x on a plane, y and z any interior value
+        const long long i = t / (a * a), q = t - i * a * a;
+        x = plane_val((int)i, d);
+        y = 1 + (int)(q / a);
+        z = 1 + (int)(q % a);
+        return;
+    }
+    t -= M * a * a;
+    if (t < N * M * a) { // x off, y on a plane, z any
+        const long long j = t / (M * a), q = t - j * M * a;
+        x = off_val((int)j, d);
+        y = plane_val((int)(q / a), d);
+        z = 1 + (int)(q % a);
+        return;
+    }
+    t -= N * M * a; // x, y off, z on a plane
+    const long long j = t / (N * M), q = t - j * N * M;
+    x = off_val((int)j, d);
+    y = off_val((int)(q / M), d);
+    z = plane_val((int)(q % M), d);
+}
+
 template <bool STATS>
 __global__ void __launch_bounds__(256) k3_surface(Args a)
 {
     __shared__ unsigned long long s_sum[8];
-    const long long S = surface_count(a.d);
-    const long long total = S * (long long)level_count(a);
+    // level 0: the whole surface of every region; level l > 0: the new plane voxels of every
+    // region subdivided at level l-1 (its first child's corner is the parent's corner)
+    const bool reuse = a.level > 0;
+    const long long S = reuse ? new_surface_count(a.d, a.r) : surface_count(a.d);
+    const uint32_t units = reuse ? *((volatile uint32_t *)&a.hdr->n_subdiv[a.level - 1]) : level_count(a);
+    const long long total = S * (long long)units;
+    const uint32_t rrr = (uint32_t)(a.r * a.r * a.r);
     unsigned long long it = 0, px = 0;
     for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
          t += (long long)gridDim.x * blockDim.x) {
         const uint32_t p = (uint32_t)(t / S);
         int x0, y0, z0, x, y, z;
-        unomega(a, a.olt_in[p], x0, y0, z0);
-        surface_voxel(t - (long long)p * S, a.d, x, y, z);
+        unomega(a, a.olt_in[reuse ? p * rrr : p], x0, y0, z0);
+        if (reuse)
+            new_surface_voxel(t - (long long)p * S, a.d, a.r, x, y, z);
+        else
+            surface_voxel(t - (long long)p * S, a.d, x, y, z);
         x += x0;
         y += y0;
         z += z0;
@@ -524,7 +570,8 @@ int mandel3d_ask(mandel3d_region reg, int64_t n, int32_t maxdwell, int32_t g, in
         a.olt_out = olt[(l + 1) & 1];
         a.fill = (uint2 *)(ws + lay.fill) + lay.fill_off[l];
         const size_t cap = lay.cap[l];
-        const size_t sblocks = (cap * (size_t)surface_count(d) + 255) / 256;
+        const size_t sblocks = (l == 0 ? cap * (size_t)surface_count(d)
+                                       : cap / ((size_t)r * r * r) * (size_t)new_surface_count(d, r)) / 256 + 1;
         if (stats)
             k3_surface<true><<<resident(k3_surface<true>, 256, sblocks), 256, 0, s>>>(a);
         else

@@ -38,9 +38,17 @@ def test_ask3d_parity(m3, w):
     assert np.array_equal(got, A)
     gst = m3.ask3d_stats(ws)
     assert _dec(gst) == _dec(st)
-    for a, b in zip([s for s in gst if s["regions_in"]], st):
-        for k in ("border_px", "border_iters", "leaf_px", "leaf_iters"):
+    gl = [s for s in gst if s["regions_in"]]
+    for lv, (a, b) in enumerate(zip(gl, st)):
+        for k in ("leaf_px", "leaf_iters"):
             assert a[k] == b[k], (k, a, b)
+        if lv == 0:  # level 0 computes whole surfaces, like the oracle
+            assert a["border_px"] == b["border_px"] and a["border_iters"] == b["border_iters"]
+        else:        # deeper levels reuse the parent's surface: only the division planes are new
+            r, d = w.r, a["side"]
+            new = (r * d - 2) ** 3 - (r * (d - 2)) ** 3
+            assert a["border_px"] == gl[lv - 1]["subdivided"] * new
+            assert a["border_iters"] <= b["border_iters"]
 
 
 @pytest.mark.parametrize("n,g,r,B,md,region", [
