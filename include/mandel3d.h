@@ -51,6 +51,8 @@ typedef struct {
 } mandel3d_level_stats;
 
 #define MANDEL3D_FLAG_STATS 1u /* also accumulate the voxel / iteration counters            */
+#define MANDEL3D_FLAG_FLAT 2u  /* plain thread-per-voxel surface and leaf kernels instead of
+                                  the lane-refill ones (A/B; same volume)                    */
 
 /* Workspace bytes for these parameters (0: invalid).  Worst case: every region subdivides. */
 size_t mandel3d_ask_workspace_bytes(int64_t n, int32_t g, int32_t r, int32_t B);
@@ -61,7 +63,8 @@ int32_t mandel3d_ask_levels(int64_t n, int32_t g, int32_t r, int32_t B);
 /* Exhaustive volume: one thread per voxel (the speedup denominator). */
 int mandel3d_exhaustive(mandel3d_region reg, int64_t n, int32_t maxdwell, int32_t *d_out, void *stream);
 
-/* 3-D ASK volume over all g^3 level-0 cubes: per level a flat surface kernel (level 0: every
+/* 3-D ASK volume over all g^3 level-0 cubes: per level a surface kernel (lane-refill engine of
+ * DESIGN.md §4.6 over voxels, or MANDEL3D_FLAG_FLAT thread-per-voxel; level 0: every
  * surface voxel of every region; deeper levels: only the division-plane voxels of each
  * subdivided parent, the rest of the children's surfaces being the parent's, already in the
  * volume), a block-per-region classification (min/max reduction;

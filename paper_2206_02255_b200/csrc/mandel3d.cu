@@ -19,6 +19,11 @@
 
 #include "../../include/mandel3d.h"
 #include "dwell.cuh"
+#include "refill.cuh" // FastDiv: 32-bit multiply-high division by host-computed magics
+
+using mandel::FastDiv;
+using mandel::fdiv;
+using mandel::make_fastdiv;
 
 namespace m3 {
 
@@ -31,6 +36,7 @@ struct Hdr {
     uint32_t n_subdiv[MAXL], n_fill[MAXL], n_leaf;
     uint32_t pad2;
     unsigned long long border_px[MAXL], border_iters[MAXL], leaf_px, leaf_iters;
+    unsigned long long cursor[MAXL + 1]; // lane-refill work cursors: surface level l, leaves
 };
 static_assert(sizeof(Hdr) <= 4096, "header");
 
@@ -85,6 +91,11 @@ struct Args {
     uint32_t *olt_out;
     uint2 *fill; // this level's segment: (Omega, value)
     uint32_t *leaf;
+    // index maps (every flat index space of a call is < n^3 <= 2^30): the level's surface-kernel
+    // unit S, d^2, d, the ring 4d-4; for the division planes a^2, a, M a, N M, M (a = r d - 2,
+    // M = 2(r-1), N = r(d-2)); the leaf interior side m = d-2 and m^3
+    FastDiv fS, fdd, fd, fring, fa2, fa, fMa, fNM, fM, fm, fI;
+    int log_d, log_fill_per, log_fill_row; // fill: d, units per cube, units per row (powers of 2)
 };
 
 __device__ __forceinline__ void unomega(const Args &a, uint32_t o, int &x, int &y, int &z)
@@ -113,20 +124,21 @@ __device__ __forceinline__ uint32_t level_count(const Args &a)
 // Surface voxel s in [0, S(d)) of the cube with corner (x0, y0, z0): the z = 0 and z = d-1
 // faces (d^2 each), then the 4d-4 ring of each slice 1..d-2 (top row, bottom row, left and
 // right columns without their corners).
-__device__ __forceinline__ void surface_voxel(long long s, int d, int &x, int &y, int &z)
+__device__ __forceinline__ void surface_voxel(const Args &a, uint32_t s, int &x, int &y, int &z)
 {
-    const long long dd = (long long)d * d;
-    if (s < 2 * dd) {
-        const int f = (int)(s / dd), q = (int)(s - f * dd);
+    const int d = a.d;
+    const uint32_t dd = a.fdd.d;
+    if (s < 2u * dd) {
+        const uint32_t f = s >= dd ? 1u : 0u, q = s - f * dd;
         z = f ? d - 1 : 0;
-        y = q / d;
-        x = q - y * d;
+        y = (int)fdiv(q, a.fd);
+        x = (int)q - y * d;
         return;
     }
-    const long long t = s - 2 * dd;
-    const int ring = 4 * d - 4;
-    const int zz = (int)(t / ring), b = (int)(t - (long long)zz * ring);
-    z = 1 + zz;
+    const uint32_t t = s - 2u * dd;
+    const uint32_t zz = fdiv(t, a.fring);
+    const int b = (int)(t - zz * a.fring.d);
+    z = 1 + (int)zz;
     if (b < d) {
         x = b;
         y = 0;
@@ -163,6 +175,195 @@ __device__ __forceinline__ unsigned long long block_sum(unsigned long long v, un
         for (int i = 0; i < TPB / 32; ++i)
             t += s[i];
     return t;
+}
+
+// ------------------------------------------------------------------------------ lane refill
+// The 2-D lane-refill engine (refill.cuh) for voxels: persistent warps grab
+// flat indices from a per-launch cursor and deal them to idle lanes; busy lanes run K-step
+// chunks with one escape test per chunk; a finished lane parks its chunk-start point and is
+// refilled once T lanes are parked; 32 parked points are replayed together by bisection over
+// the chunk.  A voxel is identified by its SFC scalar Omega (x | y << logn | z << 2 logn).
+constexpr int RK = 16, RT = 8, RCH = 64, RTPB = 256, RMINB = 4;
+__constant__ int c3_sms;
+
+struct Park3 {
+    uint32_t o;
+    float x, y;
+    unsigned it;
+};
+
+__device__ __forceinline__ void voxel_c(const Args &a, uint32_t o, float &cr, float &ci, float &w)
+{
+    int x, y, z;
+    unomega(a, o, x, y, z);
+    cr = vc(a.ax.x0, a.ax.dx, x);
+    ci = vc(a.ax.y0, a.ax.dy, y);
+    w = vc(a.ax.z0, a.ax.dz, z);
+}
+
+__device__ __forceinline__ int dwell3_per_step(float cr, float ci, float w, int maxdwell)
+{
+    float x = w, y = 0.0f, x2 = __fmul_rn(w, w), y2 = 0.0f;
+    for (int i = 1; i <= maxdwell; ++i) {
+        MANDEL_STEP(x, y, x2, y2, cr, ci);
+        if (__fadd_rn(x2, y2) > 4.0f)
+            return i;
+    }
+    return maxdwell;
+}
+
+template <bool STATS>
+struct Sink3 {
+    const Args *a;
+    unsigned long long iters, px;
+    __device__ __forceinline__ void operator()(uint32_t o, int v)
+    {
+        int x, y, z;
+        unomega(*a, o, x, y, z);
+        a->out[vidx(*a, x, y, z)] = v;
+        if (STATS) {
+            iters += (unsigned long long)v;
+            px += 1;
+        }
+    }
+};
+
+// Replay q[0..cnt) (cnt <= 32), one per lane: bisection over the K steps after the chunk start
+// for the first step where "escaped, or iteration >= maxdwell" holds (monotone, §3.2).
+template <class Sink>
+__device__ __forceinline__ void replay3(const Args &a, const Park3 *q, int cnt, unsigned md, Sink &sink)
+{
+    const int lane = threadIdx.x & 31;
+    if (lane < cnt) {
+        const Park3 p = q[lane];
+        float cr, ci, w;
+        voxel_c(a, p.o, cr, ci, w);
+        float bx = p.x, by = p.y, bx2 = __fmul_rn(bx, bx), by2 = __fmul_rn(by, by);
+        unsigned lo = p.it;
+#pragma unroll
+        for (int h = RK / 2; h >= 1; h /= 2) {
+            float x = bx, y = by, x2 = bx2, y2 = by2;
+#pragma unroll
+            for (int k = 0; k < h; ++k)
+                MANDEL_STEP(x, y, x2, y2, cr, ci);
+            const bool hit = !(__fadd_rn(x2, y2) <= 4.0f) || lo + (unsigned)h >= md;
+            if (!hit) {
+                bx = x;
+                by = y;
+                bx2 = x2;
+                by2 = y2;
+                lo += (unsigned)h;
+            }
+        }
+        sink(p.o, (int)(lo + 1u));
+    }
+    __syncwarp();
+}
+
+// Map: __device__ uint32_t operator()(unsigned long long t) const -> Omega of flat index t.
+template <class Map, class Sink>
+__device__ __forceinline__ void refill3(const Args &a, unsigned long long total, unsigned long long *cursor,
+                                        const Map &map, Sink &sink, Park3 *q)
+{
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const unsigned long long min_active = 8ull * (unsigned long long)c3_sms;
+    unsigned long long act = total / (32ull * 8ull);
+    act = act < min_active ? min_active : act;
+    act = act > nwarps ? nwarps : act;
+    const uint32_t wrank = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+    if (wrank >= act)
+        return;
+    unsigned long long grab = total / (4ull * act);
+    grab = grab < 8ull ? 8ull : (grab > (unsigned long long)RCH ? (unsigned long long)RCH : grab);
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned md = (unsigned)a.maxdwell;
+    unsigned long long pos = 0, end = 0;
+    bool exhausted = false;
+    int qn = 0;
+    bool has = false, fin = false;
+    uint32_t o = 0;
+    float cr = 0.f, ci = 0.f, x = 0.f, y = 0.f, x2 = 0.f, y2 = 0.f, sx = 0.f, sy = 0.f;
+    unsigned it = 0, sit = 0;
+    while (true) {
+        const unsigned f = __ballot_sync(FULL, fin);
+        if (f) {
+            if (fin) {
+                Park3 &e = q[qn + __popc(f & lt)];
+                e.o = o;
+                e.x = sx;
+                e.y = sy;
+                e.it = sit;
+                has = false;
+                fin = false;
+            }
+            qn += __popc(f);
+            __syncwarp();
+            if (qn >= 32) {
+                qn -= 32;
+                replay3(a, q + qn, 32, md, sink);
+            }
+        }
+        unsigned need = __ballot_sync(FULL, !has);
+        while (need && !exhausted) {
+            if (pos >= end) {
+                unsigned long long b = 0;
+                if (lane == 0)
+                    b = atomicAdd(cursor, grab);
+                b = __shfl_sync(FULL, b, 0);
+                if (b >= total) {
+                    exhausted = true;
+                    break;
+                }
+                pos = b;
+                end = b + grab < total ? b + grab : total;
+            }
+            const unsigned cnt = __popc(need);
+            const unsigned avail = (unsigned)(end - pos);
+            const unsigned take = avail < cnt ? avail : cnt;
+            const unsigned rank = __popc(need & lt);
+            if (!has && rank < take) {
+                o = map(pos + rank);
+                float w;
+                voxel_c(a, o, cr, ci, w);
+                const float c2 = __fadd_rn(__fmul_rn(cr, cr), __fmul_rn(ci, ci));
+                if (c2 <= 3.9f) {
+                    has = true;
+                    x = w;
+                    y = 0.0f;
+                    x2 = __fmul_rn(w, w);
+                    y2 = 0.0f;
+                    it = 0;
+                } else {
+                    sink(o, dwell3_per_step(cr, ci, w, a.maxdwell));
+                }
+            }
+            pos += take;
+            need = __ballot_sync(FULL, !has);
+        }
+        const unsigned active = __ballot_sync(FULL, has);
+        if (!active)
+            break;
+        const int thresh = exhausted ? 32 : RT;
+        const bool live = has;
+        while (true) {
+            const bool keep = fin || !live;
+            sx = keep ? sx : x;
+            sy = keep ? sy : y;
+            sit = keep ? sit : it;
+#pragma unroll
+            for (int k = 0; k < RK; ++k)
+                MANDEL_STEP(x, y, x2, y2, cr, ci);
+            it += RK;
+            fin = live && (fin || !(__fadd_rn(x2, y2) <= 4.0f) || it >= md);
+            const unsigned fm = __ballot_sync(FULL, fin);
+            if (fm == active || __popc(fm) >= thresh)
+                break;
+        }
+    }
+    if (qn > 0)
+        replay3(a, q, qn, md, sink);
 }
 
 // ------------------------------------------------------------------------------ kernels
@@ -212,31 +413,38 @@ __host__ __device__ __forceinline__ long long new_surface_count(int d, int r)
     const long long a = (long long)r * d - 2, N = (long long)r * (d - 2);
     return a * a * a - N * N * N;
 }
-__device__ __forceinline__ int plane_val(int i, int d) { return (i / 2 + 1) * d - 1 + (i & 1); }
-__device__ __forceinline__ int off_val(int j, int d) { return (j / (d - 2)) * d + 1 + j % (d - 2); }
-__device__ __forceinline__ void new_surface_voxel(long long t, int d, int r, int &x, int &y, int &z)
+__device__ __forceinline__ int plane_val(uint32_t i, int d) { return (int)(i / 2u + 1u) * d - 1 + (int)(i & 1u); }
+__device__ __forceinline__ int off_val(const Args &a, uint32_t j)
 {
-    const long long a = (long long)r * d - 2, M = 2 * (r - 1), N = (long long)r * (d - 2);
-    if (t < M * a * a) { // x on a plane, y and z any interior value
-        const long long i = t / (a * a), q = t - i * a * a;
-        x = plane_val((int)i, d);
-        y = 1 + (int)(q / a);
-        z = 1 + (int)(q % a);
+    const uint32_t q = fdiv(j, a.fm);
+    return (int)q * a.d + 1 + (int)(j - q * a.fm.d);
+}
+__device__ __forceinline__ void new_surface_voxel(const Args &a, uint32_t t, int &x, int &y, int &z)
+{
+    const uint32_t A2 = a.fa2.d, MA = a.fMa.d;
+    const uint32_t Mv = a.fM.d;
+    const uint32_t blk0 = Mv * A2; // x on a plane, y and z any interior value
+    if (t < blk0) {
+        const uint32_t i = fdiv(t, a.fa2), q = t - i * A2, qy = fdiv(q, a.fa);
+        x = plane_val(i, a.d);
+        y = 1 + (int)qy;
+        z = 1 + (int)(q - qy * a.fa.d);
         return;
     }
-    t -= M * a * a;
-    if (t < N * M * a) { // x off, y on a plane, z any
-        const long long j = t / (M * a), q = t - j * M * a;
-        x = off_val((int)j, d);
-        y = plane_val((int)(q / a), d);
-        z = 1 + (int)(q % a);
+    t -= blk0;
+    const uint32_t blk1 = a.fm.d ? (uint32_t)(a.fNM.d / Mv) * MA : 0u; // N M a: x off, y on, z any
+    if (t < blk1) {
+        const uint32_t j = fdiv(t, a.fMa), q = t - j * MA, qy = fdiv(q, a.fa);
+        x = off_val(a, j);
+        y = plane_val(qy, a.d);
+        z = 1 + (int)(q - qy * a.fa.d);
         return;
     }
-    t -= N * M * a; // x, y off, z on a plane
-    const long long j = t / (N * M), q = t - j * N * M;
-    x = off_val((int)j, d);
-    y = off_val((int)(q / M), d);
-    z = plane_val((int)(q % M), d);
+    t -= blk1; // x, y off, z on a plane
+    const uint32_t j = fdiv(t, a.fNM), q = t - j * a.fNM.d, qy = fdiv(q, a.fM);
+    x = off_val(a, j);
+    y = off_val(a, qy);
+    z = plane_val(q - qy * Mv, a.d);
 }
 
 template <bool STATS>
@@ -246,20 +454,18 @@ __global__ void __launch_bounds__(256) k3_surface(Args a)
     // level 0: the whole surface of every region; level l > 0: the new plane voxels of every
     // region subdivided at level l-1 (its first child's corner is the parent's corner)
     const bool reuse = a.level > 0;
-    const long long S = reuse ? new_surface_count(a.d, a.r) : surface_count(a.d);
     const uint32_t units = reuse ? *((volatile uint32_t *)&a.hdr->n_subdiv[a.level - 1]) : level_count(a);
-    const long long total = S * (long long)units;
+    const uint32_t total = a.fS.d * units;
     const uint32_t rrr = (uint32_t)(a.r * a.r * a.r);
     unsigned long long it = 0, px = 0;
-    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-         t += (long long)gridDim.x * blockDim.x) {
-        const uint32_t p = (uint32_t)(t / S);
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const uint32_t p = fdiv(t, a.fS);
         int x0, y0, z0, x, y, z;
         unomega(a, a.olt_in[reuse ? p * rrr : p], x0, y0, z0);
         if (reuse)
-            new_surface_voxel(t - (long long)p * S, a.d, a.r, x, y, z);
+            new_surface_voxel(a, t - p * a.fS.d, x, y, z);
         else
-            surface_voxel(t - (long long)p * S, a.d, x, y, z);
+            surface_voxel(a, t - p * a.fS.d, x, y, z);
         x += x0;
         y += y0;
         z += z0;
@@ -294,9 +500,9 @@ __global__ void __launch_bounds__(256) k3_classify(Args a)
         int x0, y0, z0;
         unomega(a, off, x0, y0, z0);
         int lo = INT_MAX, hi = INT_MIN;
-        for (long long s = threadIdx.x; s < S; s += blockDim.x) {
+        for (uint32_t s = threadIdx.x; s < (uint32_t)S; s += blockDim.x) {
             int x, y, z;
-            surface_voxel(s, a.d, x, y, z);
+            surface_voxel(a, s, x, y, z);
             const int v = __ldcg(a.out + vidx(a, x0 + x, y0 + y, z0 + z));
             lo = min(lo, v);
             hi = max(hi, v);
@@ -340,19 +546,18 @@ __global__ void __launch_bounds__(256) k3_classify(Args a)
 template <bool VEC>
 __global__ void __launch_bounds__(256) k3_fill(Args a)
 {
-    const unsigned long long count = *((volatile uint32_t *)&a.hdr->n_fill[a.level]);
+    const uint32_t count = *((volatile uint32_t *)&a.hdr->n_fill[a.level]);
     const int d = a.d;
-    const int lx = VEC ? d / 4 : d; // units per row
-    const unsigned long long per = (unsigned long long)lx * d * d;
-    const unsigned long long total = count * per;
-    for (unsigned long long u = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; u < total;
-         u += (unsigned long long)gridDim.x * blockDim.x) {
-        const unsigned long long e = u / per;
-        const unsigned long long rem = u - e * per;
+    const uint32_t total = count << a.log_fill_per; // units: int4 (VEC) or int
+    const uint32_t rmask = (1u << a.log_fill_row) - 1u, dmask = (uint32_t)d - 1u;
+    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < total; u += gridDim.x * blockDim.x) {
+        const uint32_t e = u >> a.log_fill_per;
+        const uint32_t rem = u - (e << a.log_fill_per);
         const uint2 f = a.fill[e];
         int x0, y0, z0;
         unomega(a, f.x, x0, y0, z0);
-        const int ux = (int)(rem % lx), y = (int)((rem / lx) % d), z = (int)(rem / ((unsigned long long)lx * d));
+        const int ux = (int)(rem & rmask), y = (int)((rem >> a.log_fill_row) & dmask),
+                  z = (int)(rem >> (a.log_fill_row + a.log_d));
         const int v = (int)f.y;
         if (VEC)
             __stcs(reinterpret_cast<int4 *>(a.out + vidx(a, x0 + 4 * ux, y0 + y, z0 + z)), make_int4(v, v, v, v));
@@ -361,22 +566,84 @@ __global__ void __launch_bounds__(256) k3_fill(Args a)
     }
 }
 
+// Flat index -> voxel maps of the surface and leaf kernels, for the lane-refill engine.
+struct SurfMap {
+    Args a;
+    bool reuse;
+    __device__ __forceinline__ uint32_t operator()(unsigned long long tt) const
+    {
+        const uint32_t t = (uint32_t)tt, p = fdiv(t, a.fS);
+        int x0, y0, z0, x, y, z;
+        unomega(a, a.olt_in[reuse ? p * (uint32_t)(a.r * a.r * a.r) : p], x0, y0, z0);
+        if (reuse)
+            new_surface_voxel(a, t - p * a.fS.d, x, y, z);
+        else
+            surface_voxel(a, t - p * a.fS.d, x, y, z);
+        return omega(a, x0 + x, y0 + y, z0 + z);
+    }
+};
+struct LeafMap3 {
+    Args a;
+    __device__ __forceinline__ uint32_t operator()(unsigned long long tt) const
+    {
+        const uint32_t t = (uint32_t)tt, li = fdiv(t, a.fI), loc = t - li * a.fI.d;
+        const uint32_t q = fdiv(loc, a.fm), lz = fdiv(q, a.fm);
+        int x0, y0, z0;
+        unomega(a, a.leaf[li], x0, y0, z0);
+        return omega(a, x0 + 1 + (int)(loc - q * a.fm.d), y0 + 1 + (int)(q - lz * a.fm.d), z0 + 1 + (int)lz);
+    }
+};
+
+template <bool STATS>
+__global__ void __launch_bounds__(RTPB, RMINB) k3_surface_rf(Args a)
+{
+    __shared__ Park3 s_q[RTPB / 32][64];
+    __shared__ unsigned long long s_sum[RTPB / 32];
+    const bool reuse = a.level > 0;
+    SurfMap map{a, reuse};
+    const uint32_t units = reuse ? *((volatile uint32_t *)&a.hdr->n_subdiv[a.level - 1]) : level_count(a);
+    Sink3<STATS> sink{&a, 0ull, 0ull};
+    refill3(a, (unsigned long long)a.fS.d * units, &a.hdr->cursor[a.level], map, sink, s_q[threadIdx.x >> 5]);
+    if (STATS) {
+        const unsigned long long it = block_sum<RTPB>(sink.iters, s_sum);
+        if (threadIdx.x == 0 && it)
+            atomicAdd(&a.hdr->border_iters[a.level], it);
+        const unsigned long long px = block_sum<RTPB>(sink.px, s_sum);
+        if (threadIdx.x == 0 && px)
+            atomicAdd(&a.hdr->border_px[a.level], px);
+    }
+}
+
+template <bool STATS>
+__global__ void __launch_bounds__(RTPB, RMINB) k3_leaf_rf(Args a)
+{
+    __shared__ Park3 s_q[RTPB / 32][64];
+    __shared__ unsigned long long s_sum[RTPB / 32];
+    LeafMap3 map{a};
+    Sink3<STATS> sink{&a, 0ull, 0ull};
+    if (a.fI.d > 0)
+        refill3(a, (unsigned long long)a.fI.d * *((volatile uint32_t *)&a.hdr->n_leaf), &a.hdr->cursor[MAXL], map,
+                sink, s_q[threadIdx.x >> 5]);
+    if (STATS) {
+        const unsigned long long it = block_sum<RTPB>(sink.iters, s_sum);
+        if (threadIdx.x == 0 && it)
+            atomicAdd(&a.hdr->leaf_iters, it);
+        const unsigned long long px = block_sum<RTPB>(sink.px, s_sum);
+        if (threadIdx.x == 0 && px)
+            atomicAdd(&a.hdr->leaf_px, px);
+    }
+}
+
 template <bool STATS>
 __global__ void __launch_bounds__(256) k3_leaf(Args a)
 {
     __shared__ unsigned long long s_sum[8];
-    const int m = a.d - 2;
-    const unsigned long long I = m > 0 ? (unsigned long long)m * m * m : 0ull;
-    const unsigned long long total = I * *((volatile uint32_t *)&a.hdr->n_leaf);
+    const uint32_t total = a.fI.d * *((volatile uint32_t *)&a.hdr->n_leaf);
+    const LeafMap3 map{a};
     unsigned long long it = 0, px = 0;
-    for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-         t += (unsigned long long)gridDim.x * blockDim.x) {
-        const unsigned long long li = t / I;
-        const unsigned long long loc = t - li * I;
-        int x0, y0, z0;
-        unomega(a, a.leaf[li], x0, y0, z0);
-        const int x = x0 + 1 + (int)(loc % m), y = y0 + 1 + (int)((loc / m) % m),
-                  z = z0 + 1 + (int)(loc / ((unsigned long long)m * m));
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        int x, y, z;
+        unomega(a, map(t), x, y, z);
         const int v = dwell3(vc(a.ax.x0, a.ax.dx, x), vc(a.ax.y0, a.ax.dy, y), vc(a.ax.z0, a.ax.dz, z), a.maxdwell);
         a.out[vidx(a, x, y, z)] = v;
         if (STATS) {
@@ -476,6 +743,15 @@ bool make_layout(int64_t n, int32_t g, int32_t r, int32_t B, Layout &lay)
     return true;
 }
 
+FastDiv nz_div(uint32_t d) // divisor 0 marks an empty index space (the map is never evaluated)
+{
+    if (d == 0) {
+        FastDiv f{0u, 0u, 0u, 0u};
+        return f;
+    }
+    return make_fastdiv(d);
+}
+
 Axis make_axis(const mandel3d_region &reg, int64_t n)
 {
     Axis ax;
@@ -534,13 +810,24 @@ int mandel3d_ask(mandel3d_region reg, int64_t n, int32_t maxdwell, int32_t g, in
                  int32_t *d_out, void *d_ws, size_t ws_bytes, void *stream)
 {
     Layout lay;
-    if (!valid_region(reg) || maxdwell < 1 || !d_out || !d_ws || (flags & ~MANDEL3D_FLAG_STATS) ||
+    if (!valid_region(reg) || maxdwell < 1 || !d_out || !d_ws || (flags & ~(MANDEL3D_FLAG_STATS | MANDEL3D_FLAG_FLAT)) ||
         !make_layout(n, g, r, B, lay) || ((uintptr_t)d_ws % 256) != 0 || ((uintptr_t)d_out % 16) != 0)
         return 1;
     if (ws_bytes < lay.total)
         return 2;
     const bool stats = (flags & MANDEL3D_FLAG_STATS) != 0;
+    const bool flat = (flags & MANDEL3D_FLAG_FLAT) != 0;
     cudaStream_t s = (cudaStream_t)stream;
+    {
+        static int sms_dev = -1; // c3_sms of the current device (the engine's active-warp floor)
+        int dev = 0, sms = 0;
+        CK3(cudaGetDevice(&dev));
+        if (dev != sms_dev) {
+            CK3(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            CK3(cudaMemcpyToSymbol(c3_sms, &sms, sizeof sms));
+            sms_dev = dev;
+        }
+    }
     char *ws = (char *)d_ws;
     Args a;
     memset(&a, 0, sizeof a);
@@ -569,13 +856,36 @@ int mandel3d_ask(mandel3d_region reg, int64_t n, int32_t maxdwell, int32_t g, in
         a.olt_in = olt[l & 1];
         a.olt_out = olt[(l + 1) & 1];
         a.fill = (uint2 *)(ws + lay.fill) + lay.fill_off[l];
+        {
+            const uint32_t A = (uint32_t)(r * d - 2), M = (uint32_t)(2 * (r - 1)), N = (uint32_t)(r * (d - 2));
+            const uint32_t m = (uint32_t)(d - 2);
+            a.fS = make_fastdiv((uint32_t)(l == 0 ? surface_count(d) : new_surface_count(d, r)));
+            a.fdd = make_fastdiv((uint32_t)(d * d));
+            a.fd = make_fastdiv((uint32_t)d);
+            a.fring = make_fastdiv((uint32_t)(4 * d - 4));
+            a.fa2 = make_fastdiv(A * A);
+            a.fa = make_fastdiv(A);
+            a.fMa = make_fastdiv(M * A);
+            a.fNM = nz_div(N * M);
+            a.fM = make_fastdiv(M);
+            a.fm = nz_div(m);
+            a.fI = nz_div(m * m * m);
+            const bool v4 = d % 4 == 0;
+            a.log_d = lg2(d);
+            a.log_fill_row = lg2(v4 ? d / 4 : d);
+            a.log_fill_per = a.log_fill_row + 2 * a.log_d;
+        }
         const size_t cap = lay.cap[l];
         const size_t sblocks = (l == 0 ? cap * (size_t)surface_count(d)
                                        : cap / ((size_t)r * r * r) * (size_t)new_surface_count(d, r)) / 256 + 1;
-        if (stats)
+        if (flat && stats)
             k3_surface<true><<<resident(k3_surface<true>, 256, sblocks), 256, 0, s>>>(a);
-        else
+        else if (flat)
             k3_surface<false><<<resident(k3_surface<false>, 256, sblocks), 256, 0, s>>>(a);
+        else if (stats)
+            k3_surface_rf<true><<<resident(k3_surface_rf<true>, RTPB, sblocks), RTPB, 0, s>>>(a);
+        else
+            k3_surface_rf<false><<<resident(k3_surface_rf<false>, RTPB, sblocks), RTPB, 0, s>>>(a);
         CK3(cudaGetLastError());
         k3_classify<<<resident(k3_classify, 256, cap), 256, 0, s>>>(a);
         CK3(cudaGetLastError());
@@ -592,10 +902,14 @@ int mandel3d_ask(mandel3d_region reg, int64_t n, int32_t maxdwell, int32_t g, in
     const size_t lblocks = (lay.cap[lay.L - 1] * (size_t)(d > 2 ? d - 2 : 0) * (d > 2 ? d - 2 : 0) *
                                 (d > 2 ? d - 2 : 0) + 255) / 256;
     if (lblocks > 0) {
-        if (stats)
+        if (flat && stats)
             k3_leaf<true><<<resident(k3_leaf<true>, 256, lblocks), 256, 0, s>>>(a);
-        else
+        else if (flat)
             k3_leaf<false><<<resident(k3_leaf<false>, 256, lblocks), 256, 0, s>>>(a);
+        else if (stats)
+            k3_leaf_rf<true><<<resident(k3_leaf_rf<true>, RTPB, lblocks), RTPB, 0, s>>>(a);
+        else
+            k3_leaf_rf<false><<<resident(k3_leaf_rf<false>, RTPB, lblocks), RTPB, 0, s>>>(a);
         CK3(cudaGetLastError());
     }
     return 0;

@@ -61,12 +61,14 @@ def exhaustive3d(region3, n: int, maxdwell: int, out=None, stream=None):
 
 
 def ask3d(region3, n: int, maxdwell: int, g: int, r: int, B: int, out=None, ws=None, stats: bool = False,
-          stream=None):
-    """3-D ASK volume over all g^3 level-0 cubes (surface test, fill / r^3 split / leaf)."""
+          flat: bool = False, stream=None):
+    """3-D ASK volume over all g^3 level-0 cubes (surface test, fill / r^3 split / leaf);
+    flat: thread-per-voxel surface/leaf kernels instead of the lane-refill engine (A/B)."""
     out = _volume(n, out)
     if ws is None:
         ws = workspace3d(n, g, r, B, device=out.device)
-    rc = _lib.load_3d().mandel3d_ask(_region(region3), n, maxdwell, g, r, B, 1 if stats else 0, out.data_ptr(),
+    rc = _lib.load_3d().mandel3d_ask(_region(region3), n, maxdwell, g, r, B, (1 if stats else 0) | (2 if flat else 0),
+                                     out.data_ptr(),
                                      ws.data_ptr(), ws.numel(), _stream_ptr(stream))
     _lib.check3(rc, "mandel3d_ask")
     return out

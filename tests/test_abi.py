@@ -199,11 +199,11 @@ def test_3d_library_exports_and_validates():
     assert l3.mandel3d_exhaustive(reg, 64, 0, fake, None) == 1
     need = l3.mandel3d_ask_workspace_bytes(64, 2, 2, 4)
     assert l3.mandel3d_ask(reg, 64, 10, 2, 2, 4, 0, fake, fake, need - 1, None) == 2
-    assert l3.mandel3d_ask(reg, 64, 10, 2, 2, 4, 2, fake, fake, need, None) == 1   # unknown flag
+    assert l3.mandel3d_ask(reg, 64, 10, 2, 2, 4, 4, fake, fake, need, None) == 1   # unknown flag
     assert l3.mandel3d_ask(reg, 64, 10, 2, 2, 4, 0, None, fake, need, None) == 1
     out = os.popen(f"/usr/local/cuda/bin/cuobjdump --list-elf {_lib.LIB3_PATH} 2>&1").read()
     assert "sm_100a" in out
     sass = os.popen(f"/usr/local/cuda/bin/cuobjdump -sass {_lib.LIB3_PATH} 2>&1").read()
     for f in re.split(r"\n\s*Function : ", sass)[1:]:
-        if any(k in f.split("\n", 1)[0] for k in ("k3_surface", "k3_leaf", "k3_exhaustive")):
+        if any(k in f.split("\n", 1)[0] for k in ("k3_surface", "k3_leaf", "k3_exhaustive")):  # incl. _rf
             assert re.search(r"\bFFMA\b", f) is None and "FMUL" in f and "FADD" in f

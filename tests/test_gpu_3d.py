@@ -30,10 +30,11 @@ def test_exhaustive3d_parity(m3, w):
     assert np.array_equal(got, oracle.exhaustive3(w.region, w.n, w.maxdwell))
 
 
+@pytest.mark.parametrize("flat", [False, True], ids=["refill", "flat"])
 @pytest.mark.parametrize("w", list(W.random_small_workloads3(40, seed=W.SEED + 62, max_n=64)), ids=lambda w: w.name)
-def test_ask3d_parity(m3, w):
+def test_ask3d_parity(m3, w, flat):
     ws = m3.workspace3d(w.n, w.g, w.r, w.B)
-    got = m3.ask3d(w.region, w.n, w.maxdwell, w.g, w.r, w.B, ws=ws, stats=True).cpu().numpy()
+    got = m3.ask3d(w.region, w.n, w.maxdwell, w.g, w.r, w.B, ws=ws, stats=True, flat=flat).cpu().numpy()
     A, st = oracle.ask3(w.region, w.n, w.maxdwell, w.g, w.r, w.B)
     assert np.array_equal(got, A)
     gst = m3.ask3d_stats(ws)

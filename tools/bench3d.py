@@ -50,6 +50,9 @@ def main():
         iters = sum(s["border_iters"] + s["leaf_iters"] for s in st)
         t_ask, t_ask_mean = timed(lambda: m3.ask3d(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=vol, ws=ws),
                                   a.reps, flush)
+        t_flat, _ = timed(lambda: m3.ask3d(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=ex, ws=ws, flat=True),
+                          a.reps, flush)  # A/B: thread-per-voxel surface and leaf kernels
+        same_flat = bool(torch.equal(ex, vol))
         t_ex, t_ex_mean = timed(lambda: m3.exhaustive3d(w.region, w.n, w.maxdwell, out=ex), max(2, a.reps // 2), flush)
         sum_ex = int(ex.sum(dtype=torch.int64).item())
         mism = int((vol != ex).sum().item())
@@ -57,6 +60,7 @@ def main():
         print(json.dumps({
             "config": w.as_dict(), "levels": len(st),
             "ask_ms": t_ask, "ask_ms_mean": t_ask_mean, "ex_ms": t_ex, "ex_ms_mean": t_ex_mean,
+            "ask_flat_ms": t_flat, "flat_same_volume": same_flat,
             "ask_mvoxel_s": nv / t_ask / 1e3, "ex_mvoxel_s": nv / t_ex / 1e3, "speedup_vs_exhaustive": t_ex / t_ask,
             "mismatch_fraction_vs_exhaustive": mism / nv,
             "ask_executed_iters": iters, "ex_iters": sum_ex, "work_ratio": sum_ex / max(1, iters),
