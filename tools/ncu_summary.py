@@ -38,8 +38,8 @@ SCALE = {"ms": 1.0, "us": 1e-3, "ns": 1e-6, "s": 1e3,
 
 
 def kind_of(name: str) -> str:
-    m = re.search(r"k_(b200_border_rf|b200_border|b200_classify|b200_leaf_rf|b200_leaf|fill|sbr_level|sbr_leaf|"
-                  r"exhaustive\w*|init)", name)
+    m = re.search(r"k3?_(b200_border_rf|b200_border|b200_classify|b200_leaf_rf|b200_leaf|fill|sbr_level|sbr_leaf|"
+                  r"exhaustive\w*|init|surface_rf|surface|classify|leaf_rf|leaf)", name)
     if not m:
         return name[:40]
     return m.group(1)[:-3] if m.group(1).endswith("_rf") else m.group(1)  # bench.py kind names
