@@ -74,6 +74,15 @@ struct ParkedPoint {
 
 constexpr int RF_QCAP = 64; // per-warp queue entries (< 32 left over + < 32 new)
 
+// Scalar engine launch shape (knobs for tools/tune_refill.py): a launch activates
+// ~total / (32 PPL) warps, at least MINW per SM (MINW / 4 per sub-partition).
+#ifndef MANDEL_RF_PPL
+#define MANDEL_RF_PPL 8u
+#endif
+#ifndef MANDEL_RF_MINW
+#define MANDEL_RF_MINW 8u
+#endif
+
 // Deferred long pixels.  A border pixel still unescaped after `cap`
 // iterations is parked in the workspace pool with its orbit state and its image (and colT)
 // slot holds the marker -1 - (pool index); its dwell is finished later (k_b200_resolve for
@@ -174,9 +183,9 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
     // B200), below which one warp per scheduler is latency-bound.  Warp w of block b has
     // rank w*gridDim+b, so the active warps spread over all SMs.  (Idle warps return here and
     // still reach the caller's block-wide reductions.)
-    constexpr uint32_t PPL = 8;
+    constexpr uint32_t PPL = MANDEL_RF_PPL;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    const uint32_t min_active = 8u * (uint32_t)c_num_sms;
+    const uint32_t min_active = MANDEL_RF_MINW * (uint32_t)c_num_sms;
     uint32_t active = total / (32u * PPL);
     active = active < min_active ? min_active : active;
     active = active > nwarps ? nwarps : active;
