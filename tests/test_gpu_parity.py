@@ -188,6 +188,11 @@ def test_full_size_ask_sampled_tiles(mb, wname):
     out = mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, ws=ws, stats=True)
     torch.cuda.synchronize()
     st = mb.ask_stats(ws)
+    # bench.py's timed launch (no counters, per-kernel timing events) gives the same image
+    bench_img = mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, ws=ws, timing=True)
+    torch.cuda.synchronize()
+    assert torch.equal(bench_img, out)
+    del bench_img
     d0 = w.n // w.g
     tiles = _sample_tiles(w.g, 2 if wname == "C4" else 3, W.SEED + int(wname[1]))
     for t in tiles:
