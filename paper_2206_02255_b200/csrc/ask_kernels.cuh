@@ -646,27 +646,80 @@ __global__ void __launch_bounds__(256) k_b200_classify(LevelArgs a)
                 }
             }
         }
-        if (t == 0) {
-            uint32_t base = UINT_MAX;
-            if (valid) {
-                if (!DEFER || mn >= 0)
-                    base = decide(a, off, lo, hi);
-                else if (hi >= 0 && (lo != hi || lo <= (int)a.dcap))
-                    base = decide(a, off, -1, a.maxdwell); // surely non-uniform; long pixels: hot
-                else
-                    a.unc[atomicAdd(&a.hdr->n_unc[a.level], 1u)] = off;
+        if (WPR == 1 && !DEFER) {
+            // Block-aggregated appends: one atomicAdd per outcome per block of 8 regions
+            // instead of two per region (the deep levels hold ~10^5 regions, and per-region
+            // atomics on a handful of counters serialise in L2).  Same outcomes and slot
+            // addressing as decide(): hot parents / leaves from the front, cold from the back.
+            __shared__ int s_cat[8];
+            __shared__ uint32_t s_cb[6];
+            if (t == 0) {
+                int cat = 0; // 0 none, 1 fill, 2/3 subdivide hot/cold, 4/5 leaf hot/cold
+                if (valid) {
+                    const bool hot = 2 * hi >= a.maxdwell;
+                    cat = lo == hi ? 1 : a.subdivide ? (hot ? 2 : 3) : (hot ? 4 : 5);
+                }
+                s_cat[slot] = cat;
             }
-            s_base[slot] = base;
-        }
-        if (WPR > 1)
             __syncthreads();
-        else
-            __syncwarp();
+            if (threadIdx.x == 0) {
+                uint32_t c[6] = {0u, 0u, 0u, 0u, 0u, 0u};
+                for (int k = 0; k < 8; ++k)
+                    ++c[s_cat[k]];
+                s_cb[1] = c[1] ? atomicAdd(&a.hdr->n_fill[a.level], c[1]) : 0u;
+                if (c[2] + c[3])
+                    atomicAdd(&a.hdr->n_subdiv[a.level], c[2] + c[3]);
+                s_cb[2] = c[2] ? atomicAdd(&a.hdr->n_sub_hot[a.level], c[2]) : 0u;
+                s_cb[3] = c[3] ? atomicAdd(&a.hdr->n_sub_cold[a.level], c[3]) : 0u;
+                if (c[4] + c[5])
+                    atomicAdd(&a.hdr->n_leaf, c[4] + c[5]);
+                s_cb[4] = c[4] ? atomicAdd(&a.hdr->n_leaf_hot, c[4]) : 0u;
+                s_cb[5] = c[5] ? atomicAdd(&a.hdr->n_leaf_cold, c[5]) : 0u;
+            }
+            __syncthreads();
+            if (t == 0) {
+                const int cat = s_cat[slot];
+                uint32_t rank = 0;
+                for (int k = 0; k < slot; ++k)
+                    rank += s_cat[k] == cat ? 1u : 0u;
+                const uint32_t e = s_cb[cat] + rank;
+                uint32_t base = UINT_MAX;
+                if (cat == 1)
+                    a.fill[e] = make_uint2(off, (uint32_t)lo);
+                else if (cat == 2)
+                    base = e;
+                else if (cat == 3)
+                    base = a.capP - 1u - e;
+                else if (cat == 4)
+                    a.leaf[e] = off;
+                else if (cat == 5)
+                    a.leaf[a.capL - 1u - e] = off;
+                s_base[slot] = base;
+            }
+            __syncthreads();
+        } else {
+            if (t == 0) {
+                uint32_t base = UINT_MAX;
+                if (valid) {
+                    if (!DEFER || mn >= 0)
+                        base = decide(a, off, lo, hi);
+                    else if (hi >= 0 && (lo != hi || lo <= (int)a.dcap))
+                        base = decide(a, off, -1, a.maxdwell); // surely non-uniform; long pixels: hot
+                    else
+                        a.unc[atomicAdd(&a.hdr->n_unc[a.level], 1u)] = off;
+                }
+                s_base[slot] = base;
+            }
+            if (WPR > 1)
+                __syncthreads();
+            else
+                __syncwarp();
+        }
         const uint32_t base = s_base[slot];
         if (base != UINT_MAX)
             for (int c = t; c < rr; c += TPR)
                 a.olt_out[(size_t)base * rr + c] = pack_xy(x0 + (c % a.r) * s, y0 + (c / a.r) * s);
-        if (WPR > 1)
+        if (WPR > 1 || !DEFER)
             __syncthreads();
         else
             __syncwarp();
