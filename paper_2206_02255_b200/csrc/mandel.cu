@@ -556,6 +556,15 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
                 CK(cudaEventRecord(fork, s));
                 CK(cudaStreamWaitEvent(sf, fork, 0));
             }
+            // An overlapped fill runs beside the level kernels; it only needs enough warps to
+            // keep HBM busy (its 128-bit stores never stall a thread), so its grid is capped at
+            // MANDEL_FILL_BPS blocks per SM (0: fully resident) to leave the SMs' warp slots to
+            // the critical path.
+#ifndef MANDEL_FILL_BPS
+#define MANDEL_FILL_BPS 0
+#endif
+            if (overlap && MANDEL_FILL_BPS > 0 && blocks > (size_t)MANDEL_FILL_BPS * sms)
+                blocks = (size_t)MANDEL_FILL_BPS * sms;
             TBEGIN(sf);
             if (vec) {
                 int gsz = resident_grid(k_fill<true>, 256, sms, blocks);
