@@ -386,8 +386,12 @@ def main():
         cb = cpu_oracle_sample(w)
         cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
+    # spread of this rank's per-step device times (mean +- stderr)
+    sd = statistics.stdev(step_ms) if len(step_ms) > 1 else 0.0
     line = {"metric": METRIC, "value": value, "unit": "Mpixel/s", "n_gpus": world, "steps": args.steps,
-            "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
+            "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,
+            "ms_per_step_stderr": sd / math.sqrt(len(step_ms)), "ms_per_step_min": min(step_ms),
+            "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": _config(w, args, world),
             "giter_s_effective": extra.get("giter_s_effective"),
