@@ -140,6 +140,10 @@ enum {
  * C = 16 * (flag bits 16-27), or MANDEL_DEFER_CAP_DEFAULT when those bits are 0; off when
  * C >= maxdwell.                                                                           */
 #define MANDEL_FLAG_DEFER 32u
+/* Like MANDEL_FLAG_TIMING, but events only around the leaf kernel (the dominant one): the
+ * event nodes of MANDEL_FLAG_TIMING sit between every pair of kernels and so cut the
+ * programmatic-dependent-launch edges of the level chain.                 */
+#define MANDEL_FLAG_TIMING_LEAF 128u
 #define MANDEL_FLAG_DEFER_CAP(C) ((((uint32_t)(C) / 16u) & 0xfffu) << 16)
 #define MANDEL_FLAG_DEFER_CAP_MASK (0xfffu << 16)
 #define MANDEL_DEFER_CAP_DEFAULT 256

@@ -98,7 +98,8 @@ def ask(region: Sequence[float], n: int, maxdwell: int, g: int, r: int, B: int, 
         groups: Optional[int] = None, defer=None, stream=None):
     """ASK dwell image over all g*g level-0 regions, or only `tiles`.
     stats: accumulate per-level counters (ask_stats); timing: per-kernel events
-    (kernel_times); flat: B200 scheme with the plain thread-per-pixel border/leaf kernels
+    (kernel_times; "leaf": around the leaf kernel only, which keeps the level chain's
+    programmatic-dependent-launch edges); flat: B200 scheme with the plain thread-per-pixel border/leaf kernels
     instead of the lane-refill ones; serial: fills on the main stream instead of concurrent
     graph branches (A/B comparisons, same image); groups: independent level-synchronous
     chains over round-robin subsets of the tiles, run as parallel graph branches; defer:
@@ -109,7 +110,8 @@ def ask(region: Sequence[float], n: int, maxdwell: int, g: int, r: int, B: int, 
     t_ptr, t_n, _keep = _lib.tiles_arg(tiles)
     rc = _lib.load().mandel_ask_tiles(_lib.region(region), n, maxdwell, g, r, B, t_ptr, t_n,
                                       SCHEMES[scheme],
-                                      (_lib.FLAG_STATS if stats else 0) | (_lib.FLAG_TIMING if timing else 0)
+                                      (_lib.FLAG_STATS if stats else 0)
+                                      | (_lib.FLAG_TIMING_LEAF if timing == "leaf" else _lib.FLAG_TIMING if timing else 0)
                                       | (_lib.FLAG_TILE_COST if tile_cost else 0)
                                       | (_lib.FLAG_FLAT if flat else 0)
                                       | (_lib.FLAG_SERIAL if serial else 0)

@@ -24,6 +24,7 @@ FLAG_TILE_COST = 4
 FLAG_FLAT = 8
 FLAG_SERIAL = 16
 FLAG_DEFER = 32
+FLAG_TIMING_LEAF = 128
 DEFER_CAP_DEFAULT = 256
 
 

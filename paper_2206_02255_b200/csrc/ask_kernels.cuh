@@ -75,6 +75,9 @@ constexpr int DWELL_K = 8;                 // iterations per escape test (dwell.
 #ifndef MANDEL_RF_TPB
 #define MANDEL_RF_TPB 256
 #endif
+#ifndef MANDEL_PDL
+#define MANDEL_PDL 1
+#endif
 constexpr int RF_TPB = MANDEL_RF_TPB;                    // threads per refill block
 constexpr int RF_MINB = MANDEL_RF_MINB * (256 / RF_TPB); // resident blocks per SM (register cap)
 constexpr int RFB_MINB = MANDEL_RFB_PACK ? MANDEL_RF2_MINB * (256 / RF_TPB) : RF_MINB;
@@ -232,6 +235,21 @@ __device__ __forceinline__ void add_tile_cost(const LevelArgs &a, int x, int y, 
         atomicAdd(&a.tile_cost[(y / a.d0) * a.g + x / a.d0], (unsigned long long)v);
 }
 
+// --------------------------------------------------------------------------- PDL
+// Programmatic dependent launch (the level chain's kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization): a kernel lets its
+// successor launch as soon as all of its blocks are running, then waits for its own
+// predecessor's completion (and memory flush) before touching any data, so the successor's
+// launch and block scheduling overlap this kernel's tail.  Both are no-ops for a kernel
+// launched without the attribute.
+__device__ __forceinline__ void pdl_entry()
+{
+#if MANDEL_PDL
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
 // --------------------------------------------------------------------------- helpers
 __device__ __forceinline__ uint32_t level_count(const LevelArgs &a)
 {
@@ -283,6 +301,7 @@ __global__ void __launch_bounds__(BX *BY) k_exhaustive(ExArgs a)
 // canonical order or the caller's tile subset; zero the counters.
 __global__ void k_init(LevelArgs a)
 {
+    pdl_entry();
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     constexpr int hdr_words = sizeof(WsHeader) / 4;
     uint32_t *hw = reinterpret_cast<uint32_t *>(a.hdr);
@@ -585,6 +604,7 @@ __global__ void __launch_bounds__(256) k_b200_border(LevelArgs a)
 template <int WPR, bool DEFER = false, bool UNC = false>
 __global__ void __launch_bounds__(256) k_b200_classify(LevelArgs a)
 {
+    pdl_entry();
     constexpr int TPR = 32 * WPR; // threads per region
     __shared__ int s_lo[8], s_hi[8], s_mn[8];
     __shared__ uint32_t s_base[8 / WPR];
@@ -848,6 +868,7 @@ __device__ __forceinline__ void sink_flush(const StoreSink<STATS, RING> &sk, uns
 template <bool STATS, bool DEFER = false>
 __global__ void __launch_bounds__(RF_TPB, RFB_MINB) k_b200_border_rf(LevelArgs a)
 {
+    pdl_entry();
     static_assert(!(STATS && DEFER), "statistics passes run every pixel to the end");
     __shared__ ParkedPoint s_q[RF_TPB / 32][MANDEL_RFB_PACK ? RF2_QCAP : RF_QCAP];
 #if MANDEL_RFB_PACK && MANDEL_RFB_PRE > 0
@@ -892,6 +913,7 @@ __global__ void __launch_bounds__(RF_TPB, RFB_MINB) k_b200_border_rf(LevelArgs a
 template <bool STATS>
 __global__ void __launch_bounds__(RF_TPB, RFL_MINB) k_b200_leaf_rf(LevelArgs a)
 {
+    pdl_entry();
     __shared__ ParkedPoint s_q[RF_TPB / 32][MANDEL_RFL_PACK ? RF2_QCAP : RF_QCAP];
 #if MANDEL_RFL_PACK && MANDEL_RFL_PRE > 0
     __shared__ SvPoint s_sv[RF_TPB / 32][MANDEL_RFL_CH];

@@ -258,10 +258,30 @@ int resident_grid(K kernel, int tpb, int sms, size_t cap_blocks)
     return (int)(g < 1 ? 1 : g);
 }
 
+// Launch on `s` with programmatic stream serialization (PDL, see pdl_entry()): under stream
+// capture this becomes a programmatic edge to the previous kernel node on `s`.
+template <typename... KArgs>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, cudaStream_t s, LevelArgs a)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = MANDEL_PDL ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, a);
+}
+
 // Per-kernel timing inside the graph (MANDEL_FLAG_TIMING): an external event-record node
 // on the kernel's own stream right before and right after every kernel.
 struct Timing {
     bool on = false;
+    bool leaf_only = false; // MANDEL_FLAG_TIMING_LEAF: events around the leaf kernel only
+    bool next_leaf = false; // set by TBEGIN_LEAF for the next t_begin
     std::vector<cudaEvent_t> evs;        // all events (owned by the cache entry)
     std::vector<int32_t> start, end;     // per kernel: indices into evs
     std::vector<int32_t> kinds;          // per kernel: kind * 100 + level
@@ -270,8 +290,14 @@ struct Timing {
 
 int t_begin(Timing *tm, cudaStream_t st)
 {
-    if (!tm || !tm->on)
+    const bool leaf = tm && tm->next_leaf;
+    if (tm)
+        tm->next_leaf = false;
+    if (!tm || !tm->on || (tm->leaf_only && !leaf)) {
+        if (tm)
+            tm->open = -1;
         return MANDEL_OK;
+    }
     cudaEvent_t ev;
     CK(cudaEventCreate(&ev));
     tm->open = (int32_t)tm->evs.size();
@@ -282,7 +308,7 @@ int t_begin(Timing *tm, cudaStream_t st)
 
 int t_end(Timing *tm, int kind, int level, cudaStream_t st)
 {
-    if (!tm || !tm->on)
+    if (!tm || !tm->on || tm->open < 0)
         return MANDEL_OK;
     cudaEvent_t ev;
     CK(cudaEventCreate(&ev));
@@ -299,6 +325,12 @@ int t_end(Timing *tm, int kind, int level, cudaStream_t st)
         int m_ = t_begin(tm, (st));                                                            \
         if (m_)                                                                                \
             return m_;                                                                         \
+    } while (0)
+#define TBEGIN_LEAF(st)                                                                        \
+    do {                                                                                       \
+        if (tm)                                                                                \
+            tm->next_leaf = true;                                                              \
+        TBEGIN(st);                                                                            \
     } while (0)
 #define TEND(kind, level, st)                                                                  \
     do {                                                                                       \
@@ -495,13 +527,13 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
                 a.fd[3] = fastdiv_nz((uint32_t)(k.r * (d - 2)));
                 if (stats) {
                     int gsz = resident_grid(k_b200_border_rf<true>, RF_TPB, sms, rf_blocks);
-                    k_b200_border_rf<true><<<gsz, RF_TPB, 0, s>>>(a);
+                    CK(launch_pdl(k_b200_border_rf<true>, gsz, RF_TPB, s, a));
                 } else if (defer) {
                     int gsz = resident_grid(k_b200_border_rf<false, true>, RF_TPB, sms, rf_blocks);
                     k_b200_border_rf<false, true><<<gsz, RF_TPB, 0, s>>>(a);
                 } else {
                     int gsz = resident_grid(k_b200_border_rf<false>, RF_TPB, sms, rf_blocks);
-                    k_b200_border_rf<false><<<gsz, RF_TPB, 0, s>>>(a);
+                    CK(launch_pdl(k_b200_border_rf<false>, gsz, RF_TPB, s, a));
                 }
             }
             CK(cudaGetLastError());
@@ -512,13 +544,13 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
                 if (defer)
                     k_b200_classify<8, true><<<gsz, 256, 0, s>>>(a);
                 else
-                    k_b200_classify<8><<<gsz, 256, 0, s>>>(a);
+                    CK(launch_pdl(k_b200_classify<8>, gsz, 256, s, a));
             } else {
                 int gsz = resident_grid(k_b200_classify<1>, 256, sms, (cap + 7) / 8);
                 if (defer)
                     k_b200_classify<1, true><<<gsz, 256, 0, s>>>(a);
                 else
-                    k_b200_classify<1><<<gsz, 256, 0, s>>>(a);
+                    CK(launch_pdl(k_b200_classify<1>, gsz, 256, s, a));
             }
             CK(cudaGetLastError());
             TEND(MANDEL_KIND_B200_CLASSIFY, l, s);
@@ -593,7 +625,7 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
         size_t cap = (size_t)ntiles;
         for (int i = 0; i < lay.L - 1; ++i)
             cap *= (size_t)k.r * k.r;
-        TBEGIN(s);
+        TBEGIN_LEAF(s);
         if (k.scheme == MANDEL_SCHEME_MBR) { // nabla[L]: multiple blocks per leaf, flat
             size_t blocks = (cap * (size_t)(d - 2) * (d - 2) + 255) / 256;
             if (stats) {
@@ -639,10 +671,10 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
                 a.fd[1] = fastdiv_nz((uint32_t)(d - 2));
                 if (stats) {
                     int gsz = resident_grid(k_b200_leaf_rf<true>, RF_TPB, sms, blocks * (256 / RF_TPB));
-                    k_b200_leaf_rf<true><<<gsz, RF_TPB, 0, s>>>(a);
+                    CK(launch_pdl(k_b200_leaf_rf<true>, gsz, RF_TPB, s, a));
                 } else {
                     int gsz = resident_grid(k_b200_leaf_rf<false>, RF_TPB, sms, blocks * (256 / RF_TPB));
-                    k_b200_leaf_rf<false><<<gsz, RF_TPB, 0, s>>>(a);
+                    CK(launch_pdl(k_b200_leaf_rf<false>, gsz, RF_TPB, s, a));
                 }
             }
         }
@@ -756,7 +788,7 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
     if (!valid_grb(n, g, r, B) || !d_ws || (scheme != MANDEL_SCHEME_SBR && scheme != MANDEL_SCHEME_B200 && scheme != MANDEL_SCHEME_MBR &&
                                   scheme != MANDEL_SCHEME_FLOW) ||
         (flags & ~(MANDEL_FLAG_STATS | MANDEL_FLAG_TIMING | MANDEL_FLAG_TILE_COST | MANDEL_FLAG_FLAT |
-                   MANDEL_FLAG_SERIAL | MANDEL_FLAG_GROUPS_MASK | MANDEL_FLAG_DEFER |
+                   MANDEL_FLAG_SERIAL | MANDEL_FLAG_GROUPS_MASK | MANDEL_FLAG_DEFER | MANDEL_FLAG_TIMING_LEAF |
                    MANDEL_FLAG_DEFER_CAP_MASK)) != 0 ||
         MANDEL_FLAG_GROUPS_OF(flags) > MAXG)
         return MANDEL_EINVAL;
@@ -847,7 +879,8 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
             return cuda_fail(ce, "cudaStreamBeginCapture");
         }
         Timing tm;
-        tm.on = (flags & MANDEL_FLAG_TIMING) != 0;
+        tm.on = (flags & (MANDEL_FLAG_TIMING | MANDEL_FLAG_TIMING_LEAF)) != 0;
+        tm.leaf_only = (flags & MANDEL_FLAG_TIMING) == 0;
         int erc = MANDEL_OK;
         if (ngroups == 1) {
             Group grp{lay.hdr, 0, ntiles, d_tiles};
