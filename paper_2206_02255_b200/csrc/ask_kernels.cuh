@@ -31,7 +31,7 @@ constexpr int DWELL_K = 8;                 // iterations per escape test (dwell.
 #define MANDEL_RFB_T 8
 #endif
 #ifndef MANDEL_RFB_CH
-#define MANDEL_RFB_CH 64
+#define MANDEL_RFB_CH 32
 #endif
 #ifndef MANDEL_RFL_K
 #define MANDEL_RFL_K 16
@@ -60,7 +60,7 @@ constexpr int DWELL_K = 8;                 // iterations per escape test (dwell.
 #define MANDEL_RFB2_T 8
 #endif
 #ifndef MANDEL_RFL2_T
-#define MANDEL_RFL2_T 16
+#define MANDEL_RFL2_T 8
 #endif
 #ifndef MANDEL_RF2_MINB
 #define MANDEL_RF2_MINB 3

@@ -82,6 +82,9 @@ constexpr int RF_QCAP = 64; // per-warp queue entries (< 32 left over + < 32 new
 #ifndef MANDEL_RF_MINW
 #define MANDEL_RF_MINW 8u
 #endif
+#ifndef MANDEL_RF_EXACT
+#define MANDEL_RF_EXACT 1
+#endif
 
 // Deferred long pixels.  A border pixel still unescaped after `cap`
 // iterations is parked in the workspace pool with its orbit state and its image (and colT)
@@ -267,9 +270,12 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
         unsigned need = __ballot_sync(FULL, !has);
         while (need && !exhausted) {
             if (pos >= end) {
+                // MANDEL_RF_EXACT: claim no more indices than idle lanes (no index waits in
+                // the warp's window behind a long pixel), at the cost of more cursor atomics
+                const uint32_t gnow = MANDEL_RF_EXACT ? min(grab, (uint32_t)__popc(need)) : grab;
                 unsigned long long b = 0;
                 if (lane == 0)
-                    b = atomicAdd(cursor, (unsigned long long)grab);
+                    b = atomicAdd(cursor, (unsigned long long)gnow);
                 b = __shfl_sync(FULL, b, 0);
                 if (b >= total) {
                     exhausted = true;
@@ -279,7 +285,7 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
                     break;
                 }
                 pos = (uint32_t)b;
-                end = (uint32_t)min(b + (unsigned long long)grab, (unsigned long long)total);
+                end = (uint32_t)min(b + (unsigned long long)gnow, (unsigned long long)total);
             }
             const unsigned cnt = __popc(need);
             const unsigned avail = end - pos;
@@ -711,9 +717,12 @@ __device__ __forceinline__ void refill_loop2(const PixMap &pm, int maxdwell, uin
                 continue;
             }
             if (pos >= end) {
+                // MANDEL_RF_EXACT: claim no more indices than idle lanes (no index waits in
+                // the warp's window behind a long pixel), at the cost of more cursor atomics
+                const uint32_t gnow = MANDEL_RF_EXACT ? min(grab, (uint32_t)(__popc(need0) + __popc(need1))) : grab;
                 unsigned long long b = 0;
                 if (lane == 0)
-                    b = atomicAdd(cursor, (unsigned long long)grab);
+                    b = atomicAdd(cursor, (unsigned long long)gnow);
                 b = __shfl_sync(FULL, b, 0);
                 if (b >= total) {
                     exhausted = true;
@@ -723,7 +732,7 @@ __device__ __forceinline__ void refill_loop2(const PixMap &pm, int maxdwell, uin
                     break;
                 }
                 pos = (uint32_t)b;
-                end = (uint32_t)min(b + (unsigned long long)grab, (unsigned long long)total);
+                end = (uint32_t)min(b + (unsigned long long)gnow, (unsigned long long)total);
             }
             const unsigned c0 = __popc(need0);
             const unsigned cnt = c0 + __popc(need1);
