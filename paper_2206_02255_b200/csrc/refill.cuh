@@ -85,6 +85,9 @@ constexpr int RF_QCAP = 64; // per-warp queue entries (< 32 left over + < 32 new
 #ifndef MANDEL_RF_EXACT
 #define MANDEL_RF_EXACT 1
 #endif
+#ifndef MANDEL_RF_EXACT_PPW
+#define MANDEL_RF_EXACT_PPW 1024u // scalar engine: exact grabs below this many pixels per warp
+#endif
 
 // Deferred long pixels.  A border pixel still unescaped after `cap`
 // iterations is parked in the workspace pool with its orbit state and its image (and colT)
@@ -200,6 +203,10 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
 #endif
     uint32_t grab = total / (4u * active);
     grab = grab < 8u ? 8u : (grab > (uint32_t)CH ? (uint32_t)CH : grab);
+    // exact grabs (below) only for launches with few pixels per warp: there a window of long
+    // pixels held by one warp is the level's tail; in big launches the extra cursor atomics
+    // cost more than the windows (C3's deep border levels)
+    const bool exact = MANDEL_RF_EXACT && total / active < MANDEL_RF_EXACT_PPW;
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
@@ -272,7 +279,7 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
             if (pos >= end) {
                 // MANDEL_RF_EXACT: claim no more indices than idle lanes (no index waits in
                 // the warp's window behind a long pixel), at the cost of more cursor atomics
-                const uint32_t gnow = MANDEL_RF_EXACT ? min(grab, (uint32_t)__popc(need)) : grab;
+                const uint32_t gnow = exact ? min(grab, (uint32_t)__popc(need)) : grab;
                 unsigned long long b = 0;
                 if (lane == 0)
                     b = atomicAdd(cursor, (unsigned long long)gnow);

@@ -16,6 +16,6 @@ import json,sys
 for l in sys.stdin:
     try: d=json.loads(l)
     except Exception: continue
-    print(d['w'], round(d['b200']['ms_notiming_mean'],3), d['b200']['kernels'].get('b200_leaf'))"
+    print(d['w'], round(d['b200']['ms_notiming_mean'],3), {k: round(v, 3) for k, v in d['b200']['kernels'].items()})"
   done
 done
