@@ -836,6 +836,7 @@ template <bool STATS, bool RING>
 struct StoreSink {
     const LevelArgs *a;
     unsigned long long iters, px;
+    unsigned long long *s_tc; // per-block tile costs in shared memory (NULL: global atomics)
     __device__ __forceinline__ void operator()(int x, int y, int v)
     {
         if (RING)
@@ -845,10 +846,35 @@ struct StoreSink {
         if (STATS) {
             iters += (unsigned long long)v;
             px += 1;
-            add_tile_cost(*a, x, y, v);
+            if (s_tc && a->tile_cost)
+                atomicAdd(&s_tc[(y / a->d0) * a->g + x / a->d0], (unsigned long long)v);
+            else
+                add_tile_cost(*a, x, y, v);
         }
     }
 };
+
+// MANDEL_FLAG_TILE_COST in the refill kernels: the preview's per-pixel cost atomics on g^2
+// global counters serialise in L2 (C3's n/8 preview: 1.07 vs 0.65 ms without them), so a
+// block accumulates them in shared memory (g^2 <= TC_SMEM) and flushes once.
+constexpr int TC_SMEM = 1024;
+__device__ __forceinline__ unsigned long long *tc_begin(const LevelArgs &a, unsigned long long *s_tc)
+{
+    const bool use = a.tile_cost && a.g * a.g <= TC_SMEM;
+    if (use)
+        for (int i = threadIdx.x; i < a.g * a.g; i += blockDim.x)
+            s_tc[i] = 0ull;
+    __syncthreads();
+    return use ? s_tc : nullptr;
+}
+__device__ __forceinline__ void tc_flush(const LevelArgs &a, unsigned long long *s_tc)
+{
+    __syncthreads();
+    if (s_tc)
+        for (int i = threadIdx.x; i < a.g * a.g; i += blockDim.x)
+            if (s_tc[i])
+                atomicAdd(&a.tile_cost[i], s_tc[i]);
+}
 
 template <bool STATS, bool RING>
 __device__ __forceinline__ void sink_flush(const StoreSink<STATS, RING> &sk, unsigned long long *it_dst,
@@ -889,7 +915,8 @@ __global__ void __launch_bounds__(RF_TPB, RFB_MINB) k_b200_border_rf(LevelArgs a
     uint32_t count = (a.level == 0) ? (uint32_t)a.ntiles
                                     : *((volatile uint32_t *)&a.hdr->n_subdiv[a.level - 1]);
     const uint32_t total = map.fper.d * count;
-    StoreSink<STATS, true> sink{&a, 0ull, 0ull};
+    __shared__ unsigned long long s_tc[STATS ? TC_SMEM : 1];
+    StoreSink<STATS, true> sink{&a, 0ull, 0ull, STATS ? tc_begin(a, s_tc) : nullptr};
 #if MANDEL_RFB_PACK && MANDEL_RFB_PRE > 0
     refill_loop2<MANDEL_RFB_K, MANDEL_RFB2_T, MANDEL_RFB_CH, BorderMap, StoreSink<STATS, true>, MANDEL_RFB_PRE>(
         a.map, a.maxdwell, total, &a.hdr->cursor[a.level], map, sink, s_q[threadIdx.x >> 5], a.level,
@@ -907,6 +934,8 @@ __global__ void __launch_bounds__(RF_TPB, RFB_MINB) k_b200_border_rf(LevelArgs a
                                                                map, sink, s_q[threadIdx.x >> 5], a.level);
     }
 #endif
+    if (STATS)
+        tc_flush(a, sink.s_tc);
     sink_flush<STATS, true>(sink, &a.hdr->border_iters[a.level], &a.hdr->border_px[a.level]);
 }
 
@@ -925,7 +954,8 @@ __global__ void __launch_bounds__(RF_TPB, RFL_MINB) k_b200_leaf_rf(LevelArgs a)
     map.fI = a.fd[0];
     map.fm = a.fd[1];
     const uint32_t total = map.fI.d * *((volatile uint32_t *)&a.hdr->n_leaf);
-    StoreSink<STATS, false> sink{&a, 0ull, 0ull};
+    __shared__ unsigned long long s_tc[STATS ? TC_SMEM : 1];
+    StoreSink<STATS, false> sink{&a, 0ull, 0ull, STATS ? tc_begin(a, s_tc) : nullptr};
     if (map.fI.d > 0)
 #if MANDEL_RFL_PACK
 #if MANDEL_RFL_PRE > 0
@@ -940,6 +970,8 @@ __global__ void __launch_bounds__(RF_TPB, RFL_MINB) k_b200_leaf_rf(LevelArgs a)
         refill_loop<MANDEL_RFL_K, MANDEL_RFL_T, MANDEL_RFL_CH>(a.map, a.maxdwell, total, &a.hdr->cursor[MAXL], map,
                                                                sink, s_q[threadIdx.x >> 5], 15);
 #endif
+    if (STATS)
+        tc_flush(a, sink.s_tc);
     sink_flush<STATS, false>(sink, &a.hdr->leaf_iters, &a.hdr->leaf_px);
 }
 

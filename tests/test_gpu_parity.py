@@ -402,3 +402,29 @@ def test_defer_full_size_equals_plain(mb, wname):
     assert _decisions(sb) == sa
     assert sum(s["deferred"] for s in sb) > 0
     del a, b
+
+
+# ----------------------------------------------------------------------------- tile costs
+@pytest.mark.parametrize("n,g,r,B,md,region", [
+    (256, 4, 2, 8, 500, W.DEFAULT_REGION),
+    (512, 8, 2, 16, 900, W.SEAHORSE_REGION),
+    (256, 16, 2, 4, 300, W.DEFAULT_REGION),
+])
+def test_tile_costs_match_oracle(mb, n, g, r, B, md, region):
+    """MANDEL_FLAG_TILE_COST (the multi-GPU deal's per-tile cost): for the B200 scheme every
+    pixel is computed once unless it lies strictly inside a filled region, so a tile's executed
+    iterations are the exhaustive dwells of its pixels minus those of its filled regions'
+    interiors (oracle terminal-region records; independent of the GPU path)."""
+    ws = mb.workspace(n, g, r, B)
+    mb.ask(region, n, md, g, r, B, ws=ws, tile_cost=True)
+    got = mb.tile_costs(ws, g)
+    E = oracle.exhaustive(region, n, md).astype(np.int64)
+    _, _, recs = oracle.ask(region, n, md, g, r, B, want_regions=True)
+    inner = np.zeros((n, n), dtype=bool)
+    for x, y, d, kind, _v, _l in recs.tolist():
+        if kind == 0 and d > 2:
+            inner[y + 1:y + d - 1, x + 1:x + d - 1] = True
+    d0 = n // g
+    want = [int(E[gy * d0:(gy + 1) * d0, gx * d0:(gx + 1) * d0][~inner[gy * d0:(gy + 1) * d0, gx * d0:(gx + 1) * d0]].sum())
+            for gy in range(g) for gx in range(g)]
+    assert got == want
