@@ -605,9 +605,13 @@ template <int WPR, bool DEFER = false, bool UNC = false>
 __global__ void __launch_bounds__(256) k_b200_classify(LevelArgs a)
 {
     pdl_entry();
-    constexpr int TPR = 32 * WPR; // threads per region
+    // threads per region: half a warp (WPR = 0: small rings, twice the regions in flight per
+    // warp at the deep levels), a warp, or WPR warps
+    constexpr int TPR = WPR == 0 ? 16 : 32 * WPR;
+    constexpr int RPB = 256 / TPR; // regions per block round
     __shared__ int s_lo[8], s_hi[8], s_mn[8];
-    __shared__ uint32_t s_base[8 / WPR];
+    __shared__ uint32_t s_base[RPB];
+    const unsigned gmask = TPR == 16 ? ((threadIdx.x & 16) ? 0xffff0000u : 0x0000ffffu) : 0xffffffffu;
     const uint32_t count = UNC ? *((volatile uint32_t *)&a.hdr->n_unc[a.level]) : level_count(a);
     const int d = a.d, ring = 4 * d - 4, s = d / a.r, rr = a.r * a.r;
     const int t = threadIdx.x % TPR, w = threadIdx.x >> 5, slot = threadIdx.x / TPR;
@@ -647,10 +651,10 @@ __global__ void __launch_bounds__(256) k_b200_classify(LevelArgs a)
                 }
             }
         }
-        lo = __reduce_min_sync(0xffffffffu, lo);
-        hi = __reduce_max_sync(0xffffffffu, hi);
+        lo = __reduce_min_sync(gmask, lo);
+        hi = __reduce_max_sync(gmask, hi);
         if (DEFER)
-            mn = __reduce_min_sync(0xffffffffu, mn);
+            mn = __reduce_min_sync(gmask, mn);
         if (WPR > 1) {
             if ((threadIdx.x & 31) == 0) {
                 s_lo[w] = lo;
@@ -666,12 +670,12 @@ __global__ void __launch_bounds__(256) k_b200_classify(LevelArgs a)
                 }
             }
         }
-        if (WPR == 1 && !DEFER) {
+        if (WPR <= 1 && !DEFER) {
             // Block-aggregated appends: one atomicAdd per outcome per block of 8 regions
             // instead of two per region (the deep levels hold ~10^5 regions, and per-region
             // atomics on a handful of counters serialise in L2).  Same outcomes and slot
             // addressing as decide(): hot parents / leaves from the front, cold from the back.
-            __shared__ int s_cat[8];
+            __shared__ int s_cat[RPB];
             __shared__ uint32_t s_cb[6];
             if (t == 0) {
                 int cat = 0; // 0 none, 1 fill, 2/3 subdivide hot/cold, 4/5 leaf hot/cold
@@ -684,7 +688,7 @@ __global__ void __launch_bounds__(256) k_b200_classify(LevelArgs a)
             __syncthreads();
             if (threadIdx.x == 0) {
                 uint32_t c[6] = {0u, 0u, 0u, 0u, 0u, 0u};
-                for (int k = 0; k < 8; ++k)
+                for (int k = 0; k < RPB; ++k)
                     ++c[s_cat[k]];
                 s_cb[1] = c[1] ? atomicAdd(&a.hdr->n_fill[a.level], c[1]) : 0u;
                 if (c[2] + c[3])

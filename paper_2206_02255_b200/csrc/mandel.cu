@@ -258,6 +258,11 @@ int resident_grid(K kernel, int tpb, int sms, size_t cap_blocks)
     return (int)(g < 1 ? 1 : g);
 }
 
+// Classification uses half a warp per region for region sides up to this (ring <= 252 pixels).
+#ifndef MANDEL_CLASSIFY_HALF_D
+#define MANDEL_CLASSIFY_HALF_D 64
+#endif
+
 // Launch on `s` with programmatic stream serialization (PDL, see pdl_entry()): under stream
 // capture this becomes a programmatic edge to the previous kernel node on `s`.
 template <typename... KArgs>
@@ -545,6 +550,9 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
                     k_b200_classify<8, true><<<gsz, 256, 0, s>>>(a);
                 else
                     CK(launch_pdl(k_b200_classify<8>, gsz, 256, s, a));
+            } else if (d <= MANDEL_CLASSIFY_HALF_D && !defer) { // half a warp per region
+                int gsz = resident_grid(k_b200_classify<0>, 256, sms, (cap + 15) / 16);
+                CK(launch_pdl(k_b200_classify<0>, gsz, 256, s, a));
             } else {
                 int gsz = resident_grid(k_b200_classify<1>, 256, sms, (cap + 7) / 8);
                 if (defer)
