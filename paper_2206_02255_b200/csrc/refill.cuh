@@ -504,6 +504,9 @@ __device__ __forceinline__ bool rf2_fetch(uint32_t t, const PixMap &pm, int maxd
 #ifndef MANDEL_PRE_WINDOW
 #define MANDEL_PRE_WINDOW 0xffffffffu // prepass pixels per decision window (default: always on)
 #endif
+#ifndef MANDEL_PRE_SLOTS
+#define MANDEL_PRE_SLOTS 0 // prepass raw pixels per free slot (0: a whole grab)
+#endif
 #ifndef MANDEL_PRE_MINFRAC
 #define MANDEL_PRE_MINFRAC 25u // keep the prepass while >= this % of its pixels escape in it
 #endif
@@ -652,16 +655,23 @@ __device__ __forceinline__ void refill_loop2(const PixMap &pm, int maxdwell, uin
         unsigned need0 = __ballot_sync(FULL, !has0), need1 = __ballot_sync(FULL, !has1);
         while ((need0 | need1) && !exhausted) {
             if (PRE > 0 && use_pre && sv_pos >= sv_end) {
-                // prepass a fresh grab; its survivors refill the buffer
+                // prepass a fresh grab; its survivors refill the buffer.  MANDEL_PRE_SLOTS > 0:
+                // at most that many raw pixels per free slot (>= 32), so the survivors -- the
+                // long pixels -- do not queue behind busy slots (the exact grabs of §4.6)
+                uint32_t gpre = grab;
+                if (MANDEL_PRE_SLOTS > 0) {
+                    const uint32_t fr = (uint32_t)(__popc(need0) + __popc(need1)) * MANDEL_PRE_SLOTS;
+                    gpre = min(grab, fr < 32u ? 32u : fr);
+                }
                 unsigned long long b = 0;
                 if (lane == 0)
-                    b = atomicAdd(cursor, (unsigned long long)grab);
+                    b = atomicAdd(cursor, (unsigned long long)gpre);
                 b = __shfl_sync(FULL, b, 0);
                 if (b >= total) {
                     exhausted = true;
                     break;
                 }
-                const uint32_t e = (uint32_t)min(b + (unsigned long long)grab, (unsigned long long)total);
+                const uint32_t e = (uint32_t)min(b + (unsigned long long)gpre, (unsigned long long)total);
                 sv_pos = 0;
                 sv_end = (uint32_t)rf2_prepass<PRE>((uint32_t)b, e, pm, maxdwell, map, sink, sv, pre_esc);
                 pre_tot += e - (uint32_t)b;
