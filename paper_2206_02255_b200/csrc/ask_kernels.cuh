@@ -75,6 +75,9 @@ constexpr int DWELL_K = 8;                 // iterations per escape test (dwell.
 #ifndef MANDEL_RF_TPB
 #define MANDEL_RF_TPB 256
 #endif
+#ifndef MANDEL_HOT_SHIFT // longest-first split: "hot" iff ring max >= maxdwell >> SHIFT
+#define MANDEL_HOT_SHIFT 1
+#endif
 #ifndef MANDEL_PDL
 #define MANDEL_PDL 1
 #endif
@@ -345,7 +348,7 @@ __device__ __forceinline__ uint32_t decide(const LevelArgs &a, uint32_t off, int
             a.fill[e] = make_uint2(off, (uint32_t)lo);
         return UINT_MAX;
     }
-    const bool hot = 2 * hi >= a.maxdwell;
+    const bool hot = ((long long)hi << MANDEL_HOT_SHIFT) >= a.maxdwell;
     if (a.subdivide) {
         atomicAdd(&a.hdr->n_subdiv[a.level], 1u);
         if (hot)
@@ -680,7 +683,7 @@ __global__ void __launch_bounds__(256) k_b200_classify(LevelArgs a)
             if (t == 0) {
                 int cat = 0; // 0 none, 1 fill, 2/3 subdivide hot/cold, 4/5 leaf hot/cold
                 if (valid) {
-                    const bool hot = 2 * hi >= a.maxdwell;
+                    const bool hot = ((long long)hi << MANDEL_HOT_SHIFT) >= a.maxdwell;
                     cat = lo == hi ? 1 : a.subdivide ? (hot ? 2 : 3) : (hot ? 4 : 5);
                 }
                 s_cat[slot] = cat;
