@@ -166,6 +166,9 @@ def _config(w: W.Workload, args, world: int):
                         f"ASK g={w.g} r={w.r} B={w.B}",
             "n": w.n, "maxdwell": w.maxdwell, "g": w.g, "r": w.r, "B": w.B, "region": list(w.region),
             "scheme": args.scheme, "deal": args.deal if world > 1 else "all tiles",
+            "deal_plan": ("per-tile costs from an n/8, maxdwell/2 preview ASK, computed once per view before "
+                          "the timed steps (preview_ms; value_incl_preview charges it to one step)")
+            if world > 1 and args.deal in ("lpt", "costrank") else None,
             "parallelism": f"tiles{world}",
             "l2": "output image 4*n^2 B >> 126 MB L2, rewritten every step; plus a 256 MiB L2 flush "
                   "between timed steps outside the per-step events"}
