@@ -75,6 +75,9 @@ constexpr int DWELL_K = 8;                 // iterations per escape test (dwell.
 #ifndef MANDEL_RF_TPB
 #define MANDEL_RF_TPB 256
 #endif
+#ifndef MANDEL_RFB_SPRE // scalar border engine: short-pixel prepass steps (0: off)
+#define MANDEL_RFB_SPRE 0
+#endif
 #ifndef MANDEL_HOT_SHIFT // longest-first split: "hot" iff ring max >= maxdwell >> SHIFT
 #define MANDEL_HOT_SHIFT 1
 #endif
@@ -937,8 +940,15 @@ __global__ void __launch_bounds__(RF_TPB, RFB_MINB) k_b200_border_rf(LevelArgs a
         refill_loop<MANDEL_RFB_K, MANDEL_RFB_T, MANDEL_RFB_CH, BorderMap, StoreSink<STATS, true>, true>(
             a.map, a.maxdwell, total, &a.hdr->cursor[a.level], map, sink, s_q[threadIdx.x >> 5], a.level, &dc);
     } else {
+#if MANDEL_RFB_SPRE > 0
+        __shared__ SvPoint s_sv[RF_TPB / 32][MANDEL_RFB_CH];
+        refill_loop<MANDEL_RFB_K, MANDEL_RFB_T, MANDEL_RFB_CH, BorderMap, StoreSink<STATS, true>, false,
+                    MANDEL_RFB_SPRE>(a.map, a.maxdwell, total, &a.hdr->cursor[a.level], map, sink,
+                                     s_q[threadIdx.x >> 5], a.level, nullptr, s_sv[threadIdx.x >> 5]);
+#else
         refill_loop<MANDEL_RFB_K, MANDEL_RFB_T, MANDEL_RFB_CH>(a.map, a.maxdwell, total, &a.hdr->cursor[a.level],
                                                                map, sink, s_q[threadIdx.x >> 5], a.level);
+#endif
     }
 #endif
     if (STATS)

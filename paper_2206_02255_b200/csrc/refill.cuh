@@ -169,6 +169,83 @@ __device__ __forceinline__ void replay_batch(const ParkedPoint *q, int cnt, cons
     __syncwarp();
 }
 
+#ifndef MANDEL_PRE_WINDOW
+#define MANDEL_PRE_WINDOW 0xffffffffu // prepass pixels per decision window (default: always on)
+#endif
+#ifndef MANDEL_PRE_SLOTS
+#define MANDEL_PRE_SLOTS 0 // prepass raw pixels per free slot (0: a whole grab)
+#endif
+#ifndef MANDEL_PRE_MINFRAC
+#define MANDEL_PRE_MINFRAC 25u // keep the prepass while >= this % of its pixels escape in it
+#endif
+// A prepass survivor: pixel and its orbit after S steps (x2, y2 are x*x, y*y again).
+struct SvPoint {
+    uint32_t pxy; // x | y << 16
+    float x, y;
+    uint32_t pad;
+};
+
+// Short-pixel prepass (PRE = S > 0, DESIGN.md §4.6): every grab of raw indices is first run
+// warp-synchronously, one pixel per lane, for S steps with an escape test after EVERY step
+// (exact dwell, no replay); pixels that escape -- 70% of the C3 leaf pixels have dwell <= 16
+// -- are stored at once and never enter the refill machinery (fetch, parking, bisection
+// replay: ~20 dispatch cycles per pixel); the survivors go to a per-warp buffer sv (CH
+// entries) and are dealt to slots with their orbit state at iteration S.  The test
+// `!(x2+y2 <= 4)` after step k first fires at the pixel's dwell (escape happens before any
+// overflow), so the stored dwell is the per-step definition's.  A warp stops using the
+// prepass once fewer than a quarter of its first >= 512 prepass pixels escaped in it
+// (boundary-heavy windows such as C5, median leaf dwell 146).
+template <int S, class Map, class Sink>
+__device__ __forceinline__ int rf2_prepass(uint32_t b, uint32_t e, const PixMap &pm, int maxdwell, const Map &map,
+                                           Sink &sink, SvPoint *sv, int &n_esc)
+{
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    int m = 0, esc = 0;
+    for (uint32_t r0 = b; r0 < e; r0 += 32) {
+        const uint32_t t = r0 + (uint32_t)lane;
+        bool surv = false;
+        uint32_t pxy = 0;
+        float x = 0.f, y = 0.f;
+        if (t < e) {
+            int px, py;
+            map(t, px, py);
+            pxy = (uint32_t)px | ((uint32_t)py << 16);
+            const float cr = pix_re(pm, px), ci = pix_im(pm, py);
+            if (__fadd_rn(__fmul_rn(cr, cr), __fmul_rn(ci, ci)) <= 3.9f) {
+                float x2 = 0.f, y2 = 0.f;
+                int dw = 0;
+#pragma unroll
+                for (int k = 1; k <= S; ++k) {
+                    MANDEL_STEP(x, y, x2, y2, cr, ci);
+                    dw = (dw == 0 && !(__fadd_rn(x2, y2) <= 4.0f)) ? k : dw;
+                }
+                if (dw) {
+                    sink(px, py, dw);
+                    ++esc;
+                } else {
+                    surv = true;
+                }
+            } else { // per-step loop (escape permanence not guaranteed)
+                sink(px, py, dwell_per_step<S>(cr, ci, maxdwell));
+                ++esc;
+            }
+        }
+        const unsigned sm = __ballot_sync(FULL, surv);
+        if (surv) {
+            SvPoint &o = sv[m + __popc(sm & lt)];
+            o.pxy = pxy;
+            o.x = x;
+            o.y = y;
+        }
+        m += __popc(sm);
+    }
+    n_esc += __reduce_add_sync(FULL, (unsigned)esc);
+    __syncwarp();
+    return m;
+}
+
 // Map: __device__ void operator()(uint32_t t, int &x, int &y) const      (t < 2^32)
 // Sink: __device__ void operator()(int x, int y, int v)                   (store + stats)
 // q: this warp's RF_QCAP-entry queue in shared memory.
@@ -177,10 +254,13 @@ __device__ __forceinline__ void replay_batch(const ParkedPoint *q, int cnt, cons
 // otherwise leave most warps idle while a few run whole grabs of maxdwell pixels), and >= 8.
 // DEFER: pixels reaching dc->cap iterations unescaped are deferred (DeferRec above) instead
 // of run to the end.  A resuming Map (map_resumes) hands out saved orbits instead of pixels.
-template <int K, int T, int CH, class Map, class Sink, bool DEFER = false>
+// PRE > 0 (raw-pixel maps only): the short-pixel prepass of rf2_prepass on every grab, with
+// the per-warp survivor buffer sv (CH entries); survivors are dealt to lanes at iteration PRE.
+template <int K, int T, int CH, class Map, class Sink, bool DEFER = false, int PRE = 0>
 __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint32_t total,
                                             unsigned long long *cursor, const Map &map, Sink &sink,
-                                            ParkedPoint *q, int tslot = 0, const DeferCtx *dc = nullptr)
+                                            ParkedPoint *q, int tslot = 0, const DeferCtx *dc = nullptr,
+                                            SvPoint *sv = nullptr)
 {
     constexpr bool RESUME = map_resumes<Map>::value;
     // Active warps: a launch with few pixels per lane runs like a thread-per-pixel kernel
@@ -215,6 +295,9 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
     uint32_t pos = 0, end = 0; // warp-uniform chunk window [pos, end)
     bool exhausted = false;    // warp-uniform: the cursor ran past total
     int qn = 0;                // warp-uniform queue fill
+    const bool use_pre = PRE > 0 && !RESUME && sv != nullptr && maxdwell > PRE;
+    uint32_t sv_pos = 0, sv_end = 0; // warp-uniform survivor buffer window
+    int pre_esc = 0;
 
     bool has = false, fin = false;
     bool dfr = false, nod = false; // DEFER: parked for the pool / pool was full (run to the end)
@@ -276,6 +359,47 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
         }
         unsigned need = __ballot_sync(FULL, !has);
         while (need && !exhausted) {
+            if constexpr (PRE > 0 && !RESUME) {
+              if (use_pre) {
+                if (sv_pos >= sv_end) { // prepass a fresh grab; its survivors refill the buffer
+                    unsigned long long b = 0;
+                    if (lane == 0)
+                        b = atomicAdd(cursor, (unsigned long long)grab);
+                    b = __shfl_sync(FULL, b, 0);
+                    if (b >= total) {
+                        exhausted = true;
+                        break;
+                    }
+                    const uint32_t e = (uint32_t)min(b + (unsigned long long)grab, (unsigned long long)total);
+                    sv_pos = 0;
+                    sv_end = (uint32_t)rf2_prepass<PRE>((uint32_t)b, e, pm, maxdwell, map, sink, sv, pre_esc);
+                    continue;
+                }
+                // deal survivors (orbit at iteration PRE) to idle lanes
+                const unsigned cnt = __popc(need);
+                const unsigned avail = sv_end - sv_pos;
+                const unsigned take = avail < cnt ? avail : cnt;
+                const unsigned rank = __popc(need & lt);
+                if (!has && rank < take) {
+                    const SvPoint pnt = sv[sv_pos + rank];
+                    px = (int)(pnt.pxy & 0xffffu);
+                    py = (int)(pnt.pxy >> 16);
+                    cr = pix_re(pm, px);
+                    ci = pix_im(pm, py);
+                    x = pnt.x;
+                    y = pnt.y;
+                    x2 = __fmul_rn(x, x);
+                    y2 = __fmul_rn(y, y);
+                    it = (unsigned)PRE;
+                    nod = false;
+                    has = true;
+                }
+                sv_pos += take;
+                __syncwarp();
+                need = __ballot_sync(FULL, !has);
+                continue;
+              }
+            }
             if (pos >= end) {
                 // MANDEL_RF_EXACT: claim no more indices than idle lanes (no index waits in
                 // the warp's window behind a long pixel), at the cost of more cursor atomics
@@ -499,83 +623,6 @@ __device__ __forceinline__ bool rf2_fetch(uint32_t t, const PixMap &pm, int maxd
         return true;
     sink(px, py, dwell_per_step<K>(cr, ci, maxdwell));
     return false;
-}
-
-#ifndef MANDEL_PRE_WINDOW
-#define MANDEL_PRE_WINDOW 0xffffffffu // prepass pixels per decision window (default: always on)
-#endif
-#ifndef MANDEL_PRE_SLOTS
-#define MANDEL_PRE_SLOTS 0 // prepass raw pixels per free slot (0: a whole grab)
-#endif
-#ifndef MANDEL_PRE_MINFRAC
-#define MANDEL_PRE_MINFRAC 25u // keep the prepass while >= this % of its pixels escape in it
-#endif
-// A prepass survivor: pixel and its orbit after S steps (x2, y2 are x*x, y*y again).
-struct SvPoint {
-    uint32_t pxy; // x | y << 16
-    float x, y;
-    uint32_t pad;
-};
-
-// Short-pixel prepass (PRE = S > 0, DESIGN.md §4.6): every grab of raw indices is first run
-// warp-synchronously, one pixel per lane, for S steps with an escape test after EVERY step
-// (exact dwell, no replay); pixels that escape -- 70% of the C3 leaf pixels have dwell <= 16
-// -- are stored at once and never enter the refill machinery (fetch, parking, bisection
-// replay: ~20 dispatch cycles per pixel); the survivors go to a per-warp buffer sv (CH
-// entries) and are dealt to slots with their orbit state at iteration S.  The test
-// `!(x2+y2 <= 4)` after step k first fires at the pixel's dwell (escape happens before any
-// overflow), so the stored dwell is the per-step definition's.  A warp stops using the
-// prepass once fewer than a quarter of its first >= 512 prepass pixels escaped in it
-// (boundary-heavy windows such as C5, median leaf dwell 146).
-template <int S, class Map, class Sink>
-__device__ __forceinline__ int rf2_prepass(uint32_t b, uint32_t e, const PixMap &pm, int maxdwell, const Map &map,
-                                           Sink &sink, SvPoint *sv, int &n_esc)
-{
-    const unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    const unsigned lt = (1u << lane) - 1u;
-    int m = 0, esc = 0;
-    for (uint32_t r0 = b; r0 < e; r0 += 32) {
-        const uint32_t t = r0 + (uint32_t)lane;
-        bool surv = false;
-        uint32_t pxy = 0;
-        float x = 0.f, y = 0.f;
-        if (t < e) {
-            int px, py;
-            map(t, px, py);
-            pxy = (uint32_t)px | ((uint32_t)py << 16);
-            const float cr = pix_re(pm, px), ci = pix_im(pm, py);
-            if (__fadd_rn(__fmul_rn(cr, cr), __fmul_rn(ci, ci)) <= 3.9f) {
-                float x2 = 0.f, y2 = 0.f;
-                int dw = 0;
-#pragma unroll
-                for (int k = 1; k <= S; ++k) {
-                    MANDEL_STEP(x, y, x2, y2, cr, ci);
-                    dw = (dw == 0 && !(__fadd_rn(x2, y2) <= 4.0f)) ? k : dw;
-                }
-                if (dw) {
-                    sink(px, py, dw);
-                    ++esc;
-                } else {
-                    surv = true;
-                }
-            } else { // per-step loop (escape permanence not guaranteed)
-                sink(px, py, dwell_per_step<S>(cr, ci, maxdwell));
-                ++esc;
-            }
-        }
-        const unsigned sm = __ballot_sync(FULL, surv);
-        if (surv) {
-            SvPoint &o = sv[m + __popc(sm & lt)];
-            o.pxy = pxy;
-            o.x = x;
-            o.y = y;
-        }
-        m += __popc(sm);
-    }
-    n_esc += __reduce_add_sync(FULL, (unsigned)esc);
-    __syncwarp();
-    return m;
 }
 
 // Same contract as refill_loop (Map, Sink, cursor, launch shape); q: RF2_QCAP entries.
