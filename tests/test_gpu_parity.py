@@ -428,3 +428,22 @@ def test_tile_costs_match_oracle(mb, n, g, r, B, md, region):
     want = [int(E[gy * d0:(gy + 1) * d0, gx * d0:(gx + 1) * d0][~inner[gy * d0:(gy + 1) * d0, gx * d0:(gx + 1) * d0]].sum())
             for gy in range(g) for gx in range(g)]
     assert got == want
+
+
+def test_timing_modes(mb):
+    """bench.py's timed steps use MANDEL_FLAG_TIMING_LEAF: events around the leaf kernel only
+    (the level chain keeps its programmatic-dependent-launch edges); MANDEL_FLAG_TIMING times
+    every kernel.  Both leave the image unchanged."""
+    w = W.C1
+    ws = mb.workspace(w.n, w.g, w.r, w.B)
+    A, _ = oracle.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B)
+    out = mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, ws=ws, timing="leaf")
+    kt = mb.kernel_times()
+    assert [k["kind"] for k in kt] == ["b200_leaf"] and kt[0]["ms"] > 0
+    assert np.array_equal(out.cpu().numpy(), A)
+    out = mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, ws=ws, timing=True)
+    kinds = [k["kind"] for k in mb.kernel_times()]
+    L = mb.levels(w.n, w.g, w.r, w.B)
+    assert kinds.count("b200_border") == L and kinds.count("b200_classify") == L
+    assert kinds.count("fill") == L and kinds.count("b200_leaf") == 1 and kinds[0] == "init"
+    assert np.array_equal(out.cpu().numpy(), A)
