@@ -96,6 +96,12 @@ struct Args {
     // M = 2(r-1), N = r(d-2)); the leaf interior side m = d-2 and m^3
     FastDiv fS, fdd, fd, fring, fa2, fa, fMa, fNM, fM, fm, fI;
     int log_d, log_fill_per, log_fill_row; // fill: d, units per cube, units per row (powers of 2)
+    // x-boundary planes, transposed (the 3-D colT): every voxel with
+    // x mod u in {0, u-1} (u = leaf side; every region's x-faces lie there) is also stored at
+    // colT[((2 (x / u) + (x mod u != 0)) * n + z) * n + y], so classification reads the
+    // surface's x-columns as runs along y instead of one 32-byte sector per voxel
+    int *colT; // NULL: off (u < 8)
+    int log_u;
 };
 
 __device__ __forceinline__ void unomega(const Args &a, uint32_t o, int &x, int &y, int &z)
@@ -112,6 +118,23 @@ __device__ __forceinline__ uint32_t omega(const Args &a, int x, int y, int z)
 __device__ __forceinline__ long long vidx(const Args &a, int x, int y, int z)
 {
     return ((long long)z << (2 * a.logn)) + ((long long)y << a.logn) + x;
+}
+
+__device__ __forceinline__ long long colT_idx(const Args &a, int x, int y, int z)
+{
+    const int m = x & ((1 << a.log_u) - 1);
+    const long long plane = 2 * (x >> a.log_u) + (m != 0);
+    return (((plane << a.logn) + z) << a.logn) + y;
+}
+// A surface voxel's dwell: the volume, plus the transposed x-plane copy when x is on one.
+__device__ __forceinline__ void store_surface(const Args &a, int x, int y, int z, int v)
+{
+    a.out[vidx(a, x, y, z)] = v;
+    if (a.colT) {
+        const int m = x & ((1 << a.log_u) - 1);
+        if (m == 0 || m == (1 << a.log_u) - 1)
+            a.colT[colT_idx(a, x, y, z)] = v;
+    }
 }
 
 __device__ __forceinline__ uint32_t level_count(const Args &a)
@@ -212,7 +235,7 @@ __device__ __forceinline__ int dwell3_per_step(float cr, float ci, float w, int 
     return maxdwell;
 }
 
-template <bool STATS>
+template <bool STATS, bool SURFACE = true>
 struct Sink3 {
     const Args *a;
     unsigned long long iters, px;
@@ -220,7 +243,10 @@ struct Sink3 {
     {
         int x, y, z;
         unomega(*a, o, x, y, z);
-        a->out[vidx(*a, x, y, z)] = v;
+        if (SURFACE)
+            store_surface(*a, x, y, z, v);
+        else
+            a->out[vidx(*a, x, y, z)] = v;
         if (STATS) {
             iters += (unsigned long long)v;
             px += 1;
@@ -470,7 +496,7 @@ __global__ void __launch_bounds__(256) k3_surface(Args a)
         y += y0;
         z += z0;
         const int v = dwell3(vc(a.ax.x0, a.ax.dx, x), vc(a.ax.y0, a.ax.dy, y), vc(a.ax.z0, a.ax.dz, z), a.maxdwell);
-        a.out[vidx(a, x, y, z)] = v;
+        store_surface(a, x, y, z, v);
         if (STATS) {
             it += (unsigned long long)v;
             px += 1;
@@ -503,7 +529,10 @@ __global__ void __launch_bounds__(256) k3_classify(Args a)
         for (uint32_t s = threadIdx.x; s < (uint32_t)S; s += blockDim.x) {
             int x, y, z;
             surface_voxel(a, s, x, y, z);
-            const int v = __ldcg(a.out + vidx(a, x0 + x, y0 + y, z0 + z));
+            // the slices' x-columns (x = 0 or d-1 off the z-faces) from the transposed planes
+            const bool col = a.colT && s >= 2u * a.fdd.d && (x == 0 || x == a.d - 1);
+            const int v = __ldcg(col ? a.colT + colT_idx(a, x0 + x, y0 + y, z0 + z)
+                                     : a.out + vidx(a, x0 + x, y0 + y, z0 + z));
             lo = min(lo, v);
             hi = max(hi, v);
         }
@@ -620,7 +649,7 @@ __global__ void __launch_bounds__(RTPB, RMINB) k3_leaf_rf(Args a)
     __shared__ Park3 s_q[RTPB / 32][64];
     __shared__ unsigned long long s_sum[RTPB / 32];
     LeafMap3 map{a};
-    Sink3<STATS> sink{&a, 0ull, 0ull};
+    Sink3<STATS, false> sink{&a, 0ull, 0ull};
     if (a.fI.d > 0)
         refill3(a, (unsigned long long)a.fI.d * *((volatile uint32_t *)&a.hdr->n_leaf), &a.hdr->cursor[MAXL], map,
                 sink, s_q[threadIdx.x >> 5]);
@@ -709,7 +738,8 @@ size_t a256(size_t v) { return (v + 255) & ~size_t(255); }
 
 struct Layout {
     int L;
-    size_t hdr, olt[2], fill, leaf, total;
+    size_t hdr, olt[2], fill, leaf, colT, colT_bytes, total;
+    int log_u;
     size_t cap[MAXL], fill_off[MAXL];
 };
 
@@ -739,6 +769,13 @@ bool make_layout(int64_t n, int32_t g, int32_t r, int32_t B, Layout &lay)
     o = a256(o + fsum * 8);
     lay.leaf = o;
     o = a256(o + capmax * 4);
+    int64_t u = n / g; // leaf side
+    for (int l = 1; l < lay.L; ++l)
+        u /= r;
+    lay.log_u = lg2(u);
+    lay.colT = o;
+    lay.colT_bytes = u >= 8 ? (size_t)(2 * (n / u)) * (size_t)n * (size_t)n * 4 : 0;
+    o = a256(o + lay.colT_bytes);
     lay.total = o;
     return true;
 }
@@ -842,6 +879,10 @@ int mandel3d_ask(mandel3d_region reg, int64_t n, int32_t maxdwell, int32_t g, in
     a.out = d_out;
     a.hdr = (Hdr *)(ws + lay.hdr);
     a.leaf = (uint32_t *)(ws + lay.leaf);
+    if (lay.colT_bytes) {
+        a.colT = (int *)(ws + lay.colT);
+        a.log_u = lay.log_u;
+    }
     uint32_t *olt[2] = {(uint32_t *)(ws + lay.olt[0]), (uint32_t *)(ws + lay.olt[1])};
     int d = (int)(n / g);
     a.level = 0;

@@ -187,10 +187,13 @@ def test_3d_library_exports_and_validates():
     assert l3.mandel3d_ask_levels(1024, 8, 2, 16) == 4      # 128, 64, 32, 16
     assert l3.mandel3d_ask_levels(2048, 8, 2, 16) == 0      # n > 1024: u32 SFC scalar
     assert l3.mandel3d_ask_levels(64, 4, 3, 4) == 0         # r not a power of two
-    # worst case: 2 OLTs + leaf list of (g r^(L-1))^3 u32 + fill lists (8 B per region)
+    # worst case: 2 OLTs + leaf list of (g r^(L-1))^3 u32 + fill lists (8 B per region),
+    # plus the transposed x-planes (2 n/u planes of n^2 int32, leaf side u = 8 here)
     M = (8 * 2 ** 3) ** 3
+    colT = 2 * (512 // 8) * 512 * 512 * 4
     ws = l3.mandel3d_ask_workspace_bytes(512, 8, 2, 8)
-    assert 3 * 4 * M + 8 * M < ws < 3 * 4 * M + 8 * M * 8 // 7 + 8192
+    assert 3 * 4 * M + 8 * M + colT < ws < 3 * 4 * M + 8 * M * 8 // 7 + colT + 8192
+    assert l3.mandel3d_ask_workspace_bytes(64, 4, 2, 4) < 1 << 20  # leaf side 4: no plane copy
     reg = _lib.Mandel3dRegion(-1.5, 0.5, -1.0, 1.0, -0.5, 0.5)
     bad = _lib.Mandel3dRegion(-1.5, 0.5, -1.0, 1.0, 0.5, -0.5)
     fake = ctypes.c_void_p(256)
