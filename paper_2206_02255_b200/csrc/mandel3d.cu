@@ -392,6 +392,316 @@ __device__ __forceinline__ void refill3(const Args &a, unsigned long long total,
         replay3(a, q, qn, md, sink);
 }
 
+// ---------------------------------------------------------------- packed lane refill (leaves)
+// The 2-D leaf engine (refill.cuh refill_loop2) for voxels: two slots per lane
+// stepped with FFMA2/FADD2 (the opaque -0 product of refill.cuh keeps every operation an
+// RN single op), T counted out of 64 slots, replay in batches of 64, and the short-voxel
+// prepass (PRE steps with a test after every step) on each grab.  Same result per voxel.
+using mandel::f2_t;
+using mandel::f2_pack;
+using mandel::f2_unpack;
+using mandel::f2_add;
+using mandel::f2_sub;
+using mandel::f2_mul;
+constexpr int PK = 16, PT = 8, PCH = 128, PPRE = 16, PMINB = 3;
+
+template <class Sink>
+__device__ __forceinline__ void replay3_2(const Args &a, const Park3 *q, int cnt, unsigned md, Sink &sink)
+{
+    const int lane = threadIdx.x & 31;
+    const bool v0 = lane < cnt, v1 = lane + 32 < cnt;
+    if (v0) {
+        Park3 p0 = q[lane], p1 = p0;
+        if (v1)
+            p1 = q[lane + 32];
+        float cr0, ci0, w0, cr1, ci1, w1;
+        voxel_c(a, p0.o, cr0, ci0, w0);
+        voxel_c(a, p1.o, cr1, ci1, w1);
+        const f2_t CR = f2_pack(cr0, cr1), CI = f2_pack(ci0, ci1);
+        f2_t BX = f2_pack(p0.x, p1.x), BY = f2_pack(p0.y, p1.y);
+        f2_t BX2 = f2_mul(BX, BX), BY2 = f2_mul(BY, BY);
+        unsigned lo0 = p0.it, lo1 = p1.it;
+#pragma unroll
+        for (int h = PK / 2; h >= 1; h /= 2) {
+            f2_t X = BX, Y = BY, X2 = BX2, Y2 = BY2;
+#pragma unroll
+            for (int k = 0; k < h; ++k)
+                MANDEL_STEP2(X, Y, X2, Y2, CR, CI);
+            float m0, m1;
+            f2_unpack(f2_add(X2, Y2), m0, m1);
+            const bool hit0 = !(m0 <= 4.0f) || lo0 + (unsigned)h >= md;
+            const bool hit1 = !(m1 <= 4.0f) || lo1 + (unsigned)h >= md;
+            float a0, a1, b0, b1;
+            f2_unpack(X, a0, a1);
+            f2_unpack(BX, b0, b1);
+            BX = f2_pack(hit0 ? b0 : a0, hit1 ? b1 : a1);
+            f2_unpack(Y, a0, a1);
+            f2_unpack(BY, b0, b1);
+            BY = f2_pack(hit0 ? b0 : a0, hit1 ? b1 : a1);
+            f2_unpack(X2, a0, a1);
+            f2_unpack(BX2, b0, b1);
+            BX2 = f2_pack(hit0 ? b0 : a0, hit1 ? b1 : a1);
+            f2_unpack(Y2, a0, a1);
+            f2_unpack(BY2, b0, b1);
+            BY2 = f2_pack(hit0 ? b0 : a0, hit1 ? b1 : a1);
+            lo0 += hit0 ? 0u : (unsigned)h;
+            lo1 += hit1 ? 0u : (unsigned)h;
+        }
+        sink(p0.o, (int)(lo0 + 1u));
+        if (v1)
+            sink(p1.o, (int)(lo1 + 1u));
+    }
+    __syncwarp();
+}
+
+// Prepass of flat indices [b, e): PPRE steps per voxel with a test after every step; escaped
+// voxels are stored, survivors go to sv (orbit at iteration PPRE).  Returns the survivor count.
+template <class Map, class Sink>
+__device__ __forceinline__ int prepass3(const Args &a, uint32_t b, uint32_t e, const Map &map, Sink &sink, Park3 *sv)
+{
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    int m = 0;
+    for (uint32_t r0 = b; r0 < e; r0 += 32) {
+        const uint32_t t = r0 + (uint32_t)lane;
+        bool surv = false;
+        uint32_t o = 0;
+        float x = 0.f, y = 0.f;
+        if (t < e) {
+            o = map(t);
+            float cr, ci, w;
+            voxel_c(a, o, cr, ci, w);
+            if (__fadd_rn(__fmul_rn(cr, cr), __fmul_rn(ci, ci)) <= 3.9f) {
+                x = w;
+                float x2 = __fmul_rn(w, w), y2 = 0.f;
+                int dw = 0;
+#pragma unroll
+                for (int k = 1; k <= PPRE; ++k) {
+                    MANDEL_STEP(x, y, x2, y2, cr, ci);
+                    dw = (dw == 0 && !(__fadd_rn(x2, y2) <= 4.0f)) ? k : dw;
+                }
+                if (dw)
+                    sink(o, dw);
+                else
+                    surv = true;
+            } else {
+                sink(o, dwell3_per_step(cr, ci, w, a.maxdwell));
+            }
+        }
+        const unsigned sm = __ballot_sync(FULL, surv);
+        if (surv) {
+            Park3 &q = sv[m + __popc(sm & lt)];
+            q.o = o;
+            q.x = x;
+            q.y = y;
+            q.it = (unsigned)PPRE;
+        }
+        m += __popc(sm);
+    }
+    __syncwarp();
+    return m;
+}
+
+template <class Map, class Sink>
+__device__ __forceinline__ void refill3_packed(const Args &a, unsigned long long total64, unsigned long long *cursor,
+                                               const Map &map, Sink &sink, Park3 *q, Park3 *sv)
+{
+    const uint32_t total = (uint32_t)total64; // < n^3 <= 2^30
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t min_active = 8u * (uint32_t)c3_sms;
+    uint32_t active = total / (64u * 8u);
+    active = active < min_active ? min_active : active;
+    active = active > nwarps ? nwarps : active;
+    const uint32_t wrank = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+    if (wrank >= active)
+        return;
+    uint32_t grab = total / (4u * active);
+    grab = grab < 8u ? 8u : (grab > (uint32_t)PCH ? (uint32_t)PCH : grab);
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned md = (unsigned)a.maxdwell;
+    const bool use_pre = a.maxdwell > PPRE;
+    bool exhausted = false;
+    int qn = 0;
+    uint32_t sv_pos = 0, sv_end = 0, pos = 0, end = 0;
+    bool has0 = false, has1 = false, fin0 = false, fin1 = false;
+    uint32_t o0 = 0, o1 = 0;
+    unsigned it0 = 0, it1 = 0, sit0 = 0, sit1 = 0;
+    float sx0 = 0.f, sy0 = 0.f, sx1 = 0.f, sy1 = 0.f;
+    f2_t X = 0, Y = 0, X2 = 0, Y2 = 0, CR = 0, CI = 0;
+    while (true) {
+        const unsigned f0 = __ballot_sync(FULL, fin0), f1 = __ballot_sync(FULL, fin1);
+        if (f0 | f1) {
+            const int n0 = __popc(f0);
+            if (fin0) {
+                Park3 &e = q[qn + __popc(f0 & lt)];
+                e.o = o0;
+                e.x = sx0;
+                e.y = sy0;
+                e.it = sit0;
+                has0 = false;
+                fin0 = false;
+            }
+            if (fin1) {
+                Park3 &e = q[qn + n0 + __popc(f1 & lt)];
+                e.o = o1;
+                e.x = sx1;
+                e.y = sy1;
+                e.it = sit1;
+                has1 = false;
+                fin1 = false;
+            }
+            qn += n0 + __popc(f1);
+            __syncwarp();
+            if (qn >= 64) {
+                qn -= 64;
+                replay3_2(a, q + qn, 64, md, sink);
+            }
+        }
+        unsigned need0 = __ballot_sync(FULL, !has0), need1 = __ballot_sync(FULL, !has1);
+        while ((need0 | need1) && !exhausted) {
+            if (use_pre && sv_pos >= sv_end) { // prepass a fresh grab
+                unsigned long long b = 0;
+                if (lane == 0)
+                    b = atomicAdd(cursor, (unsigned long long)grab);
+                b = __shfl_sync(FULL, b, 0);
+                if (b >= total) {
+                    exhausted = true;
+                    break;
+                }
+                const uint32_t e = (uint32_t)min(b + (unsigned long long)grab, (unsigned long long)total);
+                sv_pos = 0;
+                sv_end = (uint32_t)prepass3(a, (uint32_t)b, e, map, sink, sv);
+                continue;
+            }
+            // slots from the survivor buffer, or (no prepass) straight from the cursor
+            const unsigned c0 = __popc(need0);
+            const unsigned cnt = c0 + __popc(need1);
+            unsigned take;
+            uint32_t base;
+            if (use_pre) {
+                const unsigned avail = sv_end - sv_pos;
+                take = avail < cnt ? avail : cnt;
+                base = sv_pos;
+            } else {
+                if (pos >= end) {
+                    unsigned long long b = 0;
+                    if (lane == 0)
+                        b = atomicAdd(cursor, (unsigned long long)grab);
+                    b = __shfl_sync(FULL, b, 0);
+                    if (b >= total) {
+                        exhausted = true;
+                        break;
+                    }
+                    pos = (uint32_t)b;
+                    end = (uint32_t)min(b + (unsigned long long)grab, (unsigned long long)total);
+                }
+                const unsigned avail = end - pos;
+                take = avail < cnt ? avail : cnt;
+                base = pos;
+            }
+            const unsigned r0 = __popc(need0 & lt), r1 = c0 + __popc(need1 & lt);
+            float cr0, ci0, cr1, ci1, xa0, xa1, ya0, ya1, qa0, qa1, wa0, wa1;
+            f2_unpack(CR, cr0, cr1);
+            f2_unpack(CI, ci0, ci1);
+            f2_unpack(X, xa0, xa1);
+            f2_unpack(Y, ya0, ya1);
+            f2_unpack(X2, qa0, qa1);
+            f2_unpack(Y2, wa0, wa1);
+            bool new0 = false, new1 = false;
+            for (int sl = 0; sl < 2; ++sl) {
+                const bool want = sl == 0 ? (!has0 && r0 < take) : (!has1 && r1 < take);
+                if (!want)
+                    continue;
+                const unsigned rk = sl == 0 ? r0 : r1;
+                uint32_t o;
+                float x, y;
+                unsigned itv;
+                float cr, ci, w;
+                bool ok = true;
+                if (use_pre) {
+                    const Park3 pnt = sv[base + rk];
+                    o = pnt.o;
+                    voxel_c(a, o, cr, ci, w);
+                    x = pnt.x;
+                    y = pnt.y;
+                    itv = pnt.it;
+                } else {
+                    o = map(base + rk);
+                    voxel_c(a, o, cr, ci, w);
+                    x = w;
+                    y = 0.0f;
+                    itv = 0;
+                    if (!(__fadd_rn(__fmul_rn(cr, cr), __fmul_rn(ci, ci)) <= 3.9f)) {
+                        sink(o, dwell3_per_step(cr, ci, w, a.maxdwell));
+                        ok = false;
+                    }
+                }
+                if (!ok)
+                    continue;
+                if (sl == 0) {
+                    o0 = o; cr0 = cr; ci0 = ci; xa0 = x; ya0 = y;
+                    qa0 = __fmul_rn(x, x); wa0 = __fmul_rn(y, y); it0 = itv; has0 = true; new0 = true;
+                } else {
+                    o1 = o; cr1 = cr; ci1 = ci; xa1 = x; ya1 = y;
+                    qa1 = __fmul_rn(x, x); wa1 = __fmul_rn(y, y); it1 = itv; has1 = true; new1 = true;
+                }
+            }
+            if (new0 | new1) {
+                CR = f2_pack(cr0, cr1);
+                CI = f2_pack(ci0, ci1);
+                X = f2_pack(xa0, xa1);
+                Y = f2_pack(ya0, ya1);
+                X2 = f2_pack(qa0, qa1);
+                Y2 = f2_pack(wa0, wa1);
+            }
+            if (use_pre)
+                sv_pos += take;
+            else
+                pos += take;
+            __syncwarp();
+            need0 = __ballot_sync(FULL, !has0);
+            need1 = __ballot_sync(FULL, !has1);
+        }
+        const unsigned a0m = __ballot_sync(FULL, has0), a1m = __ballot_sync(FULL, has1);
+        if (!(a0m | a1m))
+            break;
+        const int thresh = exhausted ? 64 : PT;
+        const bool live0 = has0, live1 = has1;
+        while (true) {
+            float xl, xh, yl, yh;
+            f2_unpack(X, xl, xh);
+            f2_unpack(Y, yl, yh);
+            const bool keep0 = fin0 || !live0, keep1 = fin1 || !live1;
+            sx0 = keep0 ? sx0 : xl;
+            sy0 = keep0 ? sy0 : yl;
+            sit0 = keep0 ? sit0 : it0;
+            sx1 = keep1 ? sx1 : xh;
+            sy1 = keep1 ? sy1 : yh;
+            sit1 = keep1 ? sit1 : it1;
+#pragma unroll
+            for (int k = 0; k < PK; ++k)
+                MANDEL_STEP2(X, Y, X2, Y2, CR, CI);
+            it0 += PK;
+            it1 += PK;
+            float m0, m1;
+            f2_unpack(f2_add(X2, Y2), m0, m1);
+            fin0 = live0 && (fin0 || !(m0 <= 4.0f) || it0 >= md);
+            fin1 = live1 && (fin1 || !(m1 <= 4.0f) || it1 >= md);
+            const unsigned g0 = __ballot_sync(FULL, fin0), g1 = __ballot_sync(FULL, fin1);
+            if ((g0 == a0m && g1 == a1m) || __popc(g0) + __popc(g1) >= thresh)
+                break;
+        }
+    }
+    while (qn > 0) {
+        const int c = qn < 64 ? qn : 64;
+        qn -= c;
+        replay3_2(a, q + qn, c, md, sink);
+    }
+}
+
 // ------------------------------------------------------------------------------ kernels
 __global__ void k3_exhaustive(Axis ax, int n, int maxdwell, int *out)
 {
@@ -643,16 +953,27 @@ __global__ void __launch_bounds__(RTPB, RMINB) k3_surface_rf(Args a)
     }
 }
 
+#ifndef MANDEL3D_LEAF_PACK
+#define MANDEL3D_LEAF_PACK 1 // leaves on the packed FFMA2 engine (0: the scalar refill3)
+#endif
 template <bool STATS>
-__global__ void __launch_bounds__(RTPB, RMINB) k3_leaf_rf(Args a)
+__global__ void __launch_bounds__(RTPB, MANDEL3D_LEAF_PACK ? PMINB : RMINB) k3_leaf_rf(Args a)
 {
-    __shared__ Park3 s_q[RTPB / 32][64];
     __shared__ unsigned long long s_sum[RTPB / 32];
     LeafMap3 map{a};
     Sink3<STATS, false> sink{&a, 0ull, 0ull};
+#if MANDEL3D_LEAF_PACK
+    __shared__ Park3 s_q[RTPB / 32][128];
+    __shared__ Park3 s_sv[RTPB / 32][PCH];
+    if (a.fI.d > 0)
+        refill3_packed(a, (unsigned long long)a.fI.d * *((volatile uint32_t *)&a.hdr->n_leaf), &a.hdr->cursor[MAXL],
+                       map, sink, s_q[threadIdx.x >> 5], s_sv[threadIdx.x >> 5]);
+#else
+    __shared__ Park3 s_q[RTPB / 32][64];
     if (a.fI.d > 0)
         refill3(a, (unsigned long long)a.fI.d * *((volatile uint32_t *)&a.hdr->n_leaf), &a.hdr->cursor[MAXL], map,
                 sink, s_q[threadIdx.x >> 5]);
+#endif
     if (STATS) {
         const unsigned long long it = block_sum<RTPB>(sink.iters, s_sum);
         if (threadIdx.x == 0 && it)

@@ -210,3 +210,6 @@ def test_3d_library_exports_and_validates():
     for f in re.split(r"\n\s*Function : ", sass)[1:]:
         if any(k in f.split("\n", 1)[0] for k in ("k3_surface", "k3_leaf", "k3_exhaustive")):  # incl. _rf
             assert re.search(r"\bFFMA\b", f) is None and "FMUL" in f and "FADD" in f
+            for ins in re.findall(r"FFMA2 ([^;]*);", f):  # packed leaf: products fma(a, b, -0) only
+                addend = ins.split(",")[-1].strip()
+                assert addend.startswith("UR") and not addend.startswith("-"), ins
