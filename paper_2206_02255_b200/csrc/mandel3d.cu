@@ -933,16 +933,26 @@ struct LeafMap3 {
     }
 };
 
+#ifndef MANDEL3D_SURF_PACK
+#define MANDEL3D_SURF_PACK 1 // surfaces on the packed FFMA2 engine (0: the scalar refill3)
+#endif
 template <bool STATS>
-__global__ void __launch_bounds__(RTPB, RMINB) k3_surface_rf(Args a)
+__global__ void __launch_bounds__(RTPB, MANDEL3D_SURF_PACK ? PMINB : RMINB) k3_surface_rf(Args a)
 {
-    __shared__ Park3 s_q[RTPB / 32][64];
     __shared__ unsigned long long s_sum[RTPB / 32];
     const bool reuse = a.level > 0;
     SurfMap map{a, reuse};
     const uint32_t units = reuse ? *((volatile uint32_t *)&a.hdr->n_subdiv[a.level - 1]) : level_count(a);
     Sink3<STATS> sink{&a, 0ull, 0ull};
+#if MANDEL3D_SURF_PACK
+    __shared__ Park3 s_q[RTPB / 32][128];
+    __shared__ Park3 s_sv[RTPB / 32][PCH];
+    refill3_packed(a, (unsigned long long)a.fS.d * units, &a.hdr->cursor[a.level], map, sink, s_q[threadIdx.x >> 5],
+                   s_sv[threadIdx.x >> 5]);
+#else
+    __shared__ Park3 s_q[RTPB / 32][64];
     refill3(a, (unsigned long long)a.fS.d * units, &a.hdr->cursor[a.level], map, sink, s_q[threadIdx.x >> 5]);
+#endif
     if (STATS) {
         const unsigned long long it = block_sum<RTPB>(sink.iters, s_sum);
         if (threadIdx.x == 0 && it)
