@@ -880,6 +880,51 @@ __global__ void __launch_bounds__(256) k3_classify(Args a)
     }
 }
 
+// Warp per region (small cubes: the block-per-region loop above spends most of a round in
+// its two block barriers): the same reduction and decision, 8 regions per block in flight.
+__global__ void __launch_bounds__(256) k3_classify_warp(Args a)
+{
+    const uint32_t count = level_count(a);
+    const long long S = surface_count(a.d);
+    const int rrr = a.r * a.r * a.r, h = a.d / a.r;
+    const int lane = threadIdx.x & 31;
+    const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t ri = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; ri < count; ri += warps) {
+        const uint32_t off = a.olt_in[ri];
+        int x0, y0, z0;
+        unomega(a, off, x0, y0, z0);
+        int lo = INT_MAX, hi = INT_MIN;
+        for (uint32_t s = lane; s < (uint32_t)S; s += 32) {
+            int x, y, z;
+            surface_voxel(a, s, x, y, z);
+            const bool col = a.colT && s >= 2u * a.fdd.d && (x == 0 || x == a.d - 1);
+            const int v = __ldcg(col ? a.colT + colT_idx(a, x0 + x, y0 + y, z0 + z)
+                                     : a.out + vidx(a, x0 + x, y0 + y, z0 + z));
+            lo = min(lo, v);
+            hi = max(hi, v);
+        }
+        lo = __reduce_min_sync(0xffffffffu, lo);
+        hi = __reduce_max_sync(0xffffffffu, hi);
+        uint32_t base = UINT_MAX;
+        if (lane == 0) {
+            if (lo == hi) {
+                const uint32_t e = atomicAdd(&a.hdr->n_fill[a.level], 1u);
+                a.fill[e] = make_uint2(off, (uint32_t)lo);
+            } else if (a.subdivide) {
+                base = atomicAdd(&a.hdr->n_subdiv[a.level], 1u);
+            } else {
+                a.leaf[atomicAdd(&a.hdr->n_leaf, 1u)] = off;
+            }
+        }
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (base != UINT_MAX)
+            for (int c = lane; c < rrr; c += 32) {
+                const int cx = c % a.r, cy = (c / a.r) % a.r, cz = c / (a.r * a.r);
+                a.olt_out[(size_t)base * rrr + c] = omega(a, x0 + cx * h, y0 + cy * h, z0 + cz * h);
+            }
+    }
+}
+
 // Uniform cubes: flat over all voxels of the level's filled regions; int4 stores along x
 // when d % 4 == 0 (rows 16-byte aligned: the volume base is 256-byte aligned and n % 4 == 0).
 template <bool VEC>
@@ -933,6 +978,9 @@ struct LeafMap3 {
     }
 };
 
+#ifndef MANDEL3D_CLASSIFY_WARP_D // warp per region for cube sides up to this
+#define MANDEL3D_CLASSIFY_WARP_D 32
+#endif
 #ifndef MANDEL3D_SURF_PACK
 #define MANDEL3D_SURF_PACK 1 // surfaces on the packed FFMA2 engine (0: the scalar refill3)
 #endif
@@ -1186,6 +1234,23 @@ int mandel3d_ask(mandel3d_region reg, int64_t n, int32_t maxdwell, int32_t g, in
     const bool stats = (flags & MANDEL3D_FLAG_STATS) != 0;
     const bool flat = (flags & MANDEL3D_FLAG_FLAT) != 0;
     cudaStream_t s = (cudaStream_t)stream;
+    // fills (HBM-bound, terminal: no later kernel reads a filled cube's interior) run on a side
+    // stream forked after each level's classification and joined at the end (as the 2-D path)
+    static cudaStream_t side[16] = {};
+    static cudaEvent_t ev_fork[16] = {}, ev_join[16] = {};
+    int cur = 0;
+    CK3(cudaGetDevice(&cur));
+    if (cur >= 16)
+        return 1;
+    if (!side[cur]) {
+        CK3(cudaStreamCreateWithFlags(&side[cur], cudaStreamNonBlocking));
+        CK3(cudaEventCreateWithFlags(&ev_fork[cur], cudaEventDisableTiming));
+        CK3(cudaEventCreateWithFlags(&ev_join[cur], cudaEventDisableTiming));
+    }
+    cudaStream_t sf = side[cur];
+    // the side stream must not run ahead of work the caller queued before this call
+    CK3(cudaEventRecord(ev_fork[cur], s));
+    CK3(cudaStreamWaitEvent(sf, ev_fork[cur], 0));
     {
         static int sms_dev = -1; // c3_sms of the current device (the engine's active-warp floor)
         int dev = 0, sms = 0;
@@ -1259,14 +1324,19 @@ int mandel3d_ask(mandel3d_region reg, int64_t n, int32_t maxdwell, int32_t g, in
         else
             k3_surface_rf<false><<<resident(k3_surface_rf<false>, RTPB, sblocks), RTPB, 0, s>>>(a);
         CK3(cudaGetLastError());
-        k3_classify<<<resident(k3_classify, 256, cap), 256, 0, s>>>(a);
+        if (d <= MANDEL3D_CLASSIFY_WARP_D)
+            k3_classify_warp<<<resident(k3_classify_warp, 256, (cap + 7) / 8), 256, 0, s>>>(a);
+        else
+            k3_classify<<<resident(k3_classify, 256, cap), 256, 0, s>>>(a);
         CK3(cudaGetLastError());
         const bool vec = d % 4 == 0;
         const size_t fblocks = (cap * (size_t)d * d * d / (vec ? 4 : 1) + 255) / 256;
+        CK3(cudaEventRecord(ev_fork[cur], s)); // fork: this level's fill waits for its classify
+        CK3(cudaStreamWaitEvent(sf, ev_fork[cur], 0));
         if (vec)
-            k3_fill<true><<<resident(k3_fill<true>, 256, fblocks), 256, 0, s>>>(a);
+            k3_fill<true><<<resident(k3_fill<true>, 256, fblocks), 256, 0, sf>>>(a);
         else
-            k3_fill<false><<<resident(k3_fill<false>, 256, fblocks), 256, 0, s>>>(a);
+            k3_fill<false><<<resident(k3_fill<false>, 256, fblocks), 256, 0, sf>>>(a);
         CK3(cudaGetLastError());
         if (l + 1 < lay.L)
             d /= r;
@@ -1284,6 +1354,8 @@ int mandel3d_ask(mandel3d_region reg, int64_t n, int32_t maxdwell, int32_t g, in
             k3_leaf_rf<false><<<resident(k3_leaf_rf<false>, RTPB, lblocks), RTPB, 0, s>>>(a);
         CK3(cudaGetLastError());
     }
+    CK3(cudaEventRecord(ev_join[cur], sf)); // join the fills
+    CK3(cudaStreamWaitEvent(s, ev_join[cur], 0));
     return 0;
 }
 
