@@ -79,6 +79,7 @@ int mandel3d_ask(mandel3d_region reg, int64_t n, int32_t maxdwell, int32_t g, in
 int mandel3d_ask_last_stats(const void *d_ws, mandel3d_level_stats *h_out, int32_t max_levels, void *stream);
 
 const char *mandel3d_last_cuda_error(void);
+void mandel3d_shutdown(void); /* frees the per-device fill stream and events; owns no buffers */
 
 #ifdef __cplusplus
 }

@@ -234,6 +234,7 @@ _SIGS3 = [
                                     ctypes.c_int32, ctypes.c_uint32, _P, _P, ctypes.c_size_t, _P]),
     ("mandel3d_ask_last_stats", ctypes.c_int, [_P, ctypes.POINTER(Mandel3dLevelStats), ctypes.c_int32, _P]),
     ("mandel3d_last_cuda_error", ctypes.c_char_p, []),
+    ("mandel3d_shutdown", None, []),
 ]
 EXPORTED3 = [s[0] for s in _SIGS3]
 _lib3: Optional[ctypes.CDLL] = None

@@ -1194,6 +1194,10 @@ int resident(Kern k, int tpb, size_t cap_blocks)
     return (int)(gsz < 1 ? 1 : gsz);
 }
 
+// per device: the fill side stream and its fork/join events (mandel3d_shutdown frees them)
+cudaStream_t g_side[16] = {};
+cudaEvent_t g_fork[16] = {}, g_join[16] = {};
+
 } // namespace m3
 
 using namespace m3;
@@ -1236,8 +1240,8 @@ int mandel3d_ask(mandel3d_region reg, int64_t n, int32_t maxdwell, int32_t g, in
     cudaStream_t s = (cudaStream_t)stream;
     // fills (HBM-bound, terminal: no later kernel reads a filled cube's interior) run on a side
     // stream forked after each level's classification and joined at the end (as the 2-D path)
-    static cudaStream_t side[16] = {};
-    static cudaEvent_t ev_fork[16] = {}, ev_join[16] = {};
+    cudaStream_t *side = g_side;
+    cudaEvent_t *ev_fork = g_fork, *ev_join = g_join;
     int cur = 0;
     CK3(cudaGetDevice(&cur));
     if (cur >= 16)
@@ -1389,5 +1393,23 @@ int mandel3d_ask_last_stats(const void *d_ws, mandel3d_level_stats *h_out, int32
 }
 
 const char *mandel3d_last_cuda_error(void) { return g_err; }
+
+void mandel3d_shutdown(void)
+{
+    int prev = 0;
+    cudaGetDevice(&prev);
+    for (int d = 0; d < 16; ++d) {
+        if (!g_side[d])
+            continue;
+        cudaSetDevice(d);
+        cudaStreamSynchronize(g_side[d]);
+        cudaStreamDestroy(g_side[d]);
+        cudaEventDestroy(g_fork[d]);
+        cudaEventDestroy(g_join[d]);
+        g_side[d] = nullptr;
+        g_fork[d] = g_join[d] = nullptr;
+    }
+    cudaSetDevice(prev);
+}
 
 } // extern "C"

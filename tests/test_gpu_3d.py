@@ -91,3 +91,14 @@ def test_full_size_3d_sampled_tiles(m3, wname):
     ex = m3.exhaustive3d(w.region, w.n, w.maxdwell)
     for z in rng.integers(0, w.n, 2).tolist():
         assert np.array_equal(ex[z, :64].cpu().numpy(), oracle.exhaustive3(w.region, w.n, w.maxdwell, z, 1)[0, :64])
+
+
+def test_shutdown_and_reuse(m3):
+    """mandel3d_shutdown frees the fill stream/events; the next call recreates them."""
+    from paper_2206_02255_b200 import _lib
+    w = list(W.random_small_workloads3(1, seed=W.SEED + 64, max_n=32))[0]
+    a = m3.ask3d(w.region, w.n, w.maxdwell, w.g, w.r, w.B).cpu().numpy()
+    _lib.load_3d().mandel3d_shutdown()
+    b = m3.ask3d(w.region, w.n, w.maxdwell, w.g, w.r, w.B).cpu().numpy()
+    A, _ = oracle.ask3(w.region, w.n, w.maxdwell, w.g, w.r, w.B)
+    assert np.array_equal(a, A) and np.array_equal(b, A)
