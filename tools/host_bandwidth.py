@@ -1,3 +1,6 @@
+"""Host-side bandwidth on the GPU box (dev tool): pinned-buffer fill and copy GB/s by thread
+count, and the plain 4 GiB D2H copy; decided against expanding ASK fill lists on the host
+for the end-to-end path."""
 import time, torch, os
 print("cpus", len(os.sched_getaffinity(0)))
 n = 32768
