@@ -447,3 +447,21 @@ def test_timing_modes(mb):
     assert kinds.count("b200_border") == L and kinds.count("b200_classify") == L
     assert kinds.count("fill") == L and kinds.count("b200_leaf") == 1 and kinds[0] == "init"
     assert np.array_equal(out.cpu().numpy(), A)
+
+
+@pytest.mark.parametrize("scheme", ["b200", "sbr", "mbr"])
+def test_ask_empty_tile_subset(mb, scheme):
+    """A rank can receive no level-0 tile (more ranks than tiles): an empty subset writes
+    nothing, reports zero regions, and the workspace serves a full call afterwards."""
+    n, g, r, B, md = 128, 2, 2, 8, 300
+    ws = mb.workspace(n, g, r, B)
+    buf = torch.full((n, n), -5, dtype=torch.int32, device="cuda")
+    mb.ask(W.DEFAULT_REGION, n, md, g, r, B, out=buf, ws=ws, tiles=[], scheme=scheme, stats=True)
+    torch.cuda.synchronize()
+    assert int((buf != -5).sum().item()) == 0
+    assert all(s["regions_in"] == 0 and s["filled"] == 0 for s in mb.ask_stats(ws))
+    h = torch.full((n * n,), -5, dtype=torch.int32).pin_memory()
+    mb.ask_to_host(W.DEFAULT_REGION, n, md, g, r, B, h, buf, ws, tiles=[], scheme=scheme)
+    assert int((h != -5).sum().item()) == 0
+    A, _ = oracle.ask(W.DEFAULT_REGION, n, md, g, r, B)
+    assert np.array_equal(mb.ask(W.DEFAULT_REGION, n, md, g, r, B, ws=ws, scheme=scheme).cpu().numpy(), A)
