@@ -465,3 +465,18 @@ def test_ask_empty_tile_subset(mb, scheme):
     assert int((h != -5).sum().item()) == 0
     A, _ = oracle.ask(W.DEFAULT_REGION, n, md, g, r, B)
     assert np.array_equal(mb.ask(W.DEFAULT_REGION, n, md, g, r, B, ws=ws, scheme=scheme).cpu().numpy(), A)
+
+
+@pytest.mark.parametrize("md", [65537, 200003])
+def test_large_maxdwell(mb, md):
+    """maxdwell beyond 2^16 and not a multiple of any chunk: the closed-form interior window is
+    all maxdwell for Ex and every scheme; a boundary window matches the oracle."""
+    n, g, r, B = 32, 2, 2, 4
+    for scheme in ("b200", "sbr", "mbr"):
+        out = mb.ask(W.INTERIOR_REGION, n, md, g, r, B, scheme=scheme).cpu().numpy()
+        assert np.all(out == md), scheme
+    assert np.all(mb.exhaustive(W.INTERIOR_REGION, n, md).cpu().numpy() == md)
+    region = (-0.75, -0.734375, 0.09375, 0.109375)  # seahorse boundary, dyadic
+    A, _ = oracle.ask(region, 16, md, 2, 2, 4)
+    assert np.array_equal(mb.ask(region, 16, md, 2, 2, 4).cpu().numpy(), A)
+    assert np.array_equal(mb.exhaustive(region, 16, md).cpu().numpy(), oracle.exhaustive(region, 16, md))
