@@ -25,7 +25,7 @@ constexpr int DWELL_K = 8;                 // iterations per escape test (dwell.
 // grabs per cursor atomic; separately for the border (short, level-synchronous launches:
 // smaller grabs balance better) and leaf kernels.
 #ifndef MANDEL_RFB_K
-#define MANDEL_RFB_K 16
+#define MANDEL_RFB_K 32
 #endif
 #ifndef MANDEL_RFB_T
 #define MANDEL_RFB_T 8
