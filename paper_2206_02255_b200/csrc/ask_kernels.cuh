@@ -31,7 +31,7 @@ constexpr int DWELL_K = 8;                 // iterations per escape test (dwell.
 #define MANDEL_RFB_T 8
 #endif
 #ifndef MANDEL_RFB_CH
-#define MANDEL_RFB_CH 32
+#define MANDEL_RFB_CH 64
 #endif
 #ifndef MANDEL_RFL_K
 #define MANDEL_RFL_K 16
