@@ -27,9 +27,17 @@
  *     mandel_ask_tiles writes only the pixels of its tiles.  The vectorised fill needs
  *     d_out 16-byte aligned and out_pitch % 4 == 0; other layouts fall back to 4-byte stores.
  *   - d_ws: caller-owned DEVICE workspace of >= mandel_ask_workspace_bytes(...) bytes
- *     (offset lists, fill/leaf lists, counters).  One in-flight call per workspace.
+ *     (device parameter block, offset lists, fill/leaf lists, counters).  One in-flight call
+ *     per workspace.
  *   - The library never allocates device memory.  It caches one captured CUDA graph per
- *     distinct call (key: device, all arguments, pointers); mandel_shutdown() frees them.
+ *     launch shape -- key (device, n, out_pitch, g, r, B, scheme, flags, d_out, d_ws,
+ *     ws_bytes, number of tiles, whether a tile list is given) -- and frees them in
+ *     mandel_shutdown().  The region, maxdwell and the tile ids are NOT part of the key: every
+ *     call first writes them into a parameter block inside d_ws with one stream-ordered
+ *     host->device copy (staged from pageable memory, so the caller's arrays are free on
+ *     return), and the graph's kernels read them there.  One graph therefore serves every
+ *     view, maxdwell and tile list of a launch shape (the ASK state is kept
+ *     device-resident; the paper's host loop reads `count` back after every level).
  *   - Calls are asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream),
  *     except mandel_ask_last_stats, which synchronises it.
  *
@@ -68,9 +76,6 @@ typedef struct {
     int64_t border_iters; /* iterations counted for them (= sum of their dwells)            */
     int64_t leaf_px;      /* leaf interior pixels computed at this level                    */
     int64_t leaf_iters;   /* sum of their dwells                                           */
-    int64_t deferred;     /* MANDEL_FLAG_DEFER: border pixels of this level that reached the
-                             cap unescaped (parked, or computed on when the pool was full)  */
-    int64_t uncertain;    /* MANDEL_FLAG_DEFER: regions whose whole ring was unresolved      */
 } mandel_level_stats;
 
 enum {
@@ -98,17 +103,11 @@ enum {
  *                       PS as in SBR (block per region), terminal work T and leaf work L as
  *                       flat multi-block kernels over all regions of the level (nabla[T],
  *                       nabla[L]), one thread per pixel.  1 + 2L + 1 kernels.
- *   MANDEL_SCHEME_FLOW  the B200 scheme's work (border reuse, lane refill, warp
- *                       classification, fills) as ONE persistent dataflow kernel: a region's
- *                       successors start as soon as its own ring is complete instead of at
- *                       the next level barrier; decisions are region-local,
- *                       so the image is the same.  MANDEL_FLAG_GROUPS is ignored.  3 kernels.
  */
 enum {
     MANDEL_SCHEME_SBR = 0,
     MANDEL_SCHEME_B200 = 1,
-    MANDEL_SCHEME_MBR = 2,
-    MANDEL_SCHEME_FLOW = 3
+    MANDEL_SCHEME_MBR = 2
 };
 
 /* flags */
@@ -129,24 +128,10 @@ enum {
 #define MANDEL_FLAG_GROUPS(G) ((((uint32_t)(G)-1u) & 15u) << 8)
 #define MANDEL_FLAG_GROUPS_MASK (15u << 8)
 #define MANDEL_FLAG_GROUPS_OF(f) ((int)(((f) >> 8) & 15u) + 1)
-/* Deferred long pixels -- experimental, measured slower on B200 than the default scheme
- * (B200 scheme, lane-refill kernels, one group, no STATS/TILE_COST; ignored otherwise;
- * DESIGN.md §4.12).  A border pixel still unescaped after C iterations is
- * parked with its orbit state in a workspace pool and its image slot holds a marker until the
- * dwell is finished; a region is decided from the resolved part of its ring when that
- * suffices (two different values, or a value <= C beside a marker), and only regions whose
- * whole ring is unresolved wait for their markers (2 extra kernels per level).  The other
- * deferred pixels are finished by one kernel before the leaves.  Same decisions, same image.
- * C = 16 * (flag bits 16-27), or MANDEL_DEFER_CAP_DEFAULT when those bits are 0; off when
- * C >= maxdwell.                                                                           */
-#define MANDEL_FLAG_DEFER 32u
 /* Like MANDEL_FLAG_TIMING, but events only around the leaf kernel (the dominant one): the
  * event nodes of MANDEL_FLAG_TIMING sit between every pair of kernels and so cut the
  * programmatic-dependent-launch edges of the level chain.                 */
 #define MANDEL_FLAG_TIMING_LEAF 128u
-#define MANDEL_FLAG_DEFER_CAP(C) ((((uint32_t)(C) / 16u) & 0xfffu) << 16)
-#define MANDEL_FLAG_DEFER_CAP_MASK (0xfffu << 16)
-#define MANDEL_DEFER_CAP_DEFAULT 256
 
 /* Kernel kinds reported by mandel_ask_kernel_times (value = kind * 100 + level). */
 enum {
@@ -157,12 +142,7 @@ enum {
     MANDEL_KIND_B200_LEAF = 4,     /* leaf interiors, flat                                    */
     MANDEL_KIND_SBR_LEVEL = 5,     /* paper SBR/MBR: block-per-region border + decision       */
     MANDEL_KIND_SBR_LEAF = 6,      /* paper SBR: block-per-leaf interior                      */
-    MANDEL_KIND_MBR_LEAF = 7,      /* paper MBR: leaf interiors, flat multi-block             */
-    MANDEL_KIND_FLOW_INIT = 8,     /* flow scheme: level-0 tasks + per-level divisors         */
-    MANDEL_KIND_FLOW = 9,          /* flow scheme: the persistent dataflow kernel             */
-    MANDEL_KIND_B200_RESOLVE = 10, /* MANDEL_FLAG_DEFER: finish the markers on the rings of a
-                                      level's uncertain regions, then re-classify them (2)   */
-    MANDEL_KIND_B200_RESUME = 11   /* MANDEL_FLAG_DEFER: finish every remaining marker       */
+    MANDEL_KIND_MBR_LEAF = 7       /* paper MBR: leaf interiors, flat multi-block             */
 };
 
 /* Bytes of workspace mandel_ask / mandel_ask_tiles need for these parameters (worst case
@@ -175,6 +155,14 @@ int32_t mandel_ask_levels(int64_t n, int32_t g, int32_t r, int32_t B);
 /* Exhaustive dwell image Ex. */
 int mandel_exhaustive(mandel_region reg, int64_t n, int32_t maxdwell, int32_t *d_out,
                       int64_t out_pitch, void *stream);
+
+/* The same exhaustive image from a tuned flat kernel: one thread per pixel as well, but the
+ * escape test runs every 32 iterations instead of 8 (less per-chunk bookkeeping; the exact
+ * first-escape index is still recovered by replaying the last chunk) and 32 x 8 blocks.  It is
+ * the second, fairer speedup denominator SURVEY.md §8(d) asks for beside the plain kernel.
+ * Same arguments, same image. */
+int mandel_exhaustive_tuned(mandel_region reg, int64_t n, int32_t maxdwell, int32_t *d_out,
+                            int64_t out_pitch, void *stream);
 
 /* Full ASK image over all g*g level-0 regions. */
 int mandel_ask(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, int32_t r, int32_t B,
@@ -192,7 +180,7 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
  * and copies the n x n image (rows of n elements) into h_out (host; pinned for full
  * bandwidth), then synchronises `stream`.  For tile runs only the tiles' pixels are
  * meaningful.  h_out is written with row pitch n.  For the whole image (h_tile_ids NULL) the
- * call is pipelined: min(g, 4) bands of level-0 tile rows run as separate tile calls and the
+ * call is pipelined: min(g, 8) bands of level-0 tile rows run as separate tile calls and the
  * copy of each band overlaps the computation of the next (same image: level-0 regions are
  * independent).  One call at a time per device. */
 int mandel_ask_to_host(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, int32_t r,
@@ -218,9 +206,19 @@ int mandel_ask_tile_costs(const void *d_ws, uint64_t *h_costs, int32_t max_tiles
 
 /* Number of kernel launches one mandel_ask_tiles call issues for these parameters. */
 int32_t mandel_ask_kernel_count(int64_t n, int32_t g, int32_t r, int32_t B, int32_t scheme);
-/* Same, for a call with these flags and maxdwell (MANDEL_FLAG_DEFER adds kernels). */
-int32_t mandel_ask_kernel_count_ex(int64_t n, int32_t g, int32_t r, int32_t B, int32_t scheme, uint32_t flags,
-                                   int32_t maxdwell);
+
+/* Number of CUDA graphs captured and instantiated by this process so far (one per new launch
+ * shape, see "Memory and ownership"); lets a caller check that repeated calls with other
+ * regions, maxdwell values or tile lists reuse one graph. */
+long long mandel_ask_graph_captures(void);
+
+/* Measurement helper (not a step of the method): the FP32 issue rate of the dwell step on
+ * this device -- the paper's machine model charges q processors x c lanes, and
+ * bench.py divides the dwell kernels' algorithmic FP32 ops by this measured rate.  Runs the
+ * 7-op step of the dwell core on 2 independent non-escaping orbits per thread, 8 x 256
+ * threads per SM, `steps` x 8 steps each (4 runs, the first a warm-up), synchronously on
+ * `stream`; writes the best rate in T FP32 ops/s (one FADD or FMUL = 1 op) to *tops. */
+int mandel_fp32_peak_probe(int32_t steps, double *tops, void *stream);
 
 const char *mandel_strerror(int code);
 const char *mandel_last_cuda_error(void);

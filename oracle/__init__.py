@@ -14,6 +14,7 @@ Contents:
 from __future__ import annotations
 
 import ctypes
+import hashlib
 import os
 import subprocess
 import threading
@@ -33,13 +34,29 @@ _lock = threading.Lock()
 _lib: Optional[ctypes.CDLL] = None
 
 
+def source_sha() -> str:
+    """SHA-256 of the oracle's C sources and flags: the version key of every cached oracle
+    result (oracle/cache.py) and of the rebuild check below."""
+    h = hashlib.sha256()
+    for p in (_SRC, _SRC3):
+        with open(p, "rb") as f:
+            h.update(f.read())
+    h.update(" ".join(CFLAGS).encode())
+    return h.hexdigest()
+
+
 def build(force: bool = False) -> str:
-    """Compile liboracle.so with contraction off (R4)."""
-    newest = max(os.path.getmtime(_SRC), os.path.getmtime(_SRC3))
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < newest:
+    """Compile liboracle.so with contraction off (R4); rebuilt whenever the source
+    hash recorded beside it differs."""
+    digest = source_sha()
+    stamp = _LIB + ".srchash"
+    fresh = os.path.exists(_LIB) and os.path.exists(stamp) and open(stamp).read().strip() == digest
+    if force or not fresh:
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, _SRC3])
         os.replace(tmp, _LIB)
+        with open(stamp, "w") as f:
+            f.write(digest + "\n")
     return _LIB
 
 

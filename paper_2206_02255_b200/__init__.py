@@ -19,11 +19,9 @@ from typing import List, Optional, Sequence
 
 from . import _lib
 
-SCHEMES = {"sbr": _lib.SCHEME_SBR, "b200": _lib.SCHEME_B200, "mbr": _lib.SCHEME_MBR, "flow": _lib.SCHEME_FLOW}
+SCHEMES = {"sbr": _lib.SCHEME_SBR, "b200": _lib.SCHEME_B200, "mbr": _lib.SCHEME_MBR}
 # Independent ASK chains per call (MANDEL_FLAG_GROUPS); same image for any value.
 DEFAULT_GROUPS = 1
-# Deferred long pixels (MANDEL_FLAG_DEFER); same image either way.
-DEFAULT_DEFER = False
 
 
 def _torch():
@@ -37,6 +35,27 @@ def _stream_ptr(stream) -> int:
     return int(s.cuda_stream)
 
 
+def _check_device(out, *others, stream=None):
+    """The library launches on the CURRENT device (cudaGetDevice): every buffer and the stream
+    must live on out's device; the caller wraps the call in `torch.cuda.device(out.device)`."""
+    for t in others:
+        if t is not None and t.device != out.device:
+            raise ValueError(f"buffer on {t.device} but out is on {out.device}")
+    if stream is not None and stream.device != out.device:
+        raise ValueError(f"stream on {stream.device} but out is on {out.device}")
+
+
+def _temp_workspace(n, g, r, B, out, stream):
+    """A call-local workspace: allocated on out's device, and tied to `stream` (record_stream)
+    when that is not the current stream, so the caching allocator does not hand its memory to
+    another allocation while the graph launched on `stream` still uses it."""
+    torch = _torch()
+    ws = workspace(n, g, r, B, device=out.device)
+    if stream is not None and stream != torch.cuda.current_stream(out.device):
+        ws.record_stream(stream)
+    return ws
+
+
 def levels(n: int, g: int, r: int, B: int) -> int:
     return int(_lib.load().mandel_ask_levels(n, g, r, B))
 
@@ -48,13 +67,15 @@ def workspace_bytes(n: int, g: int, r: int, B: int) -> int:
     return v
 
 
-def kernel_count(n: int, g: int, r: int, B: int, scheme: str = "b200", defer=None, maxdwell: int = 0) -> int:
-    """Kernel launches of one ask() call (defer / maxdwell as passed to ask())."""
-    if not _lib.flag_defer(DEFAULT_DEFER if defer is None else defer):
-        return int(_lib.load().mandel_ask_kernel_count(n, g, r, B, SCHEMES[scheme]))
-    return int(_lib.load().mandel_ask_kernel_count_ex(n, g, r, B, SCHEMES[scheme],
-                                                      _lib.flag_defer(DEFAULT_DEFER if defer is None else defer),
-                                                      max(1, int(maxdwell))))
+def kernel_count(n: int, g: int, r: int, B: int, scheme: str = "b200") -> int:
+    """Kernel launches of one ask() call."""
+    return int(_lib.load().mandel_ask_kernel_count(n, g, r, B, SCHEMES[scheme]))
+
+
+def graph_captures() -> int:
+    """CUDA graphs captured so far by the library (one per launch shape; regions, maxdwell and
+    tile lists are per-call parameters and reuse it)."""
+    return int(_lib.load().mandel_ask_graph_captures())
 
 
 def workspace(n: int, g: int, r: int, B: int, device=None):
@@ -73,12 +94,16 @@ def _image(n: int, out, device=None):
     return out
 
 
-def exhaustive(region: Sequence[float], n: int, maxdwell: int, out=None, stream=None):
-    """Exhaustive dwell image: one thread per pixel."""
+def exhaustive(region: Sequence[float], n: int, maxdwell: int, out=None, stream=None, tuned: bool = False):
+    """Exhaustive dwell image: one thread per pixel.  tuned: the kernel with
+    32-step escape-test chunks (mandel_exhaustive_tuned; same image)."""
     out = _image(n, out)
-    rc = _lib.load().mandel_exhaustive(_lib.region(region), n, maxdwell, out.data_ptr(),
-                                       out.stride(0), _stream_ptr(stream))
-    _lib.check(rc, "mandel_exhaustive")
+    _check_device(out, stream=stream)
+    lib = _lib.load()
+    fn = lib.mandel_exhaustive_tuned if tuned else lib.mandel_exhaustive
+    with _torch().cuda.device(out.device):
+        rc = fn(_lib.region(region), n, maxdwell, out.data_ptr(), out.stride(0), _stream_ptr(stream))
+    _lib.check(rc, "mandel_exhaustive_tuned" if tuned else "mandel_exhaustive")
     return out
 
 
@@ -86,8 +111,10 @@ def dp(region: Sequence[float], n: int, maxdwell: int, g: int, r: int, B: int, o
     """The paper's Dynamic Parallelism baseline (include/mandel_dp.h, libmandel_dp.so):
     recursive Mariani-Silver, one child grid per subdividing node.  Same image as ask()."""
     out = _image(n, out)
-    rc = _lib.load_dp().mandel_dp(_lib.region(region), n, maxdwell, g, r, B, out.data_ptr(), out.stride(0),
-                                  _stream_ptr(stream))
+    _check_device(out, stream=stream)
+    with _torch().cuda.device(out.device):
+        rc = _lib.load_dp().mandel_dp(_lib.region(region), n, maxdwell, g, r, B, out.data_ptr(), out.stride(0),
+                                      _stream_ptr(stream))
     _lib.check_dp(rc, "mandel_dp")
     return out
 
@@ -95,37 +122,38 @@ def dp(region: Sequence[float], n: int, maxdwell: int, g: int, r: int, B: int, o
 def ask(region: Sequence[float], n: int, maxdwell: int, g: int, r: int, B: int, out=None, ws=None,
         tiles: Optional[Sequence[int]] = None, scheme: str = "b200", stats: bool = False,
         timing: bool = False, tile_cost: bool = False, flat: bool = False, serial: bool = False,
-        groups: Optional[int] = None, defer=None, stream=None):
+        groups: Optional[int] = None, stream=None):
     """ASK dwell image over all g*g level-0 regions, or only `tiles`.
     stats: accumulate per-level counters (ask_stats); timing: per-kernel events
     (kernel_times; "leaf": around the leaf kernel only, which keeps the level chain's
-    programmatic-dependent-launch edges); flat: B200 scheme with the plain thread-per-pixel border/leaf kernels
-    instead of the lane-refill ones; serial: fills on the main stream instead of concurrent
-    graph branches (A/B comparisons, same image); groups: independent level-synchronous
-    chains over round-robin subsets of the tiles, run as parallel graph branches; defer:
-    MANDEL_FLAG_DEFER (True: default cap, int: that iteration cap, False: off)."""
+    programmatic-dependent-launch edges); flat: B200 scheme with the plain thread-per-pixel
+    border/leaf kernels instead of the lane-refill ones; serial: fills on the main stream
+    instead of concurrent graph branches (A/B comparisons, same image); groups: independent
+    level-synchronous chains over round-robin subsets of the tiles, run as parallel graph
+    branches."""
     out = _image(n, out)
+    _check_device(out, ws, stream=stream)
     if ws is None:
-        ws = workspace(n, g, r, B, device=out.device)
+        ws = _temp_workspace(n, g, r, B, out, stream)
     t_ptr, t_n, _keep = _lib.tiles_arg(tiles)
-    rc = _lib.load().mandel_ask_tiles(_lib.region(region), n, maxdwell, g, r, B, t_ptr, t_n,
-                                      SCHEMES[scheme],
-                                      (_lib.FLAG_STATS if stats else 0)
-                                      | (_lib.FLAG_TIMING_LEAF if timing == "leaf" else _lib.FLAG_TIMING if timing else 0)
-                                      | (_lib.FLAG_TILE_COST if tile_cost else 0)
-                                      | (_lib.FLAG_FLAT if flat else 0)
-                                      | (_lib.FLAG_SERIAL if serial else 0)
-                                      | _lib.flag_groups(DEFAULT_GROUPS if groups is None else groups)
-                                      | _lib.flag_defer(DEFAULT_DEFER if defer is None else defer),
-                                      out.data_ptr(), out.stride(0), ws.data_ptr(), ws.numel(),
-                                      _stream_ptr(stream))
+    flags = ((_lib.FLAG_STATS if stats else 0)
+             | (_lib.FLAG_TIMING_LEAF if timing == "leaf" else _lib.FLAG_TIMING if timing else 0)
+             | (_lib.FLAG_TILE_COST if tile_cost else 0)
+             | (_lib.FLAG_FLAT if flat else 0)
+             | (_lib.FLAG_SERIAL if serial else 0)
+             | _lib.flag_groups(DEFAULT_GROUPS if groups is None else groups))
+    with _torch().cuda.device(out.device):
+        rc = _lib.load().mandel_ask_tiles(_lib.region(region), n, maxdwell, g, r, B, t_ptr, t_n,
+                                          SCHEMES[scheme], flags, out.data_ptr(), out.stride(0),
+                                          ws.data_ptr(), ws.numel(), _stream_ptr(stream))
     _lib.check(rc, "mandel_ask_tiles")
     return out
 
 
 def ask_stats(ws, stream=None) -> List[dict]:
     """Per-level statistics of the last ASK call on `ws` (synchronises the stream)."""
-    return _lib.stats(ws.data_ptr(), _stream_ptr(stream))
+    with _torch().cuda.device(ws.device):
+        return _lib.stats(ws.data_ptr(), _stream_ptr(stream))
 
 
 def ask_to_host(region, n, maxdwell, g, r, B, h_out, out, ws, tiles=None, scheme="b200", stream=None):
@@ -133,17 +161,20 @@ def ask_to_host(region, n, maxdwell, g, r, B, h_out, out, ws, tiles=None, scheme
     torch = _torch()
     if h_out.dtype != torch.int32 or h_out.is_cuda or not h_out.is_contiguous() or h_out.numel() < n * n:
         raise ValueError("h_out must be a contiguous host int32 tensor of n*n elements")
+    _check_device(out, ws, stream=stream)
     t_ptr, t_n, _keep = _lib.tiles_arg(tiles)
-    rc = _lib.load().mandel_ask_to_host(_lib.region(region), n, maxdwell, g, r, B, t_ptr, t_n,
-                                        SCHEMES[scheme], out.data_ptr(), out.stride(0), ws.data_ptr(),
-                                        ws.numel(), h_out.data_ptr(), _stream_ptr(stream))
+    with torch.cuda.device(out.device):
+        rc = _lib.load().mandel_ask_to_host(_lib.region(region), n, maxdwell, g, r, B, t_ptr, t_n,
+                                            SCHEMES[scheme], out.data_ptr(), out.stride(0), ws.data_ptr(),
+                                            ws.numel(), h_out.data_ptr(), _stream_ptr(stream))
     _lib.check(rc, "mandel_ask_to_host")
     return h_out
 
 
 def tile_costs(ws, g: int, stream=None) -> List[int]:
     """Executed iterations per level-0 tile of the last ask(..., tile_cost=True) on `ws`."""
-    return _lib.tile_costs(ws.data_ptr(), g, _stream_ptr(stream))
+    with _torch().cuda.device(ws.device):
+        return _lib.tile_costs(ws.data_ptr(), g, _stream_ptr(stream))
 
 
 def preview_costs(region, n: int, maxdwell: int, g: int, r: int, B: int, shrink: int = 8,
@@ -161,6 +192,16 @@ def preview_costs(region, n: int, maxdwell: int, g: int, r: int, B: int, shrink:
     ws = workspace(pn, g, r, pB)
     ask(region, pn, pmd, g, r, pB, ws=ws, scheme=scheme, tile_cost=True)
     return tile_costs(ws, g)
+
+
+def fp32_peak_tops(steps: int = 2048, stream=None) -> float:
+    """Measured FP32 rate of the dwell step on the current device, T ops/s (ALU roofline
+    denominator; mandel_fp32_peak_probe)."""
+    import ctypes
+    v = ctypes.c_double(0.0)
+    _lib.check(_lib.load().mandel_fp32_peak_probe(steps, ctypes.byref(v), _stream_ptr(stream)),
+               "mandel_fp32_peak_probe")
+    return float(v.value)
 
 
 def kernel_times() -> List[dict]:

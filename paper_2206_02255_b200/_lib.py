@@ -17,28 +17,13 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("MANDEL_B200_LIB") or os.path.join(HERE, "libmandel_b200.so")
 
 MANDEL_OK, MANDEL_EINVAL, MANDEL_EWORKSPACE, MANDEL_ECUDA = 0, 1, 2, 3
-SCHEME_SBR, SCHEME_B200, SCHEME_MBR, SCHEME_FLOW = 0, 1, 2, 3
+SCHEME_SBR, SCHEME_B200, SCHEME_MBR = 0, 1, 2
 FLAG_STATS = 1
 FLAG_TIMING = 2
 FLAG_TILE_COST = 4
 FLAG_FLAT = 8
 FLAG_SERIAL = 16
-FLAG_DEFER = 32
 FLAG_TIMING_LEAF = 128
-DEFER_CAP_DEFAULT = 256
-
-
-def flag_defer(defer) -> int:
-    """MANDEL_FLAG_DEFER (| MANDEL_FLAG_DEFER_CAP(c)): defer=False/0 off, True the library's
-    default cap, an int > 1 that cap (iterations, rounded to the border chunk)."""
-    if defer is None or defer is False or defer == 0:
-        return 0
-    if defer is True or defer == 1:
-        return FLAG_DEFER
-    c = int(defer)
-    if not 16 <= c <= 16 * 0xfff:
-        raise ValueError("defer cap must be in [16, 65520]")
-    return FLAG_DEFER | (((c // 16) & 0xfff) << 16)
 MAX_GROUPS = 8
 
 
@@ -48,8 +33,7 @@ def flag_groups(g: int) -> int:
         raise ValueError(f"groups must be in [1, {MAX_GROUPS}]")
     return ((int(g) - 1) & 15) << 8
 KIND_NAMES = {0: "init", 1: "b200_border", 2: "b200_classify", 3: "fill", 4: "b200_leaf",
-              5: "sbr_level", 6: "sbr_leaf", 7: "mbr_leaf",
-              8: "flow_init", 9: "flow", 10: "b200_resolve", 11: "b200_resume"}
+              5: "sbr_level", 6: "sbr_leaf", 7: "mbr_leaf"}
 
 _lock = threading.Lock()
 _lib: Optional[ctypes.CDLL] = None
@@ -63,8 +47,7 @@ class MandelRegion(ctypes.Structure):
 class MandelLevelStats(ctypes.Structure):
     _fields_ = [("level", ctypes.c_int32), ("side", ctypes.c_int32)] + [
         (k, ctypes.c_int64) for k in ("regions_in", "filled", "subdivided", "leaves",
-                                       "border_px", "border_iters", "leaf_px", "leaf_iters",
-                                       "deferred", "uncertain")]
+                                       "border_px", "border_iters", "leaf_px", "leaf_iters")]
 
 
 class MandelError(RuntimeError):
@@ -83,6 +66,7 @@ _SIGS = [
     ("mandel_ask_workspace_bytes", ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
     ("mandel_ask_levels", ctypes.c_int32, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
     ("mandel_exhaustive", ctypes.c_int, [MandelRegion, ctypes.c_int64, ctypes.c_int32, _P, ctypes.c_int64, _P]),
+    ("mandel_exhaustive_tuned", ctypes.c_int, [MandelRegion, ctypes.c_int64, ctypes.c_int32, _P, ctypes.c_int64, _P]),
     ("mandel_ask", ctypes.c_int, [MandelRegion, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                   ctypes.c_int32, _P, ctypes.c_int64, _P, ctypes.c_size_t, _P]),
     ("mandel_ask_tiles", ctypes.c_int, [MandelRegion, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
@@ -94,8 +78,8 @@ _SIGS = [
     ("mandel_ask_last_stats", ctypes.c_int, [_P, ctypes.POINTER(MandelLevelStats), ctypes.c_int32, _P]),
     ("mandel_ask_kernel_count", ctypes.c_int32, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                                  ctypes.c_int32]),
-    ("mandel_ask_kernel_count_ex", ctypes.c_int32, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
-                                                    ctypes.c_int32, ctypes.c_uint32, ctypes.c_int32]),
+    ("mandel_ask_graph_captures", ctypes.c_longlong, []),
+    ("mandel_fp32_peak_probe", ctypes.c_int, [ctypes.c_int32, ctypes.POINTER(ctypes.c_double), _P]),
     ("mandel_ask_kernel_times", ctypes.c_int, [_P, _P, ctypes.c_int32]),
     ("mandel_ask_tile_costs", ctypes.c_int, [_P, _P, ctypes.c_int32, _P]),
     ("mandel_strerror", ctypes.c_char_p, [ctypes.c_int]),

@@ -104,16 +104,6 @@ struct WsHeader {
     unsigned long long border_px[MAXL], border_iters[MAXL];
     unsigned long long leaf_px, leaf_iters;
     unsigned long long cursor[MAXL + 1]; // lane-refill work cursors: border level l, leaves
-    // MANDEL_SCHEME_FLOW (flow.cuh): task / unit / fill allocation, publication watermark,
-    // consumer cursor, tasks not yet retired
-    uint32_t f_task_alloc, f_unit_alloc, f_cursor, f_fill_alloc, f_pending, f_exited;
-    // deferred long pixels: pool entries taken; per level, regions whose
-    // whole ring was unresolved ("uncertain"); work cursors of the resolve kernels and of
-    // the final resume kernel
-    uint32_t n_defer;
-    uint32_t n_unc[MAXL];
-    uint32_t n_defer_snap[MAXL]; // n_defer after level l's border kernel (statistics)
-    unsigned long long cursor_res[MAXL + 1];
 };
 static_assert(sizeof(WsHeader) <= 4096, "header");
 
@@ -147,9 +137,24 @@ struct ExArgs {
     int *out;
 };
 
+// Per-call parameters in the workspace: the host writes them with one
+// stream-ordered copy before every graph launch, so one captured graph serves any region,
+// maxdwell and tile list (the OLT state stays device-resident between calls).
+struct DevParams {
+    PixMap map;       // pixel -> c of the call's region (dwell.cuh, R3)
+    int32_t maxdwell; // >= 1
+    int32_t ntiles;   // level-0 tiles of the call (the graph is keyed on it)
+    uint32_t magic;   // PRM_MAGIC
+    uint32_t pad;
+    // followed at byte offset PRM_TILES by the call's tile list (int32, group-dealt order)
+};
+constexpr uint32_t PRM_MAGIC = 0x4d505242u; // "BRPM"
+constexpr size_t PRM_TILES = 256;
+
 struct LevelArgs {
-    PixMap map;
-    int maxdwell;
+    PixMap map;              // filled from *prm at kernel entry (with_params)
+    int maxdwell;            // filled from *prm at kernel entry
+    const DevParams *prm;    // device parameter block of the call
     long long pitch;
     int *out;
     WsHeader *hdr;
@@ -157,7 +162,7 @@ struct LevelArgs {
     uint32_t *olt_out;       // children for the next level
     uint2 *fill;             // this level's fill segment
     uint32_t *leaf;
-    const int32_t *tiles;    // k_init only (device-visible, may be NULL)
+    const int32_t *tiles;    // k_init only: the group's tile list in the parameter block (NULL: canonical)
     int level, d, r, B, g, ntiles, levels, scheme;
     int subdivide;           // d / r >= B
     int log2_q4, log2_row4;  // fill: log2(d*d/4), log2(d/4)
@@ -175,18 +180,6 @@ struct LevelArgs {
     uint32_t capP;           // parent slots of an OLT buffer (= OLT entries / r^2)
     uint32_t capL;           // leaf list entries
     int ngroups;
-    // MANDEL_SCHEME_FLOW (flow.cuh)
-    struct FlowTask *ftask;
-    uint4 *funit;
-    uint2 *ffill;
-    FastDiv *ffd; // 4 per level
-    uint32_t *fmark; // FLOW_CLEAN: the unit array is all zero (survives k_init)
-    int r_log2;
-    // deferred long pixels: pool, iteration cap (0: off), uncertain list
-    DeferRec *pool;
-    uint32_t capD;
-    unsigned dcap;
-    uint32_t *unc;
 };
 
 // Hot/cold list addressing: the q-th subdivided parent of level l-1 (q < hot count: front
@@ -256,6 +249,15 @@ __device__ __forceinline__ void pdl_entry()
 #endif
 }
 
+// The call's region map and maxdwell, read from the device parameter block (written by the
+// stream-ordered copy that precedes the graph launch).
+__device__ __forceinline__ LevelArgs with_params(LevelArgs a)
+{
+    a.map = a.prm->map;
+    a.maxdwell = a.prm->maxdwell;
+    return a;
+}
+
 // --------------------------------------------------------------------------- helpers
 __device__ __forceinline__ uint32_t level_count(const LevelArgs &a)
 {
@@ -290,16 +292,51 @@ __device__ __forceinline__ unsigned long long block_sum_u64(unsigned long long v
 }
 
 // --------------------------------------------------------------------------- Ex
-// Exhaustive approach: one thread per pixel over the n x n grid.
-template <int BX, int BY>
+// Exhaustive approach: one thread per pixel over the n x n grid.  K is the
+// escape-test interval of the dwell core (dwell.cuh): the plain baseline uses the same K = 8
+// as the paper-faithful ASK kernels; the tuned variant (mandel_exhaustive_tuned) tests every
+// 32 steps, so the per-chunk bookkeeping (state save, test, branch) costs ~4% of the issue
+// slots instead of ~13%, at the price of a longer exact replay once per pixel.
+template <int BX, int BY, int K = DWELL_K>
 __global__ void __launch_bounds__(BX *BY) k_exhaustive(ExArgs a)
 {
     const int x = blockIdx.x * BX + threadIdx.x;
     const int y = blockIdx.y * BY + threadIdx.y;
     if (x >= a.n || y >= a.n)
         return;
-    const int v = dwell<DWELL_K>(pix_re(a.map, x), pix_im(a.map, y), a.maxdwell);
+    const int v = dwell<K>(pix_re(a.map, x), pix_im(a.map, y), a.maxdwell);
     a.out[(long long)y * a.pitch + x] = v;
+}
+
+// --------------------------------------------------------------------------- FP32 probe
+// Measured denominator of the ALU roofline (P:280-287 models the machine as q processors of
+// c lanes): the dwell step itself (7 non-fused FP32 ops, dwell.cuh) on CH independent orbits
+// per thread from a non-escaping c (c = -1: period-2 cycle), no escape test, so the only
+// instructions in the loop are the 7 * CH FP32 ops per step.  Ops/s = 7 * CH * steps *
+// threads / time.
+template <int CH>
+__global__ void __launch_bounds__(256) k_probe_fp32(float cr, float ci, int steps, float *sink)
+{
+    float x[CH], y[CH], x2[CH], y2[CH], c[CH];
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+        x[j] = y[j] = x2[j] = y2[j] = 0.0f;
+        c[j] = __fadd_rn(cr, __fmul_rn((float)(threadIdx.x * CH + j), 1e-9f));
+    }
+    for (int i = 0; i < steps; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+#pragma unroll
+            for (int j = 0; j < CH; ++j)
+                MANDEL_STEP(x[j], y[j], x2[j], y2[j], c[j], ci);
+        }
+    }
+    float acc = 0.0f;
+#pragma unroll
+    for (int j = 0; j < CH; ++j)
+        acc = __fadd_rn(acc, __fadd_rn(x[j], y[j]));
+    if (acc == 12345.0f) // never true; keeps the loop alive
+        sink[blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
 
 // --------------------------------------------------------------------------- init
@@ -330,8 +367,6 @@ __global__ void k_init(LevelArgs a)
         const int k = a.tiles ? a.tiles[t] : t;
         const int gx = k % a.g, gy = k / a.g;
         const_cast<uint32_t *>(a.olt_in)[t] = pack_xy(gx * a.d, gy * a.d);
-        if (a.tile_cost) // only this group's tiles (groups run concurrently)
-            a.tile_cost[k] = 0ull;
     }
 }
 
@@ -395,8 +430,9 @@ __device__ __forceinline__ void block_fill_region(const LevelArgs &a, int x0, in
 // then fills a uniform region.  !FILL (ASK-MBR, nabla[(1-P) T]): uniform regions go to the
 // level's fill list for the flat multi-block k_fill.
 template <int TPB, bool STATS, bool FILL = false>
-__global__ void __launch_bounds__(TPB) k_sbr_level(LevelArgs a)
+__global__ void __launch_bounds__(TPB) k_sbr_level(LevelArgs a_)
 {
+    const LevelArgs a = with_params(a_);
     __shared__ int s_lo[TPB / 32], s_hi[TPB / 32];
     __shared__ unsigned long long s_sum[TPB / 32];
     __shared__ uint32_t s_base;
@@ -457,8 +493,9 @@ __global__ void __launch_bounds__(TPB) k_sbr_level(LevelArgs a)
 // Leaf work L, SBR: one block per last-level non-uniform region computes its
 // (d-2)^2 interior pixels (the border is already in the image).
 template <int TPB, bool STATS>
-__global__ void __launch_bounds__(TPB) k_sbr_leaf(LevelArgs a)
+__global__ void __launch_bounds__(TPB) k_sbr_leaf(LevelArgs a_)
 {
+    const LevelArgs a = with_params(a_);
     __shared__ unsigned long long s_sum[TPB / 32];
     const uint32_t count = *((volatile uint32_t *)&a.hdr->n_leaf);
     const int d = a.d, m = d - 2, I = m * m;
@@ -537,8 +574,9 @@ __host__ __device__ __forceinline__ uint32_t new_border_px_per_parent(int D, int
 }
 
 template <bool STATS>
-__global__ void __launch_bounds__(256) k_b200_border(LevelArgs a)
+__global__ void __launch_bounds__(256) k_b200_border(LevelArgs a_)
 {
+    const LevelArgs a = with_params(a_);
     __shared__ unsigned long long s_sum[8];
     unsigned long long total, per;
     const int d = a.d;
@@ -597,40 +635,32 @@ __global__ void __launch_bounds__(256) k_b200_border(LevelArgs a)
 
 // Classification: read each region's 4d-4 ring dwells back (rows from the
 // image, columns from colT), reduce (min, max) with warp reductions, decide, and append
-// (children written by the region's lanes).  WPR warps per region: one warp for small rings;
-// the whole 256-thread block for large ones (d >= 256, i.e. the first levels, where a warp
-// per region would serialise ~d/8 dependent load rounds).
-//
-// DEFER: ring values may be markers (< 0) of deferred pixels, whose dwell is
-// known only to exceed the cap C.  The region is non-uniform as soon as two resolved values
-// differ, or a resolved value <= C sits beside a marker; uniform when every value is resolved
-// and equal; otherwise ("uncertain": every resolved value equal and > C, with markers) it
-// goes to the level's uncertain list, whose markers k_b200_resolve finishes before
-// UNC = true re-classifies those regions from the list.
-template <int WPR, bool DEFER = false, bool UNC = false>
-__global__ void __launch_bounds__(256) k_b200_classify(LevelArgs a)
+// (children written by the region's lanes).  WPR warps per region: half a warp (WPR = 0) or
+// one warp for small rings; the whole 256-thread block for large ones (d >= 256, i.e. the
+// first levels, where a warp per region would serialise ~d/8 dependent load rounds).
+template <int WPR>
+__global__ void __launch_bounds__(256) k_b200_classify(LevelArgs a_)
 {
     pdl_entry();
+    const LevelArgs a = with_params(a_);
     // threads per region: half a warp (WPR = 0: small rings, twice the regions in flight per
     // warp at the deep levels), a warp, or WPR warps
     constexpr int TPR = WPR == 0 ? 16 : 32 * WPR;
     constexpr int RPB = 256 / TPR; // regions per block round
-    __shared__ int s_lo[8], s_hi[8], s_mn[8];
+    __shared__ int s_lo[8], s_hi[8];
     __shared__ uint32_t s_base[RPB];
     const unsigned gmask = TPR == 16 ? ((threadIdx.x & 16) ? 0xffff0000u : 0x0000ffffu) : 0xffffffffu;
-    const uint32_t count = UNC ? *((volatile uint32_t *)&a.hdr->n_unc[a.level]) : level_count(a);
+    const uint32_t count = level_count(a);
     const int d = a.d, ring = 4 * d - 4, s = d / a.r, rr = a.r * a.r;
     const int t = threadIdx.x % TPR, w = threadIdx.x >> 5, slot = threadIdx.x / TPR;
     const uint32_t per_block = 256 / TPR;
     const uint32_t nh = sub_hot(a);
-    if (DEFER && blockIdx.x == 0 && threadIdx.x == 0)
-        a.hdr->n_defer_snap[a.level] = *((volatile uint32_t *)&a.hdr->n_defer);
     for (uint32_t ri0 = blockIdx.x * per_block; ri0 < count; ri0 += gridDim.x * per_block) {
         const uint32_t ri = ri0 + slot;
         const bool valid = ri < count;
-        const uint32_t off = valid ? (UNC ? a.unc[ri] : region_origin(a, ri, nh)) : 0u;
+        const uint32_t off = valid ? region_origin(a, ri, nh) : 0u;
         const int x0 = unpack_x(off), y0 = unpack_y(off);
-        int lo = INT_MAX, hi = INT_MIN, mn = INT_MAX; // resolved min, max, raw min (markers < 0)
+        int lo = INT_MAX, hi = INT_MIN;
         if (valid) {
             // batches of 8 independent loads in flight per thread (the ring of a level-0
             // region is 8188 pixels: latency, not bandwidth, bounds this loop)
@@ -647,37 +677,29 @@ __global__ void __launch_bounds__(256) k_b200_classify(LevelArgs a)
                 }
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    if (DEFER) {
-                        mn = min(mn, v[j]);
-                        lo = min(lo, v[j] < 0 ? INT_MAX : v[j]);
-                    } else {
-                        lo = min(lo, v[j]);
-                    }
+                    lo = min(lo, v[j]);
                     hi = max(hi, v[j]);
                 }
             }
         }
         lo = __reduce_min_sync(gmask, lo);
         hi = __reduce_max_sync(gmask, hi);
-        if (DEFER)
-            mn = __reduce_min_sync(gmask, mn);
         if (WPR > 1) {
             if ((threadIdx.x & 31) == 0) {
                 s_lo[w] = lo;
                 s_hi[w] = hi;
-                s_mn[w] = mn;
             }
             __syncthreads();
             if (t == 0) {
                 for (int k = 1; k < WPR; ++k) {
                     lo = min(lo, s_lo[k]);
                     hi = max(hi, s_hi[k]);
-                    mn = min(mn, s_mn[k]);
                 }
+                s_base[slot] = valid ? decide(a, off, lo, hi) : UINT_MAX;
             }
-        }
-        if (WPR <= 1 && !DEFER) {
-            // Block-aggregated appends: one atomicAdd per outcome per block of 8 regions
+            __syncthreads();
+        } else {
+            // Block-aggregated appends: one atomicAdd per outcome per block of 8 or 16 regions
             // instead of two per region (the deep levels hold ~10^5 regions, and per-region
             // atomics on a handful of counters serialise in L2).  Same outcomes and slot
             // addressing as decide(): hot parents / leaves from the front, cold from the back.
@@ -727,39 +749,20 @@ __global__ void __launch_bounds__(256) k_b200_classify(LevelArgs a)
                 s_base[slot] = base;
             }
             __syncthreads();
-        } else {
-            if (t == 0) {
-                uint32_t base = UINT_MAX;
-                if (valid) {
-                    if (!DEFER || mn >= 0)
-                        base = decide(a, off, lo, hi);
-                    else if (hi >= 0 && (lo != hi || lo <= (int)a.dcap))
-                        base = decide(a, off, -1, a.maxdwell); // surely non-uniform; long pixels: hot
-                    else
-                        a.unc[atomicAdd(&a.hdr->n_unc[a.level], 1u)] = off;
-                }
-                s_base[slot] = base;
-            }
-            if (WPR > 1)
-                __syncthreads();
-            else
-                __syncwarp();
         }
         const uint32_t base = s_base[slot];
         if (base != UINT_MAX)
             for (int c = t; c < rr; c += TPR)
                 a.olt_out[(size_t)base * rr + c] = pack_xy(x0 + (c % a.r) * s, y0 + (c / a.r) * s);
-        if (WPR > 1 || !DEFER)
-            __syncthreads();
-        else
-            __syncwarp();
+        __syncthreads();
     }
 }
 
 // Leaf interiors, flat: one thread per interior pixel of all leaves (grid-stride).
 template <bool STATS>
-__global__ void __launch_bounds__(256) k_b200_leaf(LevelArgs a)
+__global__ void __launch_bounds__(256) k_b200_leaf(LevelArgs a_)
 {
+    const LevelArgs a = with_params(a_);
     __shared__ unsigned long long s_sum[8];
     const int d = a.d, m = d - 2;
     const unsigned long long I = (unsigned long long)m * m;
@@ -901,11 +904,11 @@ __device__ __forceinline__ void sink_flush(const StoreSink<STATS, RING> &sk, uns
         atomicAdd(px_dst, px);
 }
 
-template <bool STATS, bool DEFER = false>
-__global__ void __launch_bounds__(RF_TPB, RFB_MINB) k_b200_border_rf(LevelArgs a)
+template <bool STATS>
+__global__ void __launch_bounds__(RF_TPB, RFB_MINB) k_b200_border_rf(LevelArgs a_)
 {
     pdl_entry();
-    static_assert(!(STATS && DEFER), "statistics passes run every pixel to the end");
+    const LevelArgs a = with_params(a_);
     __shared__ ParkedPoint s_q[RF_TPB / 32][MANDEL_RFB_PACK ? RF2_QCAP : RF_QCAP];
 #if MANDEL_RFB_PACK && MANDEL_RFB_PRE > 0
     __shared__ SvPoint s_sv[RF_TPB / 32][MANDEL_RFB_CH];
@@ -935,21 +938,15 @@ __global__ void __launch_bounds__(RF_TPB, RFB_MINB) k_b200_border_rf(LevelArgs a
     refill_loop2<MANDEL_RFB_K, MANDEL_RFB2_T, MANDEL_RFB_CH>(a.map, a.maxdwell, total, &a.hdr->cursor[a.level], map,
                                                              sink, s_q[threadIdx.x >> 5], a.level);
 #else
-    if constexpr (DEFER) {
-        const DeferCtx dc{a.pool, a.capD, &a.hdr->n_defer, a.dcap};
-        refill_loop<MANDEL_RFB_K, MANDEL_RFB_T, MANDEL_RFB_CH, BorderMap, StoreSink<STATS, true>, true>(
-            a.map, a.maxdwell, total, &a.hdr->cursor[a.level], map, sink, s_q[threadIdx.x >> 5], a.level, &dc);
-    } else {
 #if MANDEL_RFB_SPRE > 0
-        __shared__ SvPoint s_sv[RF_TPB / 32][MANDEL_RFB_CH];
-        refill_loop<MANDEL_RFB_K, MANDEL_RFB_T, MANDEL_RFB_CH, BorderMap, StoreSink<STATS, true>, false,
-                    MANDEL_RFB_SPRE>(a.map, a.maxdwell, total, &a.hdr->cursor[a.level], map, sink,
-                                     s_q[threadIdx.x >> 5], a.level, nullptr, s_sv[threadIdx.x >> 5]);
+    __shared__ SvPoint s_sv[RF_TPB / 32][MANDEL_RFB_CH];
+    refill_loop<MANDEL_RFB_K, MANDEL_RFB_T, MANDEL_RFB_CH, BorderMap, StoreSink<STATS, true>, MANDEL_RFB_SPRE>(
+        a.map, a.maxdwell, total, &a.hdr->cursor[a.level], map, sink, s_q[threadIdx.x >> 5], a.level,
+        s_sv[threadIdx.x >> 5]);
 #else
-        refill_loop<MANDEL_RFB_K, MANDEL_RFB_T, MANDEL_RFB_CH>(a.map, a.maxdwell, total, &a.hdr->cursor[a.level],
-                                                               map, sink, s_q[threadIdx.x >> 5], a.level);
+    refill_loop<MANDEL_RFB_K, MANDEL_RFB_T, MANDEL_RFB_CH>(a.map, a.maxdwell, total, &a.hdr->cursor[a.level], map,
+                                                           sink, s_q[threadIdx.x >> 5], a.level);
 #endif
-    }
 #endif
     if (STATS)
         tc_flush(a, sink.s_tc);
@@ -957,9 +954,10 @@ __global__ void __launch_bounds__(RF_TPB, RFB_MINB) k_b200_border_rf(LevelArgs a
 }
 
 template <bool STATS>
-__global__ void __launch_bounds__(RF_TPB, RFL_MINB) k_b200_leaf_rf(LevelArgs a)
+__global__ void __launch_bounds__(RF_TPB, RFL_MINB) k_b200_leaf_rf(LevelArgs a_)
 {
     pdl_entry();
+    const LevelArgs a = with_params(a_);
     __shared__ ParkedPoint s_q[RF_TPB / 32][MANDEL_RFL_PACK ? RF2_QCAP : RF_QCAP];
 #if MANDEL_RFL_PACK && MANDEL_RFL_PRE > 0
     __shared__ SvPoint s_sv[RF_TPB / 32][MANDEL_RFL_CH];
@@ -990,74 +988,6 @@ __global__ void __launch_bounds__(RF_TPB, RFL_MINB) k_b200_leaf_rf(LevelArgs a)
     if (STATS)
         tc_flush(a, sink.s_tc);
     sink_flush<STATS, false>(sink, &a.hdr->leaf_iters, &a.hdr->leaf_px);
-}
-
-// ----------------------------------------------------------------------- deferred pixels
-// Markers on the rings of this level's uncertain regions: t = region * (4d-4) + ring pixel.
-// A pixel shared by two listed regions may be resumed twice; both write the same dwell.
-struct ResolveMap {
-    static constexpr bool kResume = true;
-    const uint32_t *unc;
-    const int *out;
-    long long pitch;
-    const DeferRec *pool;
-    int d;
-    FastDiv fring; // 4d-4
-    __device__ __forceinline__ bool state(uint32_t t, int &px, int &py, float &x, float &y, unsigned &it) const
-    {
-        const uint32_t u = fdiv(t, fring), b = t - u * fring.d;
-        const uint32_t off = unc[u];
-        ring_pixel((int)b, d, unpack_x(off), unpack_y(off), px, py);
-        const int v = __ldcg(out + (long long)py * pitch + px);
-        if (v >= 0)
-            return false;
-        const DeferRec e = pool[-1 - v];
-        x = e.x;
-        y = e.y;
-        it = e.it;
-        return true;
-    }
-};
-
-// Every pool entry whose marker is still in the image (not resolved above).
-struct ResumeMap {
-    static constexpr bool kResume = true;
-    const int *out;
-    long long pitch;
-    const DeferRec *pool;
-    __device__ __forceinline__ bool state(uint32_t t, int &px, int &py, float &x, float &y, unsigned &it) const
-    {
-        const DeferRec e = pool[t];
-        px = (int)(e.pxy & 0xffffu);
-        py = (int)(e.pxy >> 16);
-        if (__ldcg(out + (long long)py * pitch + px) != -1 - (int)t)
-            return false;
-        x = e.x;
-        y = e.y;
-        it = e.it;
-        return true;
-    }
-};
-
-__global__ void __launch_bounds__(RF_TPB, RF_MINB) k_b200_resolve(LevelArgs a)
-{
-    __shared__ ParkedPoint s_q[RF_TPB / 32][RF_QCAP];
-    ResolveMap map{a.unc, a.out, a.pitch, a.pool, a.d, a.fd[0]};
-    const uint32_t total = map.fring.d * *((volatile uint32_t *)&a.hdr->n_unc[a.level]);
-    StoreSink<false, true> sink{&a, 0ull, 0ull};
-    refill_loop<MANDEL_RFB_K, MANDEL_RFB_T, MANDEL_RFB_CH>(a.map, a.maxdwell, total, &a.hdr->cursor_res[a.level],
-                                                           map, sink, s_q[threadIdx.x >> 5], -1);
-}
-
-__global__ void __launch_bounds__(RF_TPB, RF_MINB) k_b200_resume(LevelArgs a)
-{
-    __shared__ ParkedPoint s_q[RF_TPB / 32][RF_QCAP];
-    ResumeMap map{a.out, a.pitch, a.pool};
-    const uint32_t nd = *((volatile uint32_t *)&a.hdr->n_defer);
-    const uint32_t total = nd < a.capD ? nd : a.capD;
-    StoreSink<false, false> sink{&a, 0ull, 0ull}; // image only: colT is not read any more
-    refill_loop<MANDEL_RFB_K, MANDEL_RFB_T, MANDEL_RFB_CH>(a.map, a.maxdwell, total, &a.hdr->cursor_res[MAXL], map,
-                                                           sink, s_q[threadIdx.x >> 5], -1);
 }
 
 } // namespace mandel

@@ -9,12 +9,12 @@
 
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <vector>
 
 #include "../../include/mandel.h"
 #include "ask_kernels.cuh"
-#include "flow.cuh"
 
 using namespace mandel;
 
@@ -71,10 +71,7 @@ int levels_of(int64_t n, int32_t g, int32_t r, int32_t B)
 // Workspace layout.  cap_l = g^2 r^(2l) (every region may subdivide).
 struct Layout {
     int L;
-    size_t hdr, tiles, olt[2], fill, leaf, tile_cost, colT, colT_bytes, total;
-    size_t ftask, funit, ffill, ffd, fmark; // MANDEL_SCHEME_FLOW (flow.cuh)
-    size_t pool, unc, capD;                 // MANDEL_FLAG_DEFER: deferred-pixel pool, uncertain list
-    size_t ftask_cap, funit_cap, ffill_cap;
+    size_t hdr, prm, prm_bytes, olt[2], fill, leaf, tile_cost, colT, colT_bytes, total;
     int u_log2; // log2 of the leaf side u = (n/g) / r^(L-1)
     size_t fill_off[MAXL]; // element offset of each level's fill segment
     size_t cap[MAXL];
@@ -102,8 +99,10 @@ bool make_layout(int64_t n, int32_t g, int32_t r, int32_t B, Layout &lay)
     size_t o = 0;
     lay.hdr = o;
     o += (size_t)MAXG * 4096; // one header per group
-    lay.tiles = o;
-    o = align256(o + (size_t)g * g * 4);
+    // device parameter block (DevParams + the call's tile list), written before every launch
+    lay.prm = o;
+    lay.prm_bytes = PRM_TILES + (size_t)g * g * 4;
+    o = align256(o + lay.prm_bytes);
     lay.olt[0] = o;
     o = align256(o + capmax * 4);
     lay.olt[1] = o;
@@ -122,36 +121,6 @@ bool make_layout(int64_t n, int32_t g, int32_t r, int32_t B, Layout &lay)
     lay.colT = o;
     lay.colT_bytes = (u >= 8) ? (size_t)(2 * (n / u)) * (size_t)n * 4 : 0;
     o = align256(o + lay.colT_bytes);
-    // flow scheme: every region yields at most one task (kind 1 or 2) or one fill, plus the
-    // g^2 level-0 ring tasks; pixel units <= n^2/FLOW_U + tasks (each pixel is computed at
-    // most once, each task has at most one partial unit); fill units <= n^2/FLOW_PIECE + fills
-    size_t regions = 0;
-    for (int l = 0; l < lay.L; ++l)
-        regions += lay.cap[l];
-    lay.ftask_cap = regions + (size_t)g * g;
-    lay.ffill_cap = regions;
-    lay.funit_cap = (size_t)n * (size_t)n / FLOW_U + (size_t)n * (size_t)n / FLOW_PIECE + lay.ftask_cap +
-                    lay.ffill_cap;
-    lay.ftask = o;
-    o = align256(o + lay.ftask_cap * sizeof(FlowTask));
-    lay.funit = o;
-    o = align256(o + lay.funit_cap * 16);
-    lay.ffill = o;
-    o = align256(o + lay.ffill_cap * 8);
-    lay.ffd = o;
-    o = align256(o + (size_t)4 * MAXL * sizeof(FastDiv));
-    lay.fmark = o;
-    o = align256(o + 4);
-    // deferred long pixels: n^2/64 entries (C3 defers ~1.5% of n^2 pixels at C = 256; a pixel
-    // that finds the pool full is simply computed to the end), and one uncertain-region list
-    // reused by every level
-    lay.capD = (size_t)n * (size_t)n / 64;
-    if (lay.capD < 65536)
-        lay.capD = 65536;
-    lay.pool = o;
-    o = align256(o + lay.capD * sizeof(DeferRec));
-    lay.unc = o;
-    o = align256(o + capmax * 4);
     lay.total = o;
     return true;
 }
@@ -187,28 +156,31 @@ struct DevInfo {
     cudaEvent_t band[64] = {}, copied = nullptr;
 };
 
+// Graph cache key: everything the captured launches depend on.  The region,
+// maxdwell and the tile ids are NOT in it: they live in the workspace's device parameter
+// block, rewritten before every launch, so one graph serves every view and tile list.
 struct Key {
     int dev;
-    mandel_region reg;
     int64_t n, pitch;
-    int32_t maxdwell, g, r, B, scheme;
+    int32_t g, r, B, scheme;
     uint32_t flags;
     int32_t *out;
     void *ws;
     size_t ws_bytes;
-    std::vector<int32_t> tiles;
+    int32_t ntiles;
+    bool listed; // an explicit tile list (else canonical 0..g*g-1)
     bool operator==(const Key &o) const
     {
-        return dev == o.dev && memcmp(&reg, &o.reg, sizeof reg) == 0 && n == o.n && pitch == o.pitch &&
-               maxdwell == o.maxdwell && g == o.g && r == o.r && B == o.B && scheme == o.scheme &&
-               flags == o.flags && out == o.out && ws == o.ws && ws_bytes == o.ws_bytes && tiles == o.tiles;
+        return dev == o.dev && n == o.n && pitch == o.pitch && g == o.g && r == o.r && B == o.B &&
+               scheme == o.scheme && flags == o.flags && out == o.out && ws == o.ws && ws_bytes == o.ws_bytes &&
+               ntiles == o.ntiles && listed == o.listed;
     }
 };
 
 struct Entry {
     Key key;
     cudaGraphExec_t exec = nullptr;
-    int32_t *h_tiles = nullptr; // pinned, mapped (read by k_init through UVA)
+    int ngroups = 1;
     unsigned long long last_use = 0;
     std::vector<cudaEvent_t> evs; // MANDEL_FLAG_TIMING only
     std::vector<int32_t> kinds, t_start, t_end;
@@ -217,15 +189,18 @@ struct Entry {
 
 std::mutex g_mu;
 std::vector<Entry> g_cache;
-std::vector<DevInfo> g_dev;
+// Per-device state at stable addresses: a DevInfo pointer stays valid when another device's
+// first call grows the table (mandel_ask_to_host keeps one across several calls).
+std::vector<std::unique_ptr<DevInfo>> g_dev;
 unsigned long long g_clock = 0, g_next_id = 0, g_last_timed = 0;
+long long g_captures = 0; // graphs captured so far (mandel_ask_graph_captures)
 constexpr size_t kMaxGraphs = 64;
 
 int dev_info(int dev, DevInfo *&out)
 {
-    if ((int)g_dev.size() <= dev)
-        g_dev.resize(dev + 1);
-    DevInfo &di = g_dev[dev];
+    while ((int)g_dev.size() <= dev)
+        g_dev.emplace_back(new DevInfo());
+    DevInfo &di = *g_dev[dev];
     if (!di.cap) {
         CK(cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev));
         CK(cudaMemcpyToSymbol(c_num_sms, &di.sms, sizeof(int)));
@@ -357,33 +332,18 @@ struct Group {
 // Fills (HBM-bound) run on the side stream s2 as graph branches forked after each level's
 // classification and joined at the end, overlapping the ALU-bound dwell kernels; a fill
 // writes only the interior of regions that are terminal, which no later kernel reads.
-// Iteration cap of MANDEL_FLAG_DEFER for a call, 0 when deferral does not apply.
-unsigned defer_cap(uint32_t flags, int32_t scheme, int32_t maxdwell, int ngroups)
-{
-    if (!(flags & MANDEL_FLAG_DEFER) || scheme != MANDEL_SCHEME_B200 || ngroups > 1 ||
-        (flags & (MANDEL_FLAG_STATS | MANDEL_FLAG_TILE_COST | MANDEL_FLAG_FLAT)))
-        return 0u;
-    unsigned c = 16u * ((flags & MANDEL_FLAG_DEFER_CAP_MASK) >> 16);
-    if (c == 0u)
-        c = MANDEL_DEFER_CAP_DEFAULT;
-    c = (c + MANDEL_RFB_K - 1) / MANDEL_RFB_K * MANDEL_RFB_K; // chunk boundaries
-    return c < (unsigned)maxdwell ? c : 0u;
-}
-
 int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, int sms, cudaStream_t s,
                 cudaStream_t s2, cudaEvent_t fork, Timing *tm)
 {
     const int ntiles = grp.ntiles;
     const size_t Lm = (size_t)lay.L - 1;
     // (ASK-SBR has no fill kernels: nothing to overlap)
-    const bool overlap = (k.flags & MANDEL_FLAG_SERIAL) == 0 && k.scheme != MANDEL_SCHEME_SBR &&
-                         k.scheme != MANDEL_SCHEME_FLOW;
+    const bool overlap = (k.flags & MANDEL_FLAG_SERIAL) == 0 && k.scheme != MANDEL_SCHEME_SBR;
     cudaStream_t sf = overlap ? s2 : s; // stream of the fill kernels
     char *ws = (char *)k.ws;
     LevelArgs a;
     memset(&a, 0, sizeof a);
-    a.map = make_map(k.reg, k.n);
-    a.maxdwell = k.maxdwell;
+    a.prm = (const DevParams *)(ws + lay.prm); // region map + maxdwell: read at kernel entry
     a.pitch = k.pitch;
     a.out = k.out;
     a.hdr = (WsHeader *)(ws + grp.hdr);
@@ -402,20 +362,13 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
     a.tile_cost = (k.flags & MANDEL_FLAG_TILE_COST) ? (unsigned long long *)(ws + lay.tile_cost) : nullptr;
     const bool stats = (k.flags & (MANDEL_FLAG_STATS | MANDEL_FLAG_TILE_COST)) != 0;
     const bool flat = (k.flags & MANDEL_FLAG_FLAT) != 0;
-    if ((k.scheme == MANDEL_SCHEME_B200 || k.scheme == MANDEL_SCHEME_FLOW) && lay.colT_bytes) {
+    if (k.scheme == MANDEL_SCHEME_B200 && lay.colT_bytes) {
         a.colT = (int *)(ws + lay.colT);
         a.u_log2 = lay.u_log2;
         a.colT_pitch = k.n;
     }
     const bool vec_ok = ((uintptr_t)k.out % 16 == 0) && (k.pitch % 4 == 0);
     const int d0 = (int)(k.n / k.g);
-    a.dcap = defer_cap(k.flags, k.scheme, k.maxdwell, ngroups);
-    const bool defer = a.dcap != 0u;
-    if (defer) {
-        a.pool = (DeferRec *)(ws + lay.pool);
-        a.capD = (uint32_t)lay.capD;
-        a.unc = (uint32_t *)(ws + lay.unc);
-    }
 
     // init: level-0 OLT + zeroed counters
     a.level = 0;
@@ -425,43 +378,10 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
     a.olt_in = olt_g[0];
     {
         int nthr = ntiles > 1024 ? ntiles : 1024;
-        if (nthr < k.g * k.g)
-            nthr = k.g * k.g;
         TBEGIN(s);
         k_init<<<(nthr + 255) / 256, 256, 0, s>>>(a);
         CK(cudaGetLastError());
         TEND(MANDEL_KIND_INIT, 0, s);
-    }
-    if (k.scheme == MANDEL_SCHEME_FLOW) { // one persistent dataflow kernel (flow.cuh)
-        a.ftask = (FlowTask *)(ws + lay.ftask);
-        a.funit = (uint4 *)(ws + lay.funit);
-        a.ffill = (uint2 *)(ws + lay.ffill);
-        a.ffd = (FastDiv *)(ws + lay.ffd);
-        a.fmark = (uint32_t *)(ws + lay.fmark);
-        a.r_log2 = ilog2(k.r);
-        a.fill_vec = vec_ok ? 1 : 0;
-        a.level = 0;
-        a.d = d0;
-        {
-            int gsz = resident_grid(k_flow_clear, 256, sms, (lay.funit_cap + 255) / 256);
-            k_flow_clear<<<gsz, 256, 0, s>>>(a, lay.funit_cap);
-            CK(cudaGetLastError());
-        }
-        TBEGIN(s);
-        k_flow_init<<<(ntiles * 32 + 255) / 256 > 0 ? (ntiles * 32 + 255) / 256 : 1, 256, 0, s>>>(a);
-        CK(cudaGetLastError());
-        TEND(MANDEL_KIND_FLOW_INIT, 0, s);
-        TBEGIN(s);
-        if (stats) {
-            int gsz = resident_grid(k_flow<true>, RF_TPB, sms, (size_t)1 << 30);
-            k_flow<true><<<gsz, RF_TPB, 0, s>>>(a);
-        } else {
-            int gsz = resident_grid(k_flow<false>, RF_TPB, sms, (size_t)1 << 30);
-            k_flow<false><<<gsz, RF_TPB, 0, s>>>(a);
-        }
-        CK(cudaGetLastError());
-        TEND(MANDEL_KIND_FLOW, 0, s);
-        return MANDEL_OK;
     }
     int d = d0;
     for (int l = 0; l < lay.L; ++l) {
@@ -533,9 +453,6 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
                 if (stats) {
                     int gsz = resident_grid(k_b200_border_rf<true>, RF_TPB, sms, rf_blocks);
                     CK(launch_pdl(k_b200_border_rf<true>, gsz, RF_TPB, s, a));
-                } else if (defer) {
-                    int gsz = resident_grid(k_b200_border_rf<false, true>, RF_TPB, sms, rf_blocks);
-                    k_b200_border_rf<false, true><<<gsz, RF_TPB, 0, s>>>(a);
                 } else {
                     int gsz = resident_grid(k_b200_border_rf<false>, RF_TPB, sms, rf_blocks);
                     CK(launch_pdl(k_b200_border_rf<false>, gsz, RF_TPB, s, a));
@@ -546,43 +463,16 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
             TBEGIN(s);
             if (d >= 256) {
                 int gsz = resident_grid(k_b200_classify<8>, 256, sms, cap);
-                if (defer)
-                    k_b200_classify<8, true><<<gsz, 256, 0, s>>>(a);
-                else
-                    CK(launch_pdl(k_b200_classify<8>, gsz, 256, s, a));
-            } else if (d <= MANDEL_CLASSIFY_HALF_D && !defer) { // half a warp per region
+                CK(launch_pdl(k_b200_classify<8>, gsz, 256, s, a));
+            } else if (d <= MANDEL_CLASSIFY_HALF_D) { // half a warp per region
                 int gsz = resident_grid(k_b200_classify<0>, 256, sms, (cap + 15) / 16);
                 CK(launch_pdl(k_b200_classify<0>, gsz, 256, s, a));
             } else {
                 int gsz = resident_grid(k_b200_classify<1>, 256, sms, (cap + 7) / 8);
-                if (defer)
-                    k_b200_classify<1, true><<<gsz, 256, 0, s>>>(a);
-                else
-                    CK(launch_pdl(k_b200_classify<1>, gsz, 256, s, a));
+                CK(launch_pdl(k_b200_classify<1>, gsz, 256, s, a));
             }
             CK(cudaGetLastError());
             TEND(MANDEL_KIND_B200_CLASSIFY, l, s);
-            if (defer) { // finish the uncertain regions' markers, then decide those regions
-                a.fd[0] = fastdiv_nz((uint32_t)(4 * d - 4));
-                TBEGIN(s);
-                {
-                    const size_t rf_blocks = (cap * (size_t)(4 * d - 4) + RF_TPB - 1) / RF_TPB;
-                    int gsz = resident_grid(k_b200_resolve, RF_TPB, sms, rf_blocks);
-                    k_b200_resolve<<<gsz, RF_TPB, 0, s>>>(a);
-                    CK(cudaGetLastError());
-                }
-                TEND(MANDEL_KIND_B200_RESOLVE, l, s);
-                TBEGIN(s);
-                if (d >= 256) {
-                    int gsz = resident_grid(k_b200_classify<8, false, true>, 256, sms, cap);
-                    k_b200_classify<8, false, true><<<gsz, 256, 0, s>>>(a);
-                } else {
-                    int gsz = resident_grid(k_b200_classify<1, false, true>, 256, sms, (cap + 7) / 8);
-                    k_b200_classify<1, false, true><<<gsz, 256, 0, s>>>(a);
-                }
-                CK(cudaGetLastError());
-                TEND(MANDEL_KIND_B200_CLASSIFY, l, s);
-            }
         }
         // fill (terminal work) of this level's uniform regions: flat over all of them
         // (B200, MBR); ASK-SBR filled them inside its level kernel
@@ -596,15 +486,6 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
                 CK(cudaEventRecord(fork, s));
                 CK(cudaStreamWaitEvent(sf, fork, 0));
             }
-            // An overlapped fill runs beside the level kernels; it only needs enough warps to
-            // keep HBM busy (its 128-bit stores never stall a thread), so its grid is capped at
-            // MANDEL_FILL_BPS blocks per SM (0: fully resident) to leave the SMs' warp slots to
-            // the critical path.
-#ifndef MANDEL_FILL_BPS
-#define MANDEL_FILL_BPS 0
-#endif
-            if (overlap && MANDEL_FILL_BPS > 0 && blocks > (size_t)MANDEL_FILL_BPS * sms)
-                blocks = (size_t)MANDEL_FILL_BPS * sms;
             TBEGIN(sf);
             if (vec) {
                 int gsz = resident_grid(k_fill<true>, 256, sms, blocks);
@@ -618,13 +499,6 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
         }
         if (l + 1 < lay.L)
             d /= k.r;
-    }
-    if (defer) { // every deferred pixel not finished by a level's resolve pass
-        TBEGIN(s);
-        int gsz = resident_grid(k_b200_resume, RF_TPB, sms, (lay.capD + RF_TPB - 1) / RF_TPB);
-        k_b200_resume<<<gsz, RF_TPB, 0, s>>>(a);
-        CK(cudaGetLastError());
-        TEND(MANDEL_KIND_B200_RESUME, 0, s);
     }
     // leaves of the last level
     {
@@ -703,13 +577,10 @@ void free_entry(Entry &e)
 {
     if (e.exec)
         cudaGraphExecDestroy(e.exec);
-    if (e.h_tiles)
-        cudaFreeHost(e.h_tiles);
     for (auto ev : e.evs)
         cudaEventDestroy(ev);
     e.evs.clear();
     e.exec = nullptr;
-    e.h_tiles = nullptr;
 }
 
 int validate_common(const mandel_region &reg, int64_t n, int32_t maxdwell, int32_t *d_out, int64_t pitch)
@@ -719,6 +590,21 @@ int validate_common(const mandel_region &reg, int64_t n, int32_t maxdwell, int32
     return MANDEL_OK;
 }
 
+template <int BX, int BY, int K>
+int launch_exhaustive(const mandel_region &reg, int64_t n, int32_t maxdwell, int32_t *d_out, int64_t out_pitch,
+                      void *stream)
+{
+    ExArgs a;
+    a.map = make_map(reg, n);
+    a.n = (int)n;
+    a.maxdwell = maxdwell;
+    a.pitch = out_pitch;
+    a.out = d_out;
+    dim3 grid((unsigned)((n + BX - 1) / BX), (unsigned)((n + BY - 1) / BY));
+    k_exhaustive<BX, BY, K><<<grid, dim3(BX, BY), 0, (cudaStream_t)stream>>>(a);
+    CK(cudaGetLastError());
+    return MANDEL_OK;
+}
 } // namespace
 
 extern "C" {
@@ -738,25 +624,56 @@ int32_t mandel_ask_levels(int64_t n, int32_t g, int32_t r, int32_t B)
     return levels_of(n, g, r, B);
 }
 
+int mandel_fp32_peak_probe(int32_t steps, double *tops, void *stream)
+{
+    if (steps < 1 || !tops)
+        return MANDEL_EINVAL;
+    int dev = 0, sms = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    const int blocks = sms * 8; // 8 x 256 threads per SM: 16 warps per sub-partition
+    double best = 0.0;
+    int rc = MANDEL_OK;
+    for (int rep = 0; rep < 4 && rc == MANDEL_OK; ++rep) {
+        float ms = 0.0f;
+        cudaEventRecord(e0, st);
+        k_probe_fp32<2><<<blocks, 256, 0, st>>>(-1.0f, 0.0f, steps, nullptr);
+        cudaEventRecord(e1, st);
+        cudaError_t e = cudaEventSynchronize(e1);
+        if (e == cudaSuccess)
+            e = cudaGetLastError();
+        if (e == cudaSuccess)
+            e = cudaEventElapsedTime(&ms, e0, e1);
+        if (e != cudaSuccess) {
+            rc = cuda_fail(e, "mandel_fp32_peak_probe");
+            break;
+        }
+        const double ops = 7.0 * 2 * 8 * (double)steps * blocks * 256;
+        if (rep > 0 && ms > 0.0f && ops / (ms * 1e9) > best) // rep 0 warms up
+            best = ops / (ms * 1e9);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *tops = best;
+    return rc;
+}
+
 int32_t mandel_ask_kernel_count(int64_t n, int32_t g, int32_t r, int32_t B, int32_t scheme)
 {
     if (!valid_grb(n, g, r, B))
         return 0;
     const int L = levels_of(n, g, r, B);
-    if (scheme == MANDEL_SCHEME_FLOW)
-        return 4; // init, unit-array clear, flow init, flow
     return 1 + L * (scheme == MANDEL_SCHEME_SBR ? 1 : scheme == MANDEL_SCHEME_MBR ? 2 : 3) + 1;
 }
 
-int32_t mandel_ask_kernel_count_ex(int64_t n, int32_t g, int32_t r, int32_t B, int32_t scheme, uint32_t flags,
-                                   int32_t maxdwell)
+long long mandel_ask_graph_captures(void)
 {
-    const int32_t base = mandel_ask_kernel_count(n, g, r, B, scheme);
-    if (base == 0 || maxdwell < 1)
-        return 0;
-    if (!defer_cap(flags, scheme, maxdwell, MANDEL_FLAG_GROUPS_OF(flags)))
-        return base;
-    return base + 2 * levels_of(n, g, r, B) + 1; // resolve + re-classify per level, resume
+    std::lock_guard<std::mutex> lk(g_mu);
+    return g_captures;
 }
 
 int mandel_exhaustive(mandel_region reg, int64_t n, int32_t maxdwell, int32_t *d_out, int64_t out_pitch,
@@ -765,25 +682,21 @@ int mandel_exhaustive(mandel_region reg, int64_t n, int32_t maxdwell, int32_t *d
     int rc = validate_common(reg, n, maxdwell, d_out, out_pitch);
     if (rc)
         return rc;
-    ExArgs a;
-    a.map = make_map(reg, n);
-    a.n = (int)n;
-    a.maxdwell = maxdwell;
-    a.pitch = out_pitch;
-    a.out = d_out;
     // block shape of the flat Ex kernel (tuned on the box like the paper's Table 2 search,
     // P:459-468; profiles/r01_tune_ex.txt)
-#ifndef MANDEL_EX_BX
-#define MANDEL_EX_BX 16
+    return launch_exhaustive<16, 16, DWELL_K>(reg, n, maxdwell, d_out, out_pitch, stream);
+}
+
+int mandel_exhaustive_tuned(mandel_region reg, int64_t n, int32_t maxdwell, int32_t *d_out, int64_t out_pitch,
+                            void *stream)
+{
+    int rc = validate_common(reg, n, maxdwell, d_out, out_pitch);
+    if (rc)
+        return rc;
+#ifndef MANDEL_EXT_K
+#define MANDEL_EXT_K 32
 #endif
-#ifndef MANDEL_EX_BY
-#define MANDEL_EX_BY 16
-#endif
-    constexpr int BX = MANDEL_EX_BX, BY = MANDEL_EX_BY;
-    dim3 grid((unsigned)((n + BX - 1) / BX), (unsigned)((n + BY - 1) / BY));
-    k_exhaustive<BX, BY><<<grid, dim3(BX, BY), 0, (cudaStream_t)stream>>>(a);
-    CK(cudaGetLastError());
-    return MANDEL_OK;
+    return launch_exhaustive<32, 8, MANDEL_EXT_K>(reg, n, maxdwell, d_out, out_pitch, stream);
 }
 
 int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, int32_t r, int32_t B,
@@ -793,11 +706,10 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
     int rc = validate_common(reg, n, maxdwell, d_out, out_pitch);
     if (rc)
         return rc;
-    if (!valid_grb(n, g, r, B) || !d_ws || (scheme != MANDEL_SCHEME_SBR && scheme != MANDEL_SCHEME_B200 && scheme != MANDEL_SCHEME_MBR &&
-                                  scheme != MANDEL_SCHEME_FLOW) ||
+    if (!valid_grb(n, g, r, B) || !d_ws ||
+        (scheme != MANDEL_SCHEME_SBR && scheme != MANDEL_SCHEME_B200 && scheme != MANDEL_SCHEME_MBR) ||
         (flags & ~(MANDEL_FLAG_STATS | MANDEL_FLAG_TIMING | MANDEL_FLAG_TILE_COST | MANDEL_FLAG_FLAT |
-                   MANDEL_FLAG_SERIAL | MANDEL_FLAG_GROUPS_MASK | MANDEL_FLAG_DEFER | MANDEL_FLAG_TIMING_LEAF |
-                   MANDEL_FLAG_DEFER_CAP_MASK)) != 0 ||
+                   MANDEL_FLAG_SERIAL | MANDEL_FLAG_GROUPS_MASK | MANDEL_FLAG_TIMING_LEAF)) != 0 ||
         MANDEL_FLAG_GROUPS_OF(flags) > MAXG)
         return MANDEL_EINVAL;
     Layout lay;
@@ -808,13 +720,12 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
     if ((uintptr_t)d_ws % 256 != 0)
         return MANDEL_EINVAL;
     const int64_t G = (int64_t)g * g;
-    std::vector<int32_t> tiles;
     if (h_tile_ids) {
         if (n_tiles < 0 || n_tiles > G)
             return MANDEL_EINVAL;
         std::vector<char> seen((size_t)G, 0);
-        tiles.assign(h_tile_ids, h_tile_ids + n_tiles);
-        for (int32_t t : tiles) {
+        for (int32_t i = 0; i < n_tiles; ++i) {
+            const int32_t t = h_tile_ids[i];
             if (t < 0 || t >= G || seen[(size_t)t])
                 return MANDEL_EINVAL;
             seen[(size_t)t] = 1;
@@ -823,6 +734,11 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
         return MANDEL_EINVAL;
     }
     const int ntiles = h_tile_ids ? n_tiles : (int)G;
+    // groups: the tiles are dealt round-robin in the given order (LPT order is preserved)
+    int ngroups = MANDEL_FLAG_GROUPS_OF(flags);
+    if (ngroups > ntiles)
+        ngroups = ntiles > 0 ? ntiles : 1;
+    const bool listed = h_tile_ids != nullptr || ngroups > 1;
 
     int dev = 0;
     CK(cudaGetDevice(&dev));
@@ -831,7 +747,32 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
     if ((rc = dev_info(dev, di)))
         return rc;
 
-    Key key{dev, reg, n, out_pitch, maxdwell, g, r, B, scheme, flags, d_out, d_ws, ws_bytes, tiles};
+    // ---- per-call device parameter block: region map, maxdwell, the group-dealt tile list.
+    // Pageable source: cudaMemcpyAsync stages it before returning, so the buffer is free for
+    // the next call while this one is still queued.
+    thread_local std::vector<unsigned char> hp;
+    hp.assign(PRM_TILES + (listed ? (size_t)ntiles * 4 : 0), 0);
+    DevParams prm;
+    memset(&prm, 0, sizeof prm);
+    prm.map = make_map(reg, n);
+    prm.maxdwell = maxdwell;
+    prm.ntiles = ntiles;
+    prm.magic = PRM_MAGIC;
+    memcpy(hp.data(), &prm, sizeof prm);
+    std::vector<int> gcount((size_t)ngroups, 0);
+    {
+        int32_t *ord = (int32_t *)(hp.data() + PRM_TILES);
+        size_t o = 0;
+        for (int gi = 0; gi < ngroups; ++gi)
+            for (int i = gi; i < ntiles; i += ngroups) {
+                if (listed)
+                    ord[o++] = h_tile_ids ? h_tile_ids[i] : i;
+                ++gcount[(size_t)gi];
+            }
+    }
+    CK(cudaMemcpyAsync((char *)d_ws + lay.prm, hp.data(), hp.size(), cudaMemcpyHostToDevice, (cudaStream_t)stream));
+
+    Key key{dev, n, out_pitch, g, r, B, scheme, flags, d_out, d_ws, ws_bytes, ntiles, listed};
     Entry *hit = nullptr;
     for (auto &e : g_cache)
         if (e.key == key) {
@@ -849,48 +790,23 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
         }
         Entry e;
         e.key = key;
-        // groups: tiles dealt round-robin in the given order (LPT order is preserved)
-        int ngroups = scheme == MANDEL_SCHEME_FLOW ? 1 : MANDEL_FLAG_GROUPS_OF(flags);
-        if (ngroups > ntiles)
-            ngroups = ntiles > 0 ? ntiles : 1;
-        std::vector<int32_t> order;
-        std::vector<int> gcount((size_t)ngroups, 0);
-        if (ngroups > 1 || h_tile_ids) {
-            std::vector<int32_t> all(tiles);
-            if (!h_tile_ids)
-                for (int32_t t = 0; t < ntiles; ++t)
-                    all.push_back(t);
-            for (int gi = 0; gi < ngroups; ++gi)
-                for (int i = gi; i < ntiles; i += ngroups) {
-                    order.push_back(all[(size_t)i]);
-                    ++gcount[(size_t)gi];
-                }
-        } else {
-            gcount[0] = ntiles;
-        }
-        if (!order.empty()) {
-            CK(cudaHostAlloc((void **)&e.h_tiles, order.size() * 4, cudaHostAllocMapped | cudaHostAllocPortable));
-            memcpy(e.h_tiles, order.data(), order.size() * 4);
-        }
-        int32_t *d_tiles = nullptr;
-        if (e.h_tiles) {
-            cudaError_t ce = cudaHostGetDevicePointer((void **)&d_tiles, e.h_tiles, 0);
-            if (ce != cudaSuccess) {
-                free_entry(e);
-                return cuda_fail(ce, "cudaHostGetDevicePointer");
-            }
-        }
+        e.ngroups = ngroups;
+        const int32_t *d_tiles = listed ? (const int32_t *)((char *)d_ws + lay.prm + PRM_TILES) : nullptr;
         cudaGraph_t graph = nullptr;
         cudaError_t ce = cudaStreamBeginCapture(di->cap, cudaStreamCaptureModeThreadLocal);
-        if (ce != cudaSuccess) {
-            free_entry(e);
+        if (ce != cudaSuccess)
             return cuda_fail(ce, "cudaStreamBeginCapture");
-        }
         Timing tm;
         tm.on = (flags & (MANDEL_FLAG_TIMING | MANDEL_FLAG_TIMING_LEAF)) != 0;
         tm.leaf_only = (flags & MANDEL_FLAG_TIMING) == 0;
         int erc = MANDEL_OK;
-        if (ngroups == 1) {
+        if (flags & MANDEL_FLAG_TILE_COST) { // every g*g counter starts at 0 (a memset node)
+            ce = cudaMemsetAsync((char *)d_ws + lay.tile_cost, 0, (size_t)G * 8, di->cap);
+            if (ce != cudaSuccess)
+                erc = cuda_fail(ce, "cudaMemsetAsync(tile_cost)");
+        }
+        if (erc) {
+        } else if (ngroups == 1) {
             Group grp{lay.hdr, 0, ntiles, d_tiles};
             erc = enqueue_ask(key, lay, grp, 1, di->sms, di->cap, di->side[0], di->fork[0], &tm);
         } else { // fork one branch per group off the origin stream, join them at the end
@@ -929,6 +845,7 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
             free_entry(e);
             return cuda_fail(ce, "cudaGraphInstantiate");
         }
+        ++g_captures;
         g_cache.push_back(e);
         hit = &g_cache.back();
     }
@@ -1067,7 +984,6 @@ int mandel_ask_last_stats(const void *d_ws, mandel_level_stats *h_out, int32_t m
         s.side = (int32_t)d;
         s.regions_in = regions;
         s.filled = s.subdivided = s.leaves = s.border_px = s.border_iters = s.leaf_px = s.leaf_iters = 0;
-        s.deferred = s.uncertain = 0;
         for (const auto &hg : hs) {
             s.filled += hg.n_fill[l];
             s.subdivided += hg.n_subdiv[l];
@@ -1076,10 +992,6 @@ int mandel_ask_last_stats(const void *d_ws, mandel_level_stats *h_out, int32_t m
             s.border_iters += (int64_t)hg.border_iters[l];
             s.leaf_px += (l == L - 1) ? (int64_t)hg.leaf_px : 0;
             s.leaf_iters += (l == L - 1) ? (int64_t)hg.leaf_iters : 0;
-            // snapshots are 0 for levels of a call without deferral
-            const uint32_t prev = l > 0 ? hg.n_defer_snap[l - 1] : 0u;
-            s.deferred += hg.n_defer_snap[l] >= prev ? (int64_t)(hg.n_defer_snap[l] - prev) : 0;
-            s.uncertain += hg.n_unc[l];
         }
         regions = s.subdivided * h.r * h.r;
         d /= h.r;
@@ -1146,7 +1058,8 @@ void mandel_shutdown(void)
     for (auto &e : g_cache)
         free_entry(e);
     g_cache.clear();
-    for (auto &d : g_dev) {
+    for (auto &dp : g_dev) {
+        DevInfo &d = *dp;
         if (d.cap)
             cudaStreamDestroy(d.cap);
         if (d.start)

@@ -89,33 +89,6 @@ constexpr int RF_QCAP = 64; // per-warp queue entries (< 32 left over + < 32 new
 #define MANDEL_RF_EXACT_PPW 1024u // scalar engine: exact grabs below this many pixels per warp
 #endif
 
-// Deferred long pixels.  A border pixel still unescaped after `cap`
-// iterations is parked in the workspace pool with its orbit state and its image (and colT)
-// slot holds the marker -1 - (pool index); its dwell is finished later (k_b200_resolve for
-// regions whose whole ring is unresolved, k_b200_resume for the rest at the end).
-struct DeferRec {
-    uint32_t pxy; // x | y << 16
-    float x, y;   // orbit at iteration it (x2, y2 are x*x, y*y again)
-    uint32_t it;
-};
-struct DeferCtx {
-    DeferRec *pool;
-    uint32_t capD;   // pool entries; a pixel that finds the pool full is computed to the end
-    uint32_t *count; // header counter (may run past capD)
-    unsigned cap;    // iteration cap, a multiple of K
-};
-
-// Maps whose entries resume a saved orbit define `static constexpr bool kResume = true` and
-// `bool state(t, px, py, x, y, it)` (false: nothing to do for t).
-template <class M, class = void>
-struct map_resumes {
-    static constexpr bool value = false;
-};
-template <class M>
-struct map_resumes<M, decltype((void)M::kResume)> {
-    static constexpr bool value = M::kResume;
-};
-
 // SM count of the device the kernels run on (set by the host before capture).
 __constant__ int c_num_sms;
 
@@ -252,17 +225,13 @@ __device__ __forceinline__ int rf2_prepass(uint32_t b, uint32_t e, const PixMap 
 // The grab size adapts to the launch: at most CH, but small enough that every warp of the
 // grid gets about 4 grabs (small levels -- e.g. one rank's share of a multi-GPU run -- would
 // otherwise leave most warps idle while a few run whole grabs of maxdwell pixels), and >= 8.
-// DEFER: pixels reaching dc->cap iterations unescaped are deferred (DeferRec above) instead
-// of run to the end.  A resuming Map (map_resumes) hands out saved orbits instead of pixels.
-// PRE > 0 (raw-pixel maps only): the short-pixel prepass of rf2_prepass on every grab, with
+// PRE > 0: the short-pixel prepass of rf2_prepass on every grab, with
 // the per-warp survivor buffer sv (CH entries); survivors are dealt to lanes at iteration PRE.
-template <int K, int T, int CH, class Map, class Sink, bool DEFER = false, int PRE = 0>
+template <int K, int T, int CH, class Map, class Sink, int PRE = 0>
 __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint32_t total,
                                             unsigned long long *cursor, const Map &map, Sink &sink,
-                                            ParkedPoint *q, int tslot = 0, const DeferCtx *dc = nullptr,
-                                            SvPoint *sv = nullptr)
+                                            ParkedPoint *q, int tslot = 0, SvPoint *sv = nullptr)
 {
-    constexpr bool RESUME = map_resumes<Map>::value;
     // Active warps: a launch with few pixels per lane runs like a thread-per-pixel kernel
     // (every warp waits for its slowest lane and there is nothing to refill from), so only
     // ~total/(32*PPL) warps work -- but never fewer than 2 per SM sub-partition (592 on
@@ -295,48 +264,16 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
     uint32_t pos = 0, end = 0; // warp-uniform chunk window [pos, end)
     bool exhausted = false;    // warp-uniform: the cursor ran past total
     int qn = 0;                // warp-uniform queue fill
-    const bool use_pre = PRE > 0 && !RESUME && sv != nullptr && maxdwell > PRE;
+    const bool use_pre = PRE > 0 && sv != nullptr && maxdwell > PRE;
     uint32_t sv_pos = 0, sv_end = 0; // warp-uniform survivor buffer window
     int pre_esc = 0;
 
     bool has = false, fin = false;
-    bool dfr = false, nod = false; // DEFER: parked for the pool / pool was full (run to the end)
     int px = 0, py = 0;
     float cr = 0.f, ci = 0.f, x = 0.f, y = 0.f, x2 = 0.f, y2 = 0.f, sx = 0.f, sy = 0.f;
     unsigned it = 0, sit = 0;
 
     while (true) {
-        // ---------------------------------------------------------------- defer
-        if (DEFER) {
-            const unsigned dm = __ballot_sync(FULL, dfr);
-            if (dm) {
-                uint32_t base = 0;
-                if (lane == 0)
-                    base = atomicAdd(dc->count, (uint32_t)__popc(dm));
-                base = __shfl_sync(FULL, base, 0);
-                if (dfr) {
-                    const uint32_t idx = base + (uint32_t)__popc(dm & lt);
-                    if (idx < dc->capD) {
-                        DeferRec e;
-                        e.pxy = (uint32_t)px | ((uint32_t)py << 16);
-                        e.x = sx;
-                        e.y = sy;
-                        e.it = sit;
-                        dc->pool[idx] = e;
-                        sink(px, py, -1 - (int)idx);
-                        has = false;
-                    } else { // pool full: resume from the saved point and run to the end
-                        nod = true;
-                        x = sx;
-                        y = sy;
-                        x2 = __fmul_rn(sx, sx);
-                        y2 = __fmul_rn(sy, sy);
-                        it = sit;
-                    }
-                    dfr = false;
-                }
-            }
-        }
         // ---------------------------------------------------------------- park + refill
         const unsigned f = __ballot_sync(FULL, fin);
         if (f) {
@@ -359,7 +296,7 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
         }
         unsigned need = __ballot_sync(FULL, !has);
         while (need && !exhausted) {
-            if constexpr (PRE > 0 && !RESUME) {
+            if constexpr (PRE > 0) {
               if (use_pre) {
                 if (sv_pos >= sv_end) { // prepass a fresh grab; its survivors refill the buffer
                     unsigned long long b = 0;
@@ -391,7 +328,6 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
                     x2 = __fmul_rn(x, x);
                     y2 = __fmul_rn(y, y);
                     it = (unsigned)PRE;
-                    nod = false;
                     has = true;
                 }
                 sv_pos += take;
@@ -423,32 +359,16 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
             const unsigned take = avail < cnt ? avail : cnt;
             const unsigned rank = __popc(need & lt);
             if (!has && rank < take) {
-                if constexpr (RESUME) { // a deferred orbit (|c|^2 <= 3.9: it ran chunked)
-                    float rx, ry;
-                    unsigned rit;
-                    if (map.state(pos + rank, px, py, rx, ry, rit)) {
-                        cr = pix_re(pm, px);
-                        ci = pix_im(pm, py);
-                        has = true;
-                        x = rx;
-                        y = ry;
-                        x2 = __fmul_rn(rx, rx);
-                        y2 = __fmul_rn(ry, ry);
-                        it = rit;
-                    }
-                } else {
-                    map(pos + rank, px, py);
-                    cr = pix_re(pm, px);
-                    ci = pix_im(pm, py);
-                    const float c2 = __fadd_rn(__fmul_rn(cr, cr), __fmul_rn(ci, ci));
-                    if (c2 <= 3.9f) {
-                        has = true;
-                        nod = false;
-                        x = y = x2 = y2 = 0.0f;
-                        it = 0;
-                    } else { // per-step loop (escape permanence not guaranteed)
-                        sink(px, py, dwell_per_step<K>(cr, ci, maxdwell));
-                    }
+                map(pos + rank, px, py);
+                cr = pix_re(pm, px);
+                ci = pix_im(pm, py);
+                const float c2 = __fadd_rn(__fmul_rn(cr, cr), __fmul_rn(ci, ci));
+                if (c2 <= 3.9f) {
+                    has = true;
+                    x = y = x2 = y2 = 0.0f;
+                    it = 0;
+                } else { // per-step loop (escape permanence not guaranteed)
+                    sink(px, py, dwell_per_step<K>(cr, ci, maxdwell));
                 }
             }
             pos += take;
@@ -467,7 +387,7 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
         const int thresh = exhausted ? 32 : T;
         const bool live = has;
         while (true) {
-            const bool keep = fin || dfr || !live;
+            const bool keep = fin || !live;
             sx = keep ? sx : x;
             sy = keep ? sy : y;
             sit = keep ? sit : it;
@@ -475,15 +395,8 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
             for (int k = 0; k < K; ++k)
                 MANDEL_STEP(x, y, x2, y2, cr, ci);
             it += K;
-            fin = live && !dfr && (fin || !(__fadd_rn(x2, y2) <= 4.0f) || it >= md);
-            if (DEFER) { // unescaped at the cap: keep this point (not the chunk start) for the pool
-                const bool nd = live && !fin && !dfr && !nod && it >= dc->cap;
-                sx = nd ? x : sx;
-                sy = nd ? y : sy;
-                sit = nd ? it : sit;
-                dfr = dfr || nd;
-            }
-            const unsigned fm = __ballot_sync(FULL, fin || dfr);
+            fin = live && (fin || !(__fadd_rn(x2, y2) <= 4.0f) || it >= md);
+            const unsigned fm = __ballot_sync(FULL, fin);
             if (fm == active || __popc(fm) >= thresh)
                 break;
         }

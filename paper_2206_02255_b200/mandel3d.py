@@ -27,6 +27,15 @@ def _stream_ptr(stream) -> int:
     return int(s.cuda_stream)
 
 
+def _check_device(out, *others, stream=None):
+    """libmandel3d.so launches on the current device: buffers and stream must be on out's."""
+    for t in others:
+        if t is not None and t.device != out.device:
+            raise ValueError(f"buffer on {t.device} but out is on {out.device}")
+    if stream is not None and stream.device != out.device:
+        raise ValueError(f"stream on {stream.device} but out is on {out.device}")
+
+
 def levels3d(n: int, g: int, r: int, B: int) -> int:
     return int(_lib.load_3d().mandel3d_ask_levels(n, g, r, B))
 
@@ -55,8 +64,10 @@ def _region(region3: Sequence[float]):
 def exhaustive3d(region3, n: int, maxdwell: int, out=None, stream=None):
     """Exhaustive dwell volume: one thread per voxel."""
     out = _volume(n, out)
-    _lib.check3(_lib.load_3d().mandel3d_exhaustive(_region(region3), n, maxdwell, out.data_ptr(),
-                                                   _stream_ptr(stream)), "mandel3d_exhaustive")
+    _check_device(out, stream=stream)
+    with _torch().cuda.device(out.device):
+        rc = _lib.load_3d().mandel3d_exhaustive(_region(region3), n, maxdwell, out.data_ptr(), _stream_ptr(stream))
+    _lib.check3(rc, "mandel3d_exhaustive")
     return out
 
 
@@ -65,18 +76,24 @@ def ask3d(region3, n: int, maxdwell: int, g: int, r: int, B: int, out=None, ws=N
     """3-D ASK volume over all g^3 level-0 cubes (surface test, fill / r^3 split / leaf);
     flat: thread-per-voxel surface/leaf kernels instead of the lane-refill engine (A/B)."""
     out = _volume(n, out)
+    _check_device(out, ws, stream=stream)
     if ws is None:
         ws = workspace3d(n, g, r, B, device=out.device)
-    rc = _lib.load_3d().mandel3d_ask(_region(region3), n, maxdwell, g, r, B, (1 if stats else 0) | (2 if flat else 0),
-                                     out.data_ptr(),
-                                     ws.data_ptr(), ws.numel(), _stream_ptr(stream))
+        torch = _torch()
+        if stream is not None and stream != torch.cuda.current_stream(out.device):
+            ws.record_stream(stream)  # a call-local workspace must outlive the launch on `stream`
+    with _torch().cuda.device(out.device):
+        rc = _lib.load_3d().mandel3d_ask(_region(region3), n, maxdwell, g, r, B,
+                                         (1 if stats else 0) | (2 if flat else 0), out.data_ptr(),
+                                         ws.data_ptr(), ws.numel(), _stream_ptr(stream))
     _lib.check3(rc, "mandel3d_ask")
     return out
 
 
 def ask3d_stats(ws, stream=None) -> List[dict]:
     buf = (_lib.Mandel3dLevelStats * MAX_LEVELS)()
-    L = _lib.load_3d().mandel3d_ask_last_stats(ws.data_ptr(), buf, MAX_LEVELS, _stream_ptr(stream))
+    with _torch().cuda.device(ws.device):
+        L = _lib.load_3d().mandel3d_ask_last_stats(ws.data_ptr(), buf, MAX_LEVELS, _stream_ptr(stream))
     if L < 0:
         raise RuntimeError("mandel3d_ask_last_stats failed")
     return [{k: int(getattr(buf[i], k)) for k, _ in _lib.Mandel3dLevelStats._fields_} for i in range(min(L, MAX_LEVELS))]

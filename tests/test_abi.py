@@ -73,7 +73,7 @@ def test_no_fma_in_dwell_kernels():
     for f in funcs[1:]:
         name = f.split("\n", 1)[0]
         if any(k in name for k in ("k_exhaustive", "k_sbr_level", "k_sbr_leaf", "k_b200_border", "k_b200_leaf",
-                                   "k_b200_resolve", "k_b200_resume", "k_dp")):
+                                   "k_dp")):
             # no scalar FFMA at all
             assert re.search(r"\bFFMA\b", f) is None, name
             # packed engine: every FFMA2 is a product fma(a, b, -0) whose addend is the
@@ -86,6 +86,13 @@ def test_no_fma_in_dwell_kernels():
             assert ("FMUL" in f and "FADD" in f) or (ffma2 and "FADD2" in f), name
             checked += 1
     assert checked >= 7
+    assert lib_has_no_experimental_kernels(sass)
+
+
+def lib_has_no_experimental_kernels(sass: str) -> bool:
+    """The rejected round-1 experiments (dataflow scheme, deferred pixels) are not in the
+    product library any more (git history keeps them)."""
+    return not any(k in sass for k in ("k_flow", "k_b200_resolve", "k_b200_resume"))
 
 
 def test_levels_and_workspace(lib):
@@ -96,31 +103,18 @@ def test_levels_and_workspace(lib):
     assert mb.levels(8192, 2, 4, 32) == 4      # non-exact tiling: 4096,1024,256,64
     assert mb.levels(64, 8, 2, 8) == 1
     # worst case: 2 OLTs + leaf list of (n/B_last)^2 u32 + 4/3 of it as 8-byte fill entries,
-    # plus the transposed column lines (2 n/u columns of n int32, leaf side u >= 8)
-    # plus the flow scheme's arrays: tasks (16 B, <= regions + g^2), pixel/fill units (16 B,
-    # <= n^2/64 + n^2/4096 + tasks + fills), fills (8 B, <= regions)
-    # plus MANDEL_FLAG_DEFER's pool (16 B x max(n^2/64, 65536)) and uncertain list (4 B x M)
-    def flow_bytes(n, g, r, L):
-        regions = sum(g * g * r ** (2 * l) for l in range(L))
-        tasks = regions + g * g
-        return (16 * tasks + 16 * (n * n // 64 + n * n // 4096 + tasks + regions) + 8 * regions
-                + 16 * max(n * n // 64, 65536) + 4 * (g * r ** (L - 1)) ** 2)
+    # plus the transposed column lines (2 n/u columns of n int32, leaf side u >= 8), plus the
+    # headers and the device parameter block (256 B + 4 B per level-0 tile)
     ws = mb.workspace_bytes(65536, 16, 2, 32)
     M = (65536 // 32) ** 2
     colT = 2 * (65536 // 32) * 65536 * 4
-    fb = flow_bytes(65536, 16, 2, 8)
-    assert 3 * 4 * M + 8 * M + colT + fb < ws < 3 * 4 * M + 8 * M * 4 // 3 + colT + fb + 2 * 1024 * 1024
+    assert 3 * 4 * M + 8 * M + colT < ws < 3 * 4 * M + 8 * M * 4 // 3 + colT + (1 << 20)
     # leaf side 4 (< 8): no column copy
     M4 = (1024 // 4) ** 2
-    assert mb.workspace_bytes(1024, 4, 2, 4) < 3 * 4 * M4 + 8 * M4 * 4 // 3 + flow_bytes(1024, 4, 2, 7) + 2 * 1024 * 1024
+    assert mb.workspace_bytes(1024, 4, 2, 4) < 3 * 4 * M4 + 8 * M4 * 4 // 3 + (1 << 20)
     assert mb.kernel_count(32768, 16, 2, 32, "b200") == 1 + 7 * 3 + 1
     assert mb.kernel_count(32768, 16, 2, 32, "sbr") == 1 + 7 * 1 + 1   # fills inside the level kernel
     assert mb.kernel_count(32768, 16, 2, 32, "mbr") == 1 + 7 * 2 + 1   # + flat fill per level
-    # MANDEL_FLAG_DEFER: + resolve and re-classify per level, + one resume kernel
-    assert mb.kernel_count(32768, 16, 2, 32, "b200", defer=True, maxdwell=2048) == 1 + 7 * 5 + 2
-    assert mb.kernel_count(32768, 16, 2, 32, "b200", defer=True, maxdwell=256) == 1 + 7 * 3 + 1  # cap >= maxdwell
-    assert mb.kernel_count(32768, 16, 2, 32, "sbr", defer=True, maxdwell=2048) == 1 + 7 * 1 + 1  # B200 only
-    assert mb.kernel_count(32768, 16, 2, 32, "flow") == 4              # init, clear, flow init, flow
 
 
 @pytest.mark.parametrize("n,g,r,B", [(1000, 4, 2, 32), (1024, 3, 2, 32), (1024, 4, 1, 32),
@@ -153,8 +147,8 @@ def test_validation_before_any_launch(lib):
     assert lib.mandel_ask_tiles(*args, None, 0, 7, 0, fake, 64, fake, ws_need, None) == 1
     assert lib.mandel_ask_tiles(*args, None, 0, 1, 64, fake, 64, fake, ws_need, None) == 1       # unknown flag bit
     assert lib.mandel_ask_tiles(*args, None, 0, 1, 1 << 28, fake, 64, fake, ws_need, None) == 1
-    assert _lib.flag_defer(True) == 32 and _lib.flag_defer(False) == 0
-    assert _lib.flag_defer(512) == 32 | (32 << 16)
+    assert lib.mandel_ask_tiles(*args, None, 0, 3, 0, fake, 64, fake, ws_need, None) == 1        # no scheme 3
+    assert lib.mandel_ask_tiles(*args, None, 0, 1, 32, fake, 64, fake, ws_need, None) == 1       # no flag 32
     # more than 8 groups (MANDEL_FLAG_GROUPS bits 8-11 hold G-1)
     assert lib.mandel_ask_tiles(*args, None, 0, 1, 8 << 8, fake, 64, fake, ws_need, None) == 1
     assert _lib.flag_groups(1) == 0 and _lib.flag_groups(8) == 7 << 8

@@ -11,7 +11,7 @@ import workloads as W
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-SCHEMES = ("b200", "sbr", "mbr", "flow")
+SCHEMES = ("b200", "sbr", "mbr")
 
 
 @pytest.fixture(scope="module")
@@ -42,12 +42,21 @@ def _cmp_stats(gpu, orc, scheme):
 
 
 # ----------------------------------------------------------------------------- exhaustive
+@pytest.mark.parametrize("tuned", [False, True])
 @pytest.mark.parametrize("w", [W.C1] + list(W.random_small_workloads(12, seed=W.SEED + 11, max_n=512)),
                          ids=lambda w: w.name)
-def test_exhaustive_parity(mb, w):
-    out = mb.exhaustive(w.region, w.n, w.maxdwell)
+def test_exhaustive_parity(mb, w, tuned):
+    out = mb.exhaustive(w.region, w.n, w.maxdwell, tuned=tuned)
     E = oracle.exhaustive(w.region, w.n, w.maxdwell)
     assert np.array_equal(out.cpu().numpy(), E)
+
+
+@pytest.mark.parametrize("tuned", [False, True])
+@pytest.mark.parametrize("region", W.NONDYADIC_REGIONS)
+def test_exhaustive_non_dyadic(mb, region, tuned):
+    """Non-dyadic windows: the rounded pixel-centre mapping (R3) is bit-identical."""
+    n, md = 512, 1200
+    assert np.array_equal(mb.exhaustive(region, n, md, tuned=tuned).cpu().numpy(), oracle.exhaustive(region, n, md))
 
 
 def test_exhaustive_pitched(mb):
@@ -94,6 +103,9 @@ def test_ask_random_small(mb, w, scheme):
     (256, 4, 2, 8, 64, W.INTERIOR_REGION),      # closed form: all maxdwell
     (256, 4, 2, 8, 64, W.ESCAPE_REGION),        # closed form: all 1
     (2048, 8, 2, 16, 3000, (-0.75, -0.5, 0.0, 0.25)),  # maxdwell not a multiple of the chunk
+    (1024, 8, 2, 16, 2000, W.NONDYADIC_REGIONS[0]),    # non-dyadic windows: rounded
+    (512, 4, 4, 8, 700, W.NONDYADIC_REGIONS[1]),       # pixel centres, op order decides bits
+    (256, 2, 2, 4, 1500, W.NONDYADIC_REGIONS[2]),      # non-square window (dx != dy)
 ])
 def test_ask_edge_cases(mb, scheme, n, g, r, B, md, region):
     ws = mb.workspace(n, g, r, B)
@@ -140,14 +152,48 @@ def test_ask_equals_lookup_of_gpu_exhaustive(mb):
 def test_repeat_calls_reuse_graph_and_are_deterministic(mb):
     w = W.C1
     ws = mb.workspace(w.n, w.g, w.r, w.B)
-    a = mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, ws=ws).clone()
+    out = torch.empty((w.n, w.n), dtype=torch.int32, device="cuda")
+    a = mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws).clone()
+    c0 = mb.graph_captures()
     for _ in range(3):
-        b = mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, ws=ws)
+        b = mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws)
         assert torch.equal(a, b)
-    # a different region through the same workspace/output (new graph) still matches
-    b = mb.ask(W.SEAHORSE_REGION, w.n, w.maxdwell, w.g, w.r, w.B, ws=ws)
+    # a different region through the same workspace/output: same graph, oracle's image
+    b = mb.ask(W.SEAHORSE_REGION, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws)
     A, _ = oracle.ask(W.SEAHORSE_REGION, w.n, w.maxdwell, w.g, w.r, w.B)
     assert np.array_equal(b.cpu().numpy(), A)
+    assert mb.graph_captures() == c0
+
+
+def test_one_graph_serves_views_maxdwell_and_tile_lists(mb):
+    """Device-side parameter block: three different views,
+    maxdwell values and tile lists of the same size run through ONE captured graph, each
+    bit-exact against the oracle; the first call's capture + instantiate cost is reported."""
+    import time
+    n, g, r, B = 512, 8, 2, 8
+    ws = mb.workspace(n, g, r, B)
+    out = torch.empty((n, n), dtype=torch.int32, device="cuda")
+    rng = np.random.default_rng(W.SEED + 77)
+    cases = [(W.SEAHORSE_REGION, 900), ((-0.74531, -0.74419, 0.11273, 0.11385), 1500),
+             (W.DEFAULT_REGION, 300)]
+    c0 = mb.graph_captures()
+    times = []
+    for i, (region, md) in enumerate(cases):
+        tiles = rng.permutation(g * g)[:21].tolist()
+        out.fill_(-9)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        mb.ask(region, n, md, g, r, B, out=out, ws=ws, tiles=tiles)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+        A, _ = oracle.ask(region, n, md, g, r, B, tiles=tiles)
+        got = out.cpu().numpy()
+        mine = A != -1
+        assert np.array_equal(got[mine], A[mine]), i
+        assert np.all(got[~mine] == -9), i
+        assert mb.graph_captures() == c0 + 1, i   # captured by the first call only
+    print(f"first call (capture + instantiate + run) {1e3 * times[0]:.2f} ms, "
+          f"later calls {1e3 * times[1]:.2f} / {1e3 * times[2]:.2f} ms")
 
 
 def test_ask_to_host(mb):
@@ -212,7 +258,12 @@ def test_full_size_ask_sampled_tiles(mb, wname):
 @pytest.mark.parametrize("wname", ["C3", "C5", "C4"])
 def test_full_size_exhaustive_sampled_pixels(mb, wname):
     w = W.CONFIGS[wname]
-    out = mb.exhaustive(w.region, w.n, w.maxdwell)
+    out = mb.exhaustive(w.region, w.n, w.maxdwell, tuned=True)
+    # the tuned kernel's image equals the plain one's on every pixel
+    plain = mb.exhaustive(w.region, w.n, w.maxdwell)
+    torch.cuda.synchronize()
+    assert torch.equal(out, plain)
+    del plain
     rng = np.random.default_rng(W.SEED)
     ii = rng.integers(0, w.n, 4000)
     jj = rng.integers(0, w.n, 4000)
@@ -236,6 +287,8 @@ def test_ask_maxdwell_not_multiple_of_chunk(mb, md):
         assert np.array_equal(out.cpu().numpy(), A), (region, md)
         ex = mb.exhaustive(region, n, md).cpu().numpy()
         assert np.array_equal(ex, oracle.exhaustive(region, n, md)), (region, md)
+        ext = mb.exhaustive(region, n, md, tuned=True).cpu().numpy()
+        assert np.array_equal(ext, ex), (region, md)
 
 
 def test_ask_large_region_outside_radius(mb):
@@ -317,93 +370,6 @@ def test_dp_full_size_c3_equals_ask(mb):
     assert np.array_equal(d[gy * d0:(gy + 1) * d0, gx * d0:(gx + 1) * d0].cpu().numpy(), A)
 
 
-@pytest.mark.parametrize("wname", ["C3", "C5"])
-def test_flow_full_size_equals_b200(mb, wname):
-    """The dataflow scheme at full size: same image and same per-level statistics as the
-    level-synchronous B200 scheme (every decision is region-local)."""
-    w = W.CONFIGS[wname]
-    ws = mb.workspace(w.n, w.g, w.r, w.B)
-    a = mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, ws=ws, stats=True)
-    sa = mb.ask_stats(ws)
-    f = mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, ws=ws, scheme="flow", stats=True)
-    sf = mb.ask_stats(ws)
-    torch.cuda.synchronize()
-    assert torch.equal(a, f)
-    assert sa == sf
-
-
-# ----------------------------------------------------------------------------- deferred pixels
-def _decisions(stats):
-    return [{k: s[k] for k in ("regions_in", "filled", "subdivided", "leaves")} for s in _trim(stats)]
-
-
-@pytest.mark.parametrize("cap", [16, 48, 128])
-@pytest.mark.parametrize("w", list(W.random_small_workloads(20, seed=W.SEED + 41, max_n=512)),
-                         ids=lambda w: w.name)
-def test_defer_random_small(mb, w, cap):
-    """MANDEL_FLAG_DEFER: border pixels parked at `cap` iterations, regions
-    decided from partial rings, uncertain regions resolved first: same image and the same
-    decisions as the oracle's recursion."""
-    ws = mb.workspace(w.n, w.g, w.r, w.B)
-    out = mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, ws=ws, defer=cap)
-    A, st = oracle.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B)
-    assert np.array_equal(out.cpu().numpy(), A)
-    assert _decisions(mb.ask_stats(ws)) == _decisions(st)
-
-
-@pytest.mark.parametrize("n,g,r,B,md,region", [
-    (256, 2, 2, 2, 300, W.DEFAULT_REGION),
-    (512, 4, 8, 2, 500, W.SEAHORSE_REGION),
-    (1024, 2, 4, 32, 700, W.DEFAULT_REGION),
-    (256, 128, 2, 2, 100, W.DEFAULT_REGION),
-    (512, 1, 2, 4, 1000, W.SEAHORSE_REGION),
-    (256, 4, 2, 8, 64, W.INTERIOR_REGION),      # every ring unresolved: all regions uncertain
-    (256, 4, 2, 8, 64, W.ESCAPE_REGION),        # nothing deferred
-    (2048, 8, 2, 16, 3000, (-0.75, -0.5, 0.0, 0.25)),
-    (256, 2, 2, 8, 700, (-2.25, -1.75, -0.25, 0.25)),  # |c| ~ 2: per-step pixels beside deferred ones
-])
-def test_defer_edge_cases(mb, n, g, r, B, md, region):
-    ws = mb.workspace(n, g, r, B)
-    out = mb.ask(region, n, md, g, r, B, ws=ws, defer=16)
-    A, st = oracle.ask(region, n, md, g, r, B)
-    assert np.array_equal(out.cpu().numpy(), A)
-    got = mb.ask_stats(ws)
-    assert _decisions(got) == _decisions(st)
-    if region == W.INTERIOR_REGION:
-        assert got[0]["uncertain"] == g * g and sum(s["deferred"] for s in got) > 0
-
-
-def test_defer_pool_overflow(mb):
-    """More pixels reach the cap than the pool holds (65536 entries at n <= 2048): the rest
-    are computed to the end in place; the image is unchanged."""
-    n, g, r, B, md = 2048, 4, 2, 16, 2000
-    region = W.SEAHORSE_REGION
-    ws = mb.workspace(n, g, r, B)
-    out = mb.ask(region, n, md, g, r, B, ws=ws, defer=16)
-    st = mb.ask_stats(ws)
-    assert sum(s["deferred"] for s in st) > 65536
-    A, _ = oracle.ask(region, n, md, g, r, B)
-    assert np.array_equal(out.cpu().numpy(), A)
-
-
-@pytest.mark.parametrize("wname", ["C3", "C5", "C4"])
-def test_defer_full_size_equals_plain(mb, wname):
-    """Full BASELINE sizes: the deferred scheme's image equals the plain B200 scheme's on every
-    pixel (and so the oracle wherever test_full_size_ask_sampled_tiles checks it), with the
-    same per-level decisions."""
-    w = W.CONFIGS[wname]
-    ws = mb.workspace(w.n, w.g, w.r, w.B)
-    a = mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, ws=ws, defer=False)
-    sa = _decisions(mb.ask_stats(ws))
-    b = mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, ws=ws, defer=True)
-    sb = mb.ask_stats(ws)
-    torch.cuda.synchronize()
-    assert torch.equal(a, b)
-    assert _decisions(sb) == sa
-    assert sum(s["deferred"] for s in sb) > 0
-    del a, b
-
-
 # ----------------------------------------------------------------------------- tile costs
 @pytest.mark.parametrize("n,g,r,B,md,region", [
     (256, 4, 2, 8, 500, W.DEFAULT_REGION),
@@ -476,6 +442,7 @@ def test_large_maxdwell(mb, md):
         out = mb.ask(W.INTERIOR_REGION, n, md, g, r, B, scheme=scheme).cpu().numpy()
         assert np.all(out == md), scheme
     assert np.all(mb.exhaustive(W.INTERIOR_REGION, n, md).cpu().numpy() == md)
+    assert np.all(mb.exhaustive(W.INTERIOR_REGION, n, md, tuned=True).cpu().numpy() == md)
     region = (-0.75, -0.734375, 0.09375, 0.109375)  # seahorse boundary, dyadic
     A, _ = oracle.ask(region, 16, md, 2, 2, 4)
     assert np.array_equal(mb.ask(region, 16, md, 2, 2, 4).cpu().numpy(), A)

@@ -138,3 +138,20 @@ def test_ask3_vs_exhaustive_mismatch_is_small():
     A, _ = oracle.ask3(W.DEFAULT_REGION3, n, md, 2, 2, 4)
     frac = float((A != E).mean())
     assert frac < 1e-2  # the heuristic may differ where a thin feature slips between surfaces
+
+
+@pytest.mark.parametrize("n,g,r,B,md", [(32, 2, 2, 4, 200), (64, 4, 2, 2, 100), (32, 2, 4, 2, 64)])
+def test_ask3_tile_equals_whole_volume(n, g, r, B, md):
+    """oracle.ask3_tile (level-0 cube at a non-zero origin (ox, oy, oz)) equals the matching
+    block of the whole-volume recursion and of the independent numpy recursion."""
+    region = W.DEFAULT_REGION3
+    A, _ = oracle.ask3(region, n, md, g, r, B)
+    E = oracle.exhaustive3(region, n, md)
+    Np, _ = _ask3_numpy(E, g, r, B)
+    d0 = n // g
+    for t in range(g ** 3):
+        gx, gy, gz = t % g, (t // g) % g, t // (g * g)
+        img, _ = oracle.ask3_tile(region, n, md, g, r, B, t)
+        sl = (slice(gz * d0, (gz + 1) * d0), slice(gy * d0, (gy + 1) * d0), slice(gx * d0, (gx + 1) * d0))
+        assert np.array_equal(img, A[sl]), t
+        assert np.array_equal(img, Np[sl]), t

@@ -337,3 +337,54 @@ def test_ask_mismatch_small_but_nonzero_possible():
     E = oracle.exhaustive(w.region, w.n, w.maxdwell)
     A, _ = oracle.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B)
     assert (A != E).mean() < 1e-3
+
+
+# ----------------------------------------------------------------------------- windowed tiles
+@pytest.mark.parametrize("w", [W.Workload("t1", W.SEAHORSE_REGION, 256, 700, 4, 2, 8),
+                               W.Workload("t2", W.NONDYADIC_REGIONS[0], 128, 900, 8, 4, 2),
+                               W.Workload("t3", W.NONDYADIC_REGIONS[1], 256, 300, 2, 2, 16),
+                               W.Workload("t4", W.NONDYADIC_REGIONS[2], 64, 1000, 4, 8, 2)],
+                         ids=lambda w: w.name)
+def test_ask_tile_equals_whole_image_and_bruteforce(w):
+    """oracle.ask_tile (the windowed path every full-size check uses, level-0 tile at origin
+    (ox, oy) != 0) equals the matching slice of the whole-image recursion AND of the
+    independent level-wise Python recursion over the exhaustive image; its statistics sum to
+    the whole image's."""
+    E = oracle.exhaustive(w.region, w.n, w.maxdwell)
+    A, st = oracle.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B)
+    Bf = _ask_levelwise_python(E, w.g, w.r, w.B)
+    d0 = w.n // w.g
+    tot = {}
+    for t in range(w.g * w.g):
+        gy, gx = divmod(t, w.g)
+        img, s = oracle.ask_tile(w.region, w.n, w.maxdwell, w.g, w.r, w.B, t)
+        sl = (slice(gy * d0, (gy + 1) * d0), slice(gx * d0, (gx + 1) * d0))
+        assert np.array_equal(img, A[sl]), t
+        assert np.array_equal(img, Bf[sl]), t
+        for lv in s:
+            for k, v in lv.items():
+                if k != "level":
+                    tot[(lv["level"], k)] = tot.get((lv["level"], k), 0) + v
+    for lv in st:
+        for k, v in lv.items():
+            if k != "level":
+                assert tot[(lv["level"], k)] == v, (lv["level"], k)
+
+
+@pytest.mark.parametrize("region", W.NONDYADIC_REGIONS)
+def test_pixel_mapping_non_dyadic_error_bound(region):
+    """Non-dyadic windows (an arbitrary window): every pixel centre is within a few
+    float32 ulps of the exact centre re_min + (j + 1/2)(re_max - re_min)/n (four rounded
+    operations, R3), and the centres are strictly increasing in j and i."""
+    n = 64
+    prev_r = prev_i = -math.inf
+    for k in range(n):
+        cr, ci = oracle.pixel_c(region, n, k, k)
+        exact_r = region[0] + (k + 0.5) * (region[1] - region[0]) / n
+        exact_i = region[2] + (k + 0.5) * (region[3] - region[2]) / n
+        for got, ex, span in ((cr, exact_r, abs(region[0]) + abs(region[1])),
+                              (ci, exact_i, abs(region[2]) + abs(region[3]))):
+            ulp = np.spacing(np.float32(max(abs(ex), span)))
+            assert abs(got - ex) <= 4 * float(ulp), (k, got, ex)
+        assert cr > prev_r and ci > prev_i
+        prev_r, prev_i = cr, ci

@@ -17,7 +17,7 @@ import torch
 import paper_2206_02255_b200 as mb
 import workloads as W
 
-VARIANTS = {"b200": dict(scheme="b200"), "flow": dict(scheme="flow"), "flat": dict(scheme="b200", flat=True), "sbr": dict(scheme="sbr"), "mbr": dict(scheme="mbr"),
+VARIANTS = {"b200": dict(scheme="b200"), "flat": dict(scheme="b200", flat=True), "sbr": dict(scheme="sbr"), "mbr": dict(scheme="mbr"),
             "serial": dict(scheme="b200", serial=True), "mbr_serial": dict(scheme="mbr", serial=True),
             "g2": dict(scheme="b200", groups=2), "g4": dict(scheme="b200", groups=4),
             "g8": dict(scheme="b200", groups=8), "g1": dict(scheme="b200", groups=1)}
@@ -58,8 +58,7 @@ def main():
                     ts.append(s.elapsed_time(e))
                 res[v] = {"ms_mean": sum(ts) / len(ts), "ms_min": min(ts), "same_image": same}
                 continue
-            # dNNN: MANDEL_FLAG_DEFER with an iteration cap of NNN
-            kw = dict(scheme="b200", defer=int(v[1:])) if v[0] == "d" and v[1:].isdigit() else VARIANTS[v]
+            kw = VARIANTS[v]
             mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, stats=True, **kw)
             st = mb.ask_stats(ws)
             iters = sum(x["border_iters"] + x["leaf_iters"] for x in st)

@@ -25,12 +25,11 @@ from paper_2206_02255_b200 import deal  # noqa: E402
 
 GROUPS = None
 SCHEME = "b200"
-DEFER = None
 
 
 def time_tiles(w, out, ws, tiles, flush, reps):
     f = lambda: mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, tiles=tiles,  # noqa: E731
-                       groups=GROUPS, scheme=SCHEME, defer=DEFER)
+                       groups=GROUPS, scheme=SCHEME)
     f()
     torch.cuda.synchronize()
     ts = []
@@ -53,13 +52,11 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--groups", type=int, default=None)
     ap.add_argument("--scheme", default="b200")
-    ap.add_argument("--defer", type=int, default=None, help="MANDEL_FLAG_DEFER cap (0: off)")
     ap.add_argument("--preview", default="8,2", help="preview shrink,dwell_shrink")
     a = ap.parse_args()
-    global GROUPS, SCHEME, DEFER
+    global GROUPS, SCHEME
     GROUPS = a.groups
     SCHEME = a.scheme
-    DEFER = a.defer
     w = W.CONFIGS[a.workload]
     out = torch.empty((w.n, w.n), dtype=torch.int32, device="cuda")
     ws = mb.workspace(w.n, w.g, w.r, w.B)
@@ -77,7 +74,7 @@ def main():
     mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, tile_cost=True)
     exact = mb.tile_costs(ws, w.g)
     t1 = time_tiles(w, out, ws, None, flush, a.reps)
-    res = {"workload": w.name, "preview": a.preview, "scheme": SCHEME, "groups": GROUPS, "defer": DEFER, "t1_ms": t1, "preview_ms": preview_ms, "deals": {}}
+    res = {"workload": w.name, "preview": a.preview, "scheme": SCHEME, "groups": GROUPS, "t1_ms": t1, "preview_ms": preview_ms, "deals": {}}
     for dname in a.deals.split(","):
         for P in [int(x) for x in a.ranks.split(",")]:
             # "<deal>_exact": dealt on the exact per-tile costs (the estimator's upper bound)
@@ -96,10 +93,10 @@ def main():
     heavy = max(parts, key=lambda p: sum(exact[k] for k in p))
     for _ in range(2):
         mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, tiles=heavy, timing=True, groups=GROUPS,
-               scheme=SCHEME, defer=DEFER)
+               scheme=SCHEME)
     torch.cuda.synchronize()
     res["heavy_rank_kernels"] = [dict(k) for k in mb.kernel_times()]
-    mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, timing=True, scheme=SCHEME, defer=DEFER)
+    mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, timing=True, scheme=SCHEME)
     torch.cuda.synchronize()
     res["full_kernels"] = [dict(k) for k in mb.kernel_times()]
     print(json.dumps(res), flush=True)

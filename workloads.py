@@ -29,6 +29,13 @@ SEAHORSE_REGION: Region = (-0.765625, -0.734375, 0.09375, 0.125)
 # Closed-form pin windows (SURVEY.md §8(c) "tiny-grid agreement"):
 INTERIOR_REGION: Region = (-0.25, 0.125, -0.25, 0.125)  # inside the main cardioid
 ESCAPE_REGION: Region = (2.5, 3.5, 2.5, 3.5)  # |c| > 2 everywhere: dwell 1
+# Non-dyadic windows (P:432 takes an arbitrary window of the complex plane): their corners
+# and pixel pitch are not exact binary fractions, so every pixel centre is rounded.
+NONDYADIC_REGIONS: Tuple[Region, ...] = (
+    (-0.74531, -0.74419, 0.11273, 0.11385),        # seahorse-valley detail
+    (-1.2345678, -0.3456789, 0.0123457, 0.9012345),  # a generic window across the boundary
+    (-0.1, 0.3, 0.6, 0.7),                          # non-square: dx != dy
+)
 
 
 @dataclasses.dataclass(frozen=True)
@@ -82,14 +89,15 @@ def random_small_workloads(count: int, seed: int = SEED, max_n: int = 512,
                            regions: Optional[Sequence[Region]] = None) -> Iterator[Workload]:
     """Seeded random small cases: powers of two with g*B <= n, r >= 2, B >= 2.
 
-    Regions are drawn from dyadic sub-windows of the default region so the pixel
-    centres are exact in FP32 (R3), plus the named windows.
+    Regions are drawn from dyadic sub-windows of the default region (pixel centres exact in
+    FP32), the named windows, and NON-dyadic windows (NONDYADIC_REGIONS), where the pixel
+    mapping of DESIGN.md R3 rounds and its operation order decides the bits.
     """
     rng = random.Random(seed)
     if regions is None:
         regions = [DEFAULT_REGION, SEAHORSE_REGION,
                    (-1.0, 0.0, 0.0, 1.0), (-0.875, -0.625, 0.0, 0.25),
-                   (-1.5, -1.25, -0.125, 0.125), (0.25, 0.5, -0.125, 0.125)]
+                   (-1.5, -1.25, -0.125, 0.125), (0.25, 0.5, -0.125, 0.125)] + list(NONDYADIC_REGIONS)
     k = 0
     while k < count:
         n = rng.choice(_pow2s(8, max_n))
