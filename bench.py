@@ -10,10 +10,11 @@ output image (4 GiB at n = 32768) is far larger than L2 and every step rewrites 
 it; an explicit 256 MiB L2 flush also runs between timed steps, outside the per-step events.
 
 N > 1: one process per GPU (torchrun), NCCL process group; level-0 tiles are dealt
-longest-first (LPT, paper_2206_02255_b200.deal) on costs from a preview run every rank computes
-redundantly before the timed steps (a per-region plan, reused by every step of the same view);
-its warm wall time is reported as preview_ms and folded into value_incl_preview; no data-path
-collective; the time is the max over ranks of the device time.
+longest-first (LPT) on the device: every timed step renders the rank's tiles with per-tile cost
+counters, all-reduces the g*g counters and computes the next step's deal (mandel_deal_lpt), so
+the plan is charged to every step; the first, untimed step is dealt on an n/32, maxdwell/8
+preview.  No collective touches the image on the data path; the time is the max over ranks of
+the device time.
 MANDEL_DIST_BACKEND=gloo (test only): gloo process group with CPU-side collectives and every
 rank on cuda:(LOCAL_RANK mod device count), so the N > 1 control flow can be exercised on a
 one-GPU box (ranks then share the GPU: the times are not scaling numbers).
@@ -165,10 +166,11 @@ def _config(w: W.Workload, args, world: int):
     return {"workload": f"{w.name}: Mandelbrot n={w.n} maxdwell={w.maxdwell} region={list(w.region)} "
                         f"ASK g={w.g} r={w.r} B={w.B}",
             "n": w.n, "maxdwell": w.maxdwell, "g": w.g, "r": w.r, "B": w.B, "region": list(w.region),
-            "scheme": args.scheme, "deal": args.deal if world > 1 else "all tiles",
-            "deal_plan": ("per-tile costs from an n/8, maxdwell/2 preview ASK, computed once per view before "
-                          "the timed steps (preview_ms; value_incl_preview charges it to one step)")
-            if world > 1 and args.deal in ("lpt", "costrank") else None,
+            "scheme": args.scheme, "deal": "lpt (device)" if world > 1 else "all tiles",
+            "deal_plan": ("charged to every timed step: per-tile cost counters of this step's render, "
+                          "NCCL all-reduce of the g*g counters, device LPT deal (mandel_deal_lpt) for the next "
+                          "step; the first, untimed step is dealt on an n/32, maxdwell/8 preview")
+            if world > 1 else None,
             "parallelism": f"tiles{world}",
             "l2": "output image 4*n^2 B >> 126 MB L2, rewritten every step; plus a 256 MiB L2 flush "
                   "between timed steps outside the per-step events"}
@@ -182,7 +184,6 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="C3", choices=sorted(W.CONFIGS))
     ap.add_argument("--scheme", default="b200", choices=["b200", "sbr", "mbr"])
-    ap.add_argument("--deal", default="lpt", choices=["lpt", "costrank", "cyclic", "diagonal"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -201,7 +202,6 @@ def main():
     import torch.distributed as dist
 
     import paper_2206_02255_b200 as mb
-    from paper_2206_02255_b200 import deal as deal_mod
     from paper_2206_02255_b200 import multigpu
 
     backend = os.environ.get("MANDEL_DIST_BACKEND", "nccl")
@@ -220,31 +220,40 @@ def main():
     w = W.CONFIGS[args.workload]
     n = w.n
 
-    # ---- partition (untimed planning is re-timed below as preview_ms)
-    preview_ms = 0.0
-    parts = [list(range(w.g * w.g))]
-    if world > 1:
-        if args.deal in ("costrank", "lpt"):
-            costs = mb.preview_costs(w.region, n, w.maxdwell, w.g, w.r, w.B)  # cold: captures its graph
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            costs = mb.preview_costs(w.region, n, w.maxdwell, w.g, w.r, w.B)
-            parts = deal_mod.deal(args.deal, w.g, world, costs)
-            torch.cuda.synchronize()
-            preview_ms = 1e3 * (time.perf_counter() - t0)
-        else:
-            parts = deal_mod.deal(args.deal, w.g, world)
-        tiles = parts[rank]
-    else:
-        tiles = None
-    ntiles = w.g * w.g if tiles is None else len(tiles)
-
+    # ---- partition.  N > 1: a device-resident LPT deal of the level-0 tiles
+    # (multigpu.DevicePlan).  Every timed step renders this rank's tiles with per-tile cost
+    # counters on, all-reduces the g*g counters across ranks and re-deals for the next step on
+    # the device (mandel_deal_lpt) -- all inside the step's events, so the plan is charged to
+    # every step.  The first (untimed) step is dealt on an n/32, maxdwell/8 preview.
     out = torch.empty((n, n), dtype=torch.int32, device=dev)
     ws = mb.workspace(n, w.g, w.r, w.B, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    plan = None
+    if world > 1:
+        plan = multigpu.DevicePlan(w, world, rank, dev)
+        costs0 = torch.zeros(w.g * w.g, dtype=torch.int64, device=dev)
+        plan.preview_costs(costs0)
+        plan.deal(costs0)
+        cview = mb.tile_cost_view(ws, n, w.g, w.r, w.B)
+
+    def allreduce_costs():
+        if backend == "nccl":
+            dist.all_reduce(cview, op=dist.ReduceOp.SUM)
+        else:  # gloo test mode: host-side collective
+            h = cview.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.SUM)
+            cview.copy_(h)
 
     # ---- per-kernel algorithmic work from one untimed counter pass (deterministic)
-    mb.ask(w.region, n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, tiles=tiles, scheme=args.scheme, stats=True)
+    if plan is None:
+        mb.ask(w.region, n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, scheme=args.scheme, stats=True)
+    else:  # converge the deal first (the timed steps run the steady state), then count
+        for _ in range(2):
+            plan.render(out, ws, tile_cost=True)
+            allreduce_costs()
+            plan.deal(cview)
+        mb.ask(w.region, n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, dtiles=(plan.tiles, plan.count),
+               scheme=args.scheme, stats=True)
     lstats = mb.ask_stats(ws)
     border_iters = sum(s["border_iters"] for s in lstats)
     leaf_iters = sum(s["leaf_iters"] for s in lstats)
@@ -255,13 +264,17 @@ def main():
     # chain's programmatic-dependent-launch edges.  The full per-kernel breakdown comes from
     # separate calls after the timed region.
     def step(timing="leaf"):
-        mb.ask(w.region, n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, tiles=tiles, scheme=args.scheme,
-               timing=timing)
+        if plan is None:
+            mb.ask(w.region, n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, scheme=args.scheme, timing=timing)
+        else:
+            plan.render(out, ws, tile_cost=True, timing=timing)
+            allreduce_costs()
+            plan.deal(cview)
 
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
-    kernels_per_step = mb.kernel_count(n, w.g, w.r, w.B, args.scheme)
+    kernels_per_step = mb.kernel_count(n, w.g, w.r, w.B, args.scheme) + (1 if plan is not None else 0)
 
     stream = torch.cuda.current_stream()
     step_ms, ktime = [], {}
@@ -292,7 +305,8 @@ def main():
     my_total = sum(step_ms)
     total_ms = multigpu.max_over_ranks(my_total, device=cdev)
     exec_iters_all = multigpu.sum_over_ranks([float(exec_iters)], device=cdev)[0]
-    preview_ms = multigpu.max_over_ranks(preview_ms, device=cdev)
+    tiles = plan.host_tiles() if plan is not None else None  # the deal of the last timed step
+    ntiles = w.g * w.g if tiles is None else len(tiles)
 
     # ---- verification gather to rank 0 (N > 1 only; timed separately, not part of `value`)
     gather = None
@@ -300,6 +314,9 @@ def main():
         torch.cuda.synchronize()
         dist.barrier()
         t0 = time.perf_counter()
+        mb.ask(w.region, n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, tiles=tiles, scheme=args.scheme)
+        parts = [None] * world
+        dist.all_gather_object(parts, tiles)
         full = multigpu.gather_image(out if backend == "nccl" else out.cpu(), parts, w.g, rank)
         torch.cuda.synchronize()
         g_ms = 1e3 * (time.perf_counter() - t0)
@@ -444,8 +461,7 @@ def main():
             "exhaustive_tuned_giter_s": extra.get("exhaustive_tuned_giter_s"),
             "mismatch_fraction_vs_exhaustive": extra.get("mismatch_fraction_vs_exhaustive"),
             "executed_iters_per_step": exec_iters_all,
-            "preview_ms": preview_ms,
-            "value_incl_preview": n * n / ((ms_per_step + preview_ms) / 1e3) / 1e6 if world > 1 else None,
+            "rank_tiles": ntiles,
             "verify_gather": gather,
             "kernel_ms_per_step": kt_all,
             "clocks": clocks, "e2e": e2e,

@@ -176,6 +176,34 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
                      uint32_t flags, int32_t *d_out, int64_t out_pitch, void *d_ws,
                      size_t ws_bytes, void *stream);
 
+/* mandel_ask_tiles with the tile list in DEVICE memory: d_tile_ids (>= g*g int32 entries) and
+ * its length *d_n_tiles (int32) are read when the call executes on `stream`, not when it is
+ * enqueued -- the captured graph copies them into the workspace's parameter block itself -- so a
+ * preceding kernel on the stream (mandel_deal_lpt) can choose the tiles and no host round trip is
+ * needed between the multi-GPU deal and the rank's ASK.  The graph is keyed on the two pointers,
+ * not on the count.  Ids must be unique and in [0, g*g) (not checked on the device).
+ * MANDEL_FLAG_GROUPS must be 1; g*g <= 4096. */
+int mandel_ask_dtiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, int32_t r,
+                      int32_t B, const int32_t *d_tile_ids, const int32_t *d_n_tiles, int32_t scheme,
+                      uint32_t flags, int32_t *d_out, int64_t out_pitch, void *d_ws, size_t ws_bytes,
+                      void *stream);
+
+/* The multi-GPU partition (north_star "initial g x g regions dealt across
+ * ranks"; P:366 the level-0 grid |G_0|), on the device: Graham's longest-processing-time list
+ * schedule of n_tiles level-0 tiles over `world` ranks on the per-tile costs d_costs (u64,
+ * canonical tile order): tiles in descending cost (ties: lower id), each to the least-loaded rank
+ * (ties: lower rank).  Writes rank `rank`'s tiles, in that descending order, to d_tile_ids and
+ * their number to *d_n_tiles (device memory), asynchronously on `stream`.  Deterministic: every
+ * rank computing it on the same costs gets a consistent partition.  n_tiles <= 4096,
+ * world <= 64. */
+int mandel_deal_lpt(const uint64_t *d_costs, int32_t n_tiles, int32_t world, int32_t rank,
+                    int32_t *d_tile_ids, int32_t *d_n_tiles, void *stream);
+
+/* Byte offset, inside a workspace of these parameters, of the per-tile executed-iteration
+ * counters (u64[g*g], canonical order) that MANDEL_FLAG_TILE_COST fills; lets the caller reduce
+ * them across ranks in place (e.g. NCCL all-reduce) and feed mandel_deal_lpt.  0 if invalid. */
+size_t mandel_ask_tile_costs_offset(int64_t n, int32_t g, int32_t r, int32_t B);
+
 /* End-to-end variant over HOST memory: runs mandel_ask_tiles into the device buffer d_out
  * and copies the n x n image (rows of n elements) into h_out (host; pinned for full
  * bandwidth), then synchronises `stream`.  For tile runs only the tiles' pixels are

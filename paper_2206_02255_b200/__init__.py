@@ -122,7 +122,7 @@ def dp(region: Sequence[float], n: int, maxdwell: int, g: int, r: int, B: int, o
 def ask(region: Sequence[float], n: int, maxdwell: int, g: int, r: int, B: int, out=None, ws=None,
         tiles: Optional[Sequence[int]] = None, scheme: str = "b200", stats: bool = False,
         timing: bool = False, tile_cost: bool = False, flat: bool = False, serial: bool = False,
-        groups: Optional[int] = None, stream=None):
+        groups: Optional[int] = None, stream=None, dtiles=None):
     """ASK dwell image over all g*g level-0 regions, or only `tiles`.
     stats: accumulate per-level counters (ask_stats); timing: per-kernel events
     (kernel_times; "leaf": around the leaf kernel only, which keeps the level chain's
@@ -143,11 +143,40 @@ def ask(region: Sequence[float], n: int, maxdwell: int, g: int, r: int, B: int, 
              | (_lib.FLAG_SERIAL if serial else 0)
              | _lib.flag_groups(DEFAULT_GROUPS if groups is None else groups))
     with _torch().cuda.device(out.device):
-        rc = _lib.load().mandel_ask_tiles(_lib.region(region), n, maxdwell, g, r, B, t_ptr, t_n,
-                                          SCHEMES[scheme], flags, out.data_ptr(), out.stride(0),
-                                          ws.data_ptr(), ws.numel(), _stream_ptr(stream))
-    _lib.check(rc, "mandel_ask_tiles")
+        if dtiles is not None:
+            rc = _lib.load().mandel_ask_dtiles(_lib.region(region), n, maxdwell, g, r, B, dtiles[0].data_ptr(),
+                                               dtiles[1].data_ptr(), SCHEMES[scheme], flags, out.data_ptr(),
+                                               out.stride(0), ws.data_ptr(), ws.numel(), _stream_ptr(stream))
+        else:
+            rc = _lib.load().mandel_ask_tiles(_lib.region(region), n, maxdwell, g, r, B, t_ptr, t_n,
+                                              SCHEMES[scheme], flags, out.data_ptr(), out.stride(0),
+                                              ws.data_ptr(), ws.numel(), _stream_ptr(stream))
+    _lib.check(rc, "mandel_ask_dtiles" if dtiles is not None else "mandel_ask_tiles")
     return out
+
+
+def tile_cost_view(ws, n: int, g: int, r: int, B: int):
+    """The workspace's per-tile cost counters (MANDEL_FLAG_TILE_COST) as an int64 cuda tensor
+    of g*g entries, a view into ws (for an in-place all-reduce across ranks)."""
+    torch = _torch()
+    off = int(_lib.load().mandel_ask_tile_costs_offset(n, g, r, B))
+    if off == 0 or off % 8:
+        raise ValueError("invalid ASK parameters")
+    return ws[off:off + 8 * g * g].view(torch.int64)
+
+
+def deal_lpt(costs, world: int, rank: int, tiles_out, count_out, stream=None):
+    """Device-side LPT deal (mandel_deal_lpt): rank `rank`'s tiles of a `world`-way
+    longest-processing-time schedule on the int64 cuda tensor `costs` (g*g, canonical order),
+    written to the int32 cuda tensors tiles_out (>= g*g) and count_out (1), asynchronously."""
+    torch = _torch()
+    if costs.dtype != torch.int64 or tiles_out.dtype != torch.int32 or count_out.dtype != torch.int32:
+        raise ValueError("deal_lpt: int64 costs, int32 outputs")
+    _check_device(costs, tiles_out, count_out, stream=stream)
+    with torch.cuda.device(costs.device):
+        rc = _lib.load().mandel_deal_lpt(costs.data_ptr(), costs.numel(), world, rank, tiles_out.data_ptr(),
+                                         count_out.data_ptr(), _stream_ptr(stream))
+    _lib.check(rc, "mandel_deal_lpt")
 
 
 def ask_stats(ws, stream=None) -> List[dict]:

@@ -72,6 +72,12 @@ _SIGS = [
     ("mandel_ask_tiles", ctypes.c_int, [MandelRegion, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                         ctypes.c_int32, _P, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, _P,
                                         ctypes.c_int64, _P, ctypes.c_size_t, _P]),
+    ("mandel_ask_dtiles", ctypes.c_int, [MandelRegion, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                         ctypes.c_int32, _P, _P, ctypes.c_int32, ctypes.c_uint32, _P,
+                                         ctypes.c_int64, _P, ctypes.c_size_t, _P]),
+    ("mandel_deal_lpt", ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _P, _P, _P]),
+    ("mandel_ask_tile_costs_offset", ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                                       ctypes.c_int32]),
     ("mandel_ask_to_host", ctypes.c_int, [MandelRegion, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                           ctypes.c_int32, ctypes.c_int32, _P, ctypes.c_int32, ctypes.c_int32, _P,
                                           ctypes.c_int64, _P, ctypes.c_size_t, _P, _P]),

@@ -143,11 +143,13 @@ struct ExArgs {
 struct DevParams {
     PixMap map;       // pixel -> c of the call's region (dwell.cuh, R3)
     int32_t maxdwell; // >= 1
-    int32_t ntiles;   // level-0 tiles of the call (the graph is keyed on it)
     uint32_t magic;   // PRM_MAGIC
+    int32_t ntiles;   // level-0 tiles of the call (host lists: the graph is keyed on it; device
+                      // lists: copied from the caller's device counter by the graph itself)
     uint32_t pad;
     // followed at byte offset PRM_TILES by the call's tile list (int32, group-dealt order)
 };
+constexpr size_t PRM_HOST_BYTES_DTILES = 24; // host-written part for device tile lists
 constexpr uint32_t PRM_MAGIC = 0x4d505242u; // "BRPM"
 constexpr size_t PRM_TILES = 256;
 
@@ -163,7 +165,7 @@ struct LevelArgs {
     uint2 *fill;             // this level's fill segment
     uint32_t *leaf;
     const int32_t *tiles;    // k_init only: the group's tile list in the parameter block (NULL: canonical)
-    int level, d, r, B, g, ntiles, levels, scheme;
+    int level, d, r, B, g, ntiles, levels, scheme; // ntiles < 0: read prm->ntiles (device list)
     int subdivide;           // d / r >= B
     int log2_q4, log2_row4;  // fill: log2(d*d/4), log2(d/4)
     int fill_vec;            // SBR in-block fill: rows 16-byte aligned and d % 4 == 0
@@ -255,6 +257,8 @@ __device__ __forceinline__ LevelArgs with_params(LevelArgs a)
 {
     a.map = a.prm->map;
     a.maxdwell = a.prm->maxdwell;
+    if (a.ntiles < 0) // device tile list: its length was copied into the block by the graph
+        a.ntiles = a.prm->ntiles;
     return a;
 }
 
@@ -339,12 +343,67 @@ __global__ void __launch_bounds__(256) k_probe_fp32(float cr, float ci, int step
         sink[blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
 
+// --------------------------------------------------------------------------- multi-GPU deal
+// Graham's longest-processing-time list schedule of the level-0 tiles over `world` ranks
+// (the multi-GPU partition of SURVEY.md §8(e); same rule as paper_2206_02255_b200/deal.py
+// `lpt`): tiles in descending cost (ties: lower id first), each to the currently least-loaded
+// rank (ties: lower rank).  Every rank runs it on the same all-reduced cost vector, so all ranks
+// derive the same partition without further communication.  Writes rank `rank`'s tiles in that
+// descending order (its level-0 offset list order) and their count.  One block; G <= 4096.
+__global__ void __launch_bounds__(1024) k_deal_lpt(const unsigned long long *costs, int G, int world, int rank,
+                                                   int32_t *tiles_out, int32_t *ntiles_out)
+{
+    __shared__ unsigned long long key[4096];
+    __shared__ unsigned long long load[64];
+    int P = 1;
+    while (P < G)
+        P <<= 1;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        // descending cost, ascending id: sort keys (cost << 16 | (0xffff - id)) descending;
+        // padding entries sort last
+        key[i] = i < G ? ((costs[i] & 0xffffffffffffull) << 16) | (unsigned long long)(0xffff - i) : 0ull;
+    }
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1) // bitonic sort, descending
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < P; i += blockDim.x) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const bool desc = (i & k) == 0;
+                    const unsigned long long a = key[i], b = key[l];
+                    if (desc ? (a < b) : (a > b)) {
+                        key[i] = b;
+                        key[l] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < world; ++q)
+            load[q] = 0ull;
+        int n = 0;
+        for (int i = 0; i < G; ++i) {
+            const int id = 0xffff - (int)(key[i] & 0xffffull);
+            int best = 0;
+            for (int q = 1; q < world; ++q)
+                if (load[q] < load[best])
+                    best = q;
+            load[best] += costs[id];
+            if (best == rank)
+                tiles_out[n++] = id;
+        }
+        *ntiles_out = n;
+    }
+}
+
 // --------------------------------------------------------------------------- init
 // Level-0 offset list: the initial g x g split ("initial compute grid |G_0|"),
 // canonical order or the caller's tile subset; zero the counters.
-__global__ void k_init(LevelArgs a)
+__global__ void k_init(LevelArgs a_)
 {
     pdl_entry();
+    const LevelArgs a = with_params(a_);
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     constexpr int hdr_words = sizeof(WsHeader) / 4;
     uint32_t *hw = reinterpret_cast<uint32_t *>(a.hdr);

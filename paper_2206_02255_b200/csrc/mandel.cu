@@ -167,13 +167,14 @@ struct Key {
     int32_t *out;
     void *ws;
     size_t ws_bytes;
-    int32_t ntiles;
-    bool listed; // an explicit tile list (else canonical 0..g*g-1)
+    int32_t ntiles; // -1: device tile list (length read on the device)
+    bool listed;    // an explicit tile list (else canonical 0..g*g-1)
+    const void *dtiles, *dntiles; // device tile list and its length (mandel_ask_dtiles), else NULL
     bool operator==(const Key &o) const
     {
         return dev == o.dev && n == o.n && pitch == o.pitch && g == o.g && r == o.r && B == o.B &&
                scheme == o.scheme && flags == o.flags && out == o.out && ws == o.ws && ws_bytes == o.ws_bytes &&
-               ntiles == o.ntiles && listed == o.listed;
+               ntiles == o.ntiles && listed == o.listed && dtiles == o.dtiles && dntiles == o.dntiles;
     }
 };
 
@@ -324,8 +325,9 @@ int t_end(Timing *tm, int kind, int level, cudaStream_t st)
 struct Group {
     size_t hdr;               // byte offset of its header
     size_t unit0;             // level-0 tiles of the groups before it (slice offset unit)
-    int ntiles;
+    int ntiles;               // -1: device tile list, length in the parameter block
     const int32_t *tiles;     // device-visible tile ids (NULL: canonical 0..ntiles-1)
+    int cap_tiles;            // upper bound of ntiles (buffer slices, grid sizes)
 };
 
 // Enqueue one group's whole ASK chain on `s` (called under stream capture).
@@ -335,7 +337,7 @@ struct Group {
 int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, int sms, cudaStream_t s,
                 cudaStream_t s2, cudaEvent_t fork, Timing *tm)
 {
-    const int ntiles = grp.ntiles;
+    const int ntiles = grp.cap_tiles; // capacities and grid sizes (== grp.ntiles for host lists)
     const size_t Lm = (size_t)lay.L - 1;
     // (ASK-SBR has no fill kernels: nothing to overlap)
     const bool overlap = (k.flags & MANDEL_FLAG_SERIAL) == 0 && k.scheme != MANDEL_SCHEME_SBR;
@@ -353,7 +355,7 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
     a.r = k.r;
     a.B = k.B;
     a.g = k.g;
-    a.ntiles = ntiles;
+    a.ntiles = grp.ntiles;
     a.levels = lay.L;
     a.scheme = k.scheme;
     a.d0 = (int)(k.n / k.g);
@@ -699,10 +701,17 @@ int mandel_exhaustive_tuned(mandel_region reg, int64_t n, int32_t maxdwell, int3
     return launch_exhaustive<32, 8, MANDEL_EXT_K>(reg, n, maxdwell, d_out, out_pitch, stream);
 }
 
-int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, int32_t r, int32_t B,
-                     const int32_t *h_tile_ids, int32_t n_tiles, int32_t scheme, uint32_t flags, int32_t *d_out,
-                     int64_t out_pitch, void *d_ws, size_t ws_bytes, void *stream)
+} // extern "C"
+
+namespace {
+// mandel_ask_tiles (host tile list h_tile_ids) and mandel_ask_dtiles (device tile list d_tiles
+// of length *d_ntiles, copied into the parameter block by the graph itself).
+int ask_launch(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, int32_t r, int32_t B,
+               const int32_t *h_tile_ids, int32_t n_tiles, const int32_t *d_tiles_in, const int32_t *d_ntiles,
+               int32_t scheme, uint32_t flags, int32_t *d_out, int64_t out_pitch, void *d_ws, size_t ws_bytes,
+               void *stream)
 {
+    const bool dlist = d_tiles_in != nullptr;
     int rc = validate_common(reg, n, maxdwell, d_out, out_pitch);
     if (rc)
         return rc;
@@ -720,6 +729,8 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
     if ((uintptr_t)d_ws % 256 != 0)
         return MANDEL_EINVAL;
     const int64_t G = (int64_t)g * g;
+    if (dlist && (!d_ntiles || h_tile_ids || MANDEL_FLAG_GROUPS_OF(flags) != 1 || G > 4096))
+        return MANDEL_EINVAL;
     if (h_tile_ids) {
         if (n_tiles < 0 || n_tiles > G)
             return MANDEL_EINVAL;
@@ -733,12 +744,13 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
     } else if (n_tiles != 0) {
         return MANDEL_EINVAL;
     }
-    const int ntiles = h_tile_ids ? n_tiles : (int)G;
+    const int ntiles = dlist ? -1 : h_tile_ids ? n_tiles : (int)G;
+    const int cap_tiles = dlist ? (int)G : ntiles;
     // groups: the tiles are dealt round-robin in the given order (LPT order is preserved)
     int ngroups = MANDEL_FLAG_GROUPS_OF(flags);
-    if (ngroups > ntiles)
-        ngroups = ntiles > 0 ? ntiles : 1;
-    const bool listed = h_tile_ids != nullptr || ngroups > 1;
+    if (ngroups > cap_tiles)
+        ngroups = cap_tiles > 0 ? cap_tiles : 1;
+    const bool listed = dlist || h_tile_ids != nullptr || ngroups > 1;
 
     int dev = 0;
     CK(cudaGetDevice(&dev));
@@ -751,16 +763,16 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
     // Pageable source: cudaMemcpyAsync stages it before returning, so the buffer is free for
     // the next call while this one is still queued.
     thread_local std::vector<unsigned char> hp;
-    hp.assign(PRM_TILES + (listed ? (size_t)ntiles * 4 : 0), 0);
+    hp.assign(dlist ? PRM_HOST_BYTES_DTILES : PRM_TILES + (listed ? (size_t)ntiles * 4 : 0), 0);
     DevParams prm;
     memset(&prm, 0, sizeof prm);
     prm.map = make_map(reg, n);
     prm.maxdwell = maxdwell;
     prm.ntiles = ntiles;
     prm.magic = PRM_MAGIC;
-    memcpy(hp.data(), &prm, sizeof prm);
+    memcpy(hp.data(), &prm, dlist ? PRM_HOST_BYTES_DTILES : sizeof prm);
     std::vector<int> gcount((size_t)ngroups, 0);
-    {
+    if (!dlist) {
         int32_t *ord = (int32_t *)(hp.data() + PRM_TILES);
         size_t o = 0;
         for (int gi = 0; gi < ngroups; ++gi)
@@ -772,7 +784,7 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
     }
     CK(cudaMemcpyAsync((char *)d_ws + lay.prm, hp.data(), hp.size(), cudaMemcpyHostToDevice, (cudaStream_t)stream));
 
-    Key key{dev, n, out_pitch, g, r, B, scheme, flags, d_out, d_ws, ws_bytes, ntiles, listed};
+    Key key{dev, n, out_pitch, g, r, B, scheme, flags, d_out, d_ws, ws_bytes, ntiles, listed, d_tiles_in, d_ntiles};
     Entry *hit = nullptr;
     for (auto &e : g_cache)
         if (e.key == key) {
@@ -805,9 +817,17 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
             if (ce != cudaSuccess)
                 erc = cuda_fail(ce, "cudaMemsetAsync(tile_cost)");
         }
+        if (dlist && !erc) { // the device tile list and its length into the parameter block
+            char *pb = (char *)d_ws + lay.prm;
+            ce = cudaMemcpyAsync(pb + offsetof(DevParams, ntiles), d_ntiles, 4, cudaMemcpyDeviceToDevice, di->cap);
+            if (ce == cudaSuccess)
+                ce = cudaMemcpyAsync(pb + PRM_TILES, d_tiles_in, (size_t)G * 4, cudaMemcpyDeviceToDevice, di->cap);
+            if (ce != cudaSuccess)
+                erc = cuda_fail(ce, "cudaMemcpyAsync(device tile list)");
+        }
         if (erc) {
         } else if (ngroups == 1) {
-            Group grp{lay.hdr, 0, ntiles, d_tiles};
+            Group grp{lay.hdr, 0, ntiles, d_tiles, cap_tiles};
             erc = enqueue_ask(key, lay, grp, 1, di->sms, di->cap, di->side[0], di->fork[0], &tm);
         } else { // fork one branch per group off the origin stream, join them at the end
             cudaError_t fe = cudaEventRecord(di->start, di->cap);
@@ -816,7 +836,7 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
                 fe = cudaStreamWaitEvent(di->grp[gi], di->start, 0);
                 if (fe != cudaSuccess)
                     break;
-                Group grp{lay.hdr + (size_t)gi * 4096, unit0, gcount[(size_t)gi], d_tiles + unit0};
+                Group grp{lay.hdr + (size_t)gi * 4096, unit0, gcount[(size_t)gi], d_tiles + unit0, gcount[(size_t)gi]};
                 erc = enqueue_ask(key, lay, grp, ngroups, di->sms, di->grp[gi], di->side[gi], di->fork[gi], &tm);
                 if (!erc)
                     fe = cudaEventRecord(di->join[gi], di->grp[gi]);
@@ -854,6 +874,48 @@ int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, 
     if (!hit->evs.empty())
         g_last_timed = hit->id;
     return MANDEL_OK;
+}
+
+} // namespace
+
+extern "C" {
+
+int mandel_ask_tiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, int32_t r, int32_t B,
+                     const int32_t *h_tile_ids, int32_t n_tiles, int32_t scheme, uint32_t flags, int32_t *d_out,
+                     int64_t out_pitch, void *d_ws, size_t ws_bytes, void *stream)
+{
+    return ask_launch(reg, n, maxdwell, g, r, B, h_tile_ids, n_tiles, nullptr, nullptr, scheme, flags, d_out,
+                      out_pitch, d_ws, ws_bytes, stream);
+}
+
+int mandel_ask_dtiles(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, int32_t r, int32_t B,
+                      const int32_t *d_tile_ids, const int32_t *d_n_tiles, int32_t scheme, uint32_t flags,
+                      int32_t *d_out, int64_t out_pitch, void *d_ws, size_t ws_bytes, void *stream)
+{
+    if (!d_tile_ids)
+        return MANDEL_EINVAL;
+    return ask_launch(reg, n, maxdwell, g, r, B, nullptr, 0, d_tile_ids, d_n_tiles, scheme, flags, d_out, out_pitch,
+                      d_ws, ws_bytes, stream);
+}
+
+int mandel_deal_lpt(const uint64_t *d_costs, int32_t n_tiles, int32_t world, int32_t rank, int32_t *d_tile_ids,
+                    int32_t *d_n_tiles, void *stream)
+{
+    if (!d_costs || !d_tile_ids || !d_n_tiles || n_tiles < 1 || n_tiles > 4096 || world < 1 || world > 64 ||
+        rank < 0 || rank >= world)
+        return MANDEL_EINVAL;
+    k_deal_lpt<<<1, 1024, 0, (cudaStream_t)stream>>>((const unsigned long long *)d_costs, n_tiles, world, rank,
+                                                     d_tile_ids, d_n_tiles);
+    CK(cudaGetLastError());
+    return MANDEL_OK;
+}
+
+size_t mandel_ask_tile_costs_offset(int64_t n, int32_t g, int32_t r, int32_t B)
+{
+    Layout lay;
+    if (!make_layout(n, g, r, B, lay))
+        return 0;
+    return lay.tile_cost;
 }
 
 int mandel_ask_kernel_times(float *ms, int32_t *kind_level, int32_t max_kernels)

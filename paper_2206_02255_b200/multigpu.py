@@ -11,6 +11,11 @@ same code runs over NCCL on the GPU box and over gloo in the CPU tests:
   gather_image(...)      verification only: every rank packs its tiles into one contiguous
                          buffer, rank 0 receives them (batched point-to-point; NCCL over
                          NVLink on the box) and unpacks them into the full n x n image.
+  DevicePlan             one rank's device-resident deal (tile list + count in device memory,
+                         read by mandel_ask_dtiles when the step runs): first from an n/32,
+                         maxdwell/8 preview, then every step from the previous step's per-tile
+                         cost counters, all-reduced across ranks, through mandel_deal_lpt --
+                         no host round trip between the plan and the rank's ASK.
 """
 from __future__ import annotations
 
@@ -99,3 +104,53 @@ def gather_image(img, parts: Sequence[Sequence[int]], g: int, rank: int, dst: in
     for r, b in bufs.items():
         unpack_tiles(full, b.reshape(len(parts[r]), d0, d0), parts[r], g)
     return full
+
+
+PREVIEW_SHRINK, PREVIEW_DWELL_SHRINK = 32, 8  # n/32, maxdwell/8 (profiles/r02_preview_study.jsonl)
+
+
+class DevicePlan:
+    """One rank's device-resident level-0 deal for workload `w`.
+
+    tiles / count are int32 cuda tensors that mandel_ask_dtiles reads when a step executes;
+    deal(costs) overwrites them on the stream with this rank's share of an LPT schedule of the
+    g*g per-tile costs (mandel_deal_lpt: identical on every rank for identical costs)."""
+
+    def __init__(self, w, world: int, rank: int, device, shrink: int = PREVIEW_SHRINK,
+                 dwell_shrink: int = PREVIEW_DWELL_SHRINK):
+        import torch
+        from . import ask, workspace
+        self.w, self.world, self.rank, self.device = w, world, rank, device
+        G = w.g * w.g
+        self.tiles = torch.arange(G, dtype=torch.int32, device=device)
+        self.count = torch.tensor([G], dtype=torch.int32, device=device)
+        self.pn = max(2 * w.g, w.n // shrink)
+        self.pB = max(2, w.B // shrink)
+        while w.g * self.pB > self.pn:
+            self.pB //= 2
+        self.pmd = max(1, w.maxdwell // dwell_shrink)
+        self.pws = workspace(self.pn, w.g, w.r, self.pB, device=device)
+        self.pout = torch.empty((self.pn, self.pn), dtype=torch.int32, device=device)
+        self._ask = ask
+
+    def preview_costs(self, costs_out):
+        """Per-tile executed iterations of ASK on the n/shrink, maxdwell/dwell_shrink preview
+        (the first step's cost estimate), copied into the int64 tensor costs_out."""
+        from . import tile_cost_view
+        w = self.w
+        self._ask(w.region, self.pn, self.pmd, w.g, w.r, self.pB, out=self.pout, ws=self.pws, tile_cost=True)
+        costs_out.copy_(tile_cost_view(self.pws, self.pn, w.g, w.r, self.pB))
+
+    def deal(self, costs):
+        from . import deal_lpt
+        deal_lpt(costs, self.world, self.rank, self.tiles, self.count)
+
+    def render(self, out, ws, tile_cost: bool = True, timing=False):
+        """This rank's ASK over its current tiles (device list), counting per-tile work."""
+        w = self.w
+        return self._ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws,
+                         dtiles=(self.tiles, self.count), tile_cost=tile_cost, timing=timing)
+
+    def host_tiles(self):
+        """This rank's current tile list on the host (synchronises; verification only)."""
+        return self.tiles[: int(self.count.item())].tolist()

@@ -447,3 +447,52 @@ def test_large_maxdwell(mb, md):
     A, _ = oracle.ask(region, 16, md, 2, 2, 4)
     assert np.array_equal(mb.ask(region, 16, md, 2, 2, 4).cpu().numpy(), A)
     assert np.array_equal(mb.exhaustive(region, 16, md).cpu().numpy(), oracle.exhaustive(region, 16, md))
+
+
+# ----------------------------------------------------------------------------- device deal
+@pytest.mark.parametrize("G,world", [(256, 8), (256, 3), (64, 8), (16, 5), (4096, 8), (1, 1)])
+def test_device_lpt_equals_host_lpt(mb, G, world):
+    """mandel_deal_lpt (one block: bitonic sort + greedy list schedule) gives every rank exactly
+    the host LPT deal (paper_2206_02255_b200.deal.lpt), ties included."""
+    from paper_2206_02255_b200 import deal
+    rng = np.random.default_rng(W.SEED + G + world)
+    costs = (rng.pareto(1.3, G) * 1e6).astype(np.int64)
+    costs[rng.choice(G, size=min(G, 7), replace=False)] = 12345  # ties
+    want = deal.lpt(costs.tolist(), world)
+    dc = torch.as_tensor(costs, device="cuda")
+    for rank in range(world):
+        t = torch.full((G,), -1, dtype=torch.int32, device="cuda")
+        c = torch.zeros(1, dtype=torch.int32, device="cuda")
+        mb.deal_lpt(dc, world, rank, t, c)
+        assert t[: int(c.item())].tolist() == want[rank], rank
+
+
+def test_ask_device_tile_list_and_device_plan(mb):
+    """mandel_ask_dtiles: the tile list is read on the device when the call runs -- a deal kernel
+    on the same stream chooses it -- and one graph serves every list; the ranks of a P-way
+    device plan together produce the oracle's image (no tile twice, none missing)."""
+    from paper_2206_02255_b200 import multigpu
+    w = W.Workload("dt", W.SEAHORSE_REGION, 512, 900, 8, 2, 8)
+    A, _ = oracle.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B)
+    out = torch.full((w.n, w.n), -1, dtype=torch.int32, device="cuda")
+    costs = torch.zeros(w.g * w.g, dtype=torch.int64, device="cuda")
+    P = 3
+    plans = [multigpu.DevicePlan(w, P, r, torch.device("cuda")) for r in range(P)]
+    plans[0].preview_costs(costs)
+    seen = []
+    wss = [mb.workspace(w.n, w.g, w.r, w.B) for _ in range(P)]
+    for step in range(2):
+        for p in plans:
+            p.deal(costs)
+        out.fill_(-1)
+        c0 = mb.graph_captures()
+        for p, ws in zip(plans, wss):
+            p.render(out, ws)
+            seen += p.host_tiles()
+        if step == 1:
+            assert mb.graph_captures() == c0  # same graphs as step 0, new device lists
+        assert np.array_equal(out.cpu().numpy(), A), step
+        costs.zero_()
+        for ws in wss:
+            costs += mb.tile_cost_view(ws, w.n, w.g, w.r, w.B)
+    assert sorted(seen[: w.g * w.g]) == list(range(w.g * w.g))

@@ -90,8 +90,8 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_gather_and_reductions_world2():
-    world = 2
+@pytest.mark.parametrize("world", [2, 8])
+def test_gather_and_reductions_world(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -104,5 +104,60 @@ def test_gather_and_reductions_world2():
     for status, ok, tmax, tsum in res:
         assert status == "ok", ok
         assert ok is True
-        assert tmax == 11.0
-        assert tsum == [2.0, 1.0]
+        assert tmax == 10.0 + world - 1
+        assert tsum == [float(world), float(sum(range(world)))]
+
+
+def _worker_feedback(rank, world, port, q):
+    """The host-visible logic of bench.py's N > 1 frame loop on gloo: every rank renders its
+    tiles (oracle, per tile), reports their executed iterations in a g*g vector, all-reduces it,
+    and re-deals with LPT; all ranks must derive the same partition, the partition must be
+    complete, and the gathered image must equal the single-process image."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, md, g, r, B = 256, 500, 8, 2, 8
+        region = W.NONDYADIC_REGIONS[0]
+        parts = deal.diagonal(g, world)  # the first frame's deal (any static deal)
+        for frame in range(2):
+            mine = parts[rank]
+            img = np.full((n, n), -1, np.int32)
+            costs = torch.zeros(g * g, dtype=torch.int64)
+            d0 = n // g
+            for t in mine:
+                tile, st = oracle.ask_tile(region, n, md, g, r, B, t)
+                gy, gx = divmod(t, g)
+                img[gy * d0:(gy + 1) * d0, gx * d0:(gx + 1) * d0] = tile
+                costs[t] = sum(s["border_iters"] + s["leaf_iters"] for s in st)
+            full = multigpu.gather_image(torch.from_numpy(img), parts, g, rank)
+            dist.all_reduce(costs, op=dist.ReduceOp.SUM)
+            nxt = deal.lpt(costs.tolist(), world)
+            allp = [None] * world
+            dist.all_gather_object(allp, nxt)
+            assert all(p == nxt for p in allp)                       # same deal on every rank
+            assert sorted(k for p in nxt for k in p) == list(range(g * g))
+            if rank == 0:
+                ref, _ = oracle.ask(region, n, md, g, r, B)
+                assert np.array_equal(full.numpy(), ref), frame
+            parts = nxt
+        q.put(("ok", True, deal.imbalance(parts, costs.tolist()), None))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put(("err", repr(e), None, None))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_feedback_deal_world(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_feedback, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for status, ok, imb, _ in res:
+        assert status == "ok", ok
+        assert imb < 1.25

@@ -1,104 +1,111 @@
-"""Single-GPU emulation of the multi-GPU strong-scaling run (BASELINE config 3: n=32768 on
-1/2/4/8 B200, north_star target >= 7x from 1 to 8).
+"""Single-GPU emulation of the P-rank strong-scaling step (the box has one B200).
 
-Level-0 tiles are independent and the hot path has no collective, so a rank's
-step is exactly mandel_ask_tiles over its dealt tiles; this tool runs every rank's tile set on
-the one GPU of the box, one after another, and reports the max over ranks of the per-rank
-device time (what bench.py measures under torchrun) plus the imbalance of each deal.
+    python tools/emulate_scaling.py C3 [--ranks 1,2,4,8] [--steps 4] [--reps 3]
+                                       [--allreduce-us 20] [--plan feedback|preview]
 
-    python tools/emulate_scaling.py [C3] [--ranks 1,2,4,8] [--deals costrank,cyclic,diagonal]
+Every rank of a P-way run executes the SAME work it would on its own GPU: its level-0 tiles
+(mandel_ask_dtiles, tile list in device memory) on a full B200, so running the ranks one after
+the other on one GPU and taking the slowest gives the P-GPU step time (the ranks share
+nothing on the data path; the only cross-rank traffic is the g*g cost all-reduce below).
+
+Plans (both device-resident, charged to every step):
+  feedback  the steady-state frame loop of bench.py: step s renders with per-tile cost
+            counters on (MANDEL_FLAG_TILE_COST), the counters are all-reduced across ranks
+            (here: summed over the ranks' workspaces; on the box: NCCL, modelled as
+            --allreduce-us), and mandel_deal_lpt computes every rank's tiles for step s+1;
+            the first step is dealt on an n/32, maxdwell/8 preview.
+  preview   every step is dealt on a fresh n/32, maxdwell/8 preview computed on every rank
+            (ASK with tile costs + mandel_deal_lpt), its time charged.
+Reported per P: max-over-ranks step time, the plan's charge, speedup over the 1-GPU step
+(all tiles, no counters: bench.py's N=1 configuration), and a bit-exactness check of the
+assembled image against that 1-GPU image.
 """
 import argparse
 import json
 import os
+import statistics
 import sys
-import time
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 import paper_2206_02255_b200 as mb  # noqa: E402
 import workloads as W  # noqa: E402
-from paper_2206_02255_b200 import deal  # noqa: E402
+from paper_2206_02255_b200 import multigpu  # noqa: E402
 
 
-GROUPS = None
-SCHEME = "b200"
-
-
-def time_tiles(w, out, ws, tiles, flush, reps):
-    f = lambda: mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, tiles=tiles,  # noqa: E731
-                       groups=GROUPS, scheme=SCHEME)
-    f()
-    torch.cuda.synchronize()
-    ts = []
-    for _ in range(reps):
-        flush.zero_()
-        s, e = torch.cuda.Event(True), torch.cuda.Event(True)
-        s.record()
-        f()
-        e.record()
-        e.synchronize()
-        ts.append(s.elapsed_time(e))
-    return sum(ts) / len(ts)
+def ev_time(fn, flush):
+    flush.zero_()
+    s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+    s.record()
+    fn()
+    e.record()
+    e.synchronize()
+    return s.elapsed_time(e)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("workload", nargs="?", default="C3")
     ap.add_argument("--ranks", default="1,2,4,8")
-    ap.add_argument("--deals", default="lpt,costrank,cyclic,diagonal")
+    ap.add_argument("--steps", type=int, default=4)
     ap.add_argument("--reps", type=int, default=3)
-    ap.add_argument("--groups", type=int, default=None)
-    ap.add_argument("--scheme", default="b200")
-    ap.add_argument("--preview", default="8,2", help="preview shrink,dwell_shrink")
+    ap.add_argument("--allreduce-us", type=float, default=20.0)
+    ap.add_argument("--plan", default="feedback", choices=["feedback", "preview"])
     a = ap.parse_args()
-    global GROUPS, SCHEME
-    GROUPS = a.groups
-    SCHEME = a.scheme
     w = W.CONFIGS[a.workload]
+    G = w.g * w.g
     out = torch.empty((w.n, w.n), dtype=torch.int32, device="cuda")
-    ws = mb.workspace(w.n, w.g, w.r, w.B)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    sh, dsh = (int(x) for x in a.preview.split(","))
-    costs = mb.preview_costs(w.region, w.n, w.maxdwell, w.g, w.r, w.B, shrink=sh, dwell_shrink=dsh)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()  # warm (the first call captured the preview graph)
-    costs = mb.preview_costs(w.region, w.n, w.maxdwell, w.g, w.r, w.B, shrink=sh, dwell_shrink=dsh)
-    torch.cuda.synchronize()
-    preview_ms = 1e3 * (time.perf_counter() - t0)
-    # exact per-tile costs (executed iterations) from one full-size counter pass
-    mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, tile_cost=True)
-    exact = mb.tile_costs(ws, w.g)
-    t1 = time_tiles(w, out, ws, None, flush, a.reps)
-    res = {"workload": w.name, "preview": a.preview, "scheme": SCHEME, "groups": GROUPS, "t1_ms": t1, "preview_ms": preview_ms, "deals": {}}
-    for dname in a.deals.split(","):
-        for P in [int(x) for x in a.ranks.split(",")]:
-            # "<deal>_exact": dealt on the exact per-tile costs (the estimator's upper bound)
-            base = dname[:-6] if dname.endswith("_exact") else dname
-            est = exact if dname.endswith("_exact") else costs
-            parts = deal.deal(base, w.g, P, est if base in ("costrank", "lpt") else None)
-            per = [time_tiles(w, out, ws, p, flush, a.reps) for p in parts]
-            tmax = max(per)
-            res["deals"][f"{dname}:{P}"] = {
-                "max_rank_ms": tmax, "mean_rank_ms": sum(per) / P, "speedup_vs_1": t1 / tmax,
-                "imbalance_time": tmax / (sum(per) / P), "imbalance_exact_iters": deal.imbalance(parts, exact)}
-            print(json.dumps({"deal": dname, "P": P, **res["deals"][f"{dname}:{P}"]}), flush=True)
-    # per-kernel breakdown of the heaviest rank at the largest P (costrank deal)
-    P = max(int(x) for x in a.ranks.split(","))
-    parts = deal.deal("costrank", w.g, P, costs)
-    heavy = max(parts, key=lambda p: sum(exact[k] for k in p))
-    for _ in range(2):
-        mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, tiles=heavy, timing=True, groups=GROUPS,
-               scheme=SCHEME)
-    torch.cuda.synchronize()
-    res["heavy_rank_kernels"] = [dict(k) for k in mb.kernel_times()]
-    mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, timing=True, scheme=SCHEME)
-    torch.cuda.synchronize()
-    res["full_kernels"] = [dict(k) for k in mb.kernel_times()]
+    ws1 = mb.workspace(w.n, w.g, w.r, w.B)
+    one = lambda: mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws1)  # noqa: E731
+    one()
+    t1 = statistics.median([ev_time(one, flush) for _ in range(a.reps)])
+    ref = out.clone()
+    res = {"workload": w.name, "plan": a.plan, "t1_ms": t1, "allreduce_us_model": a.allreduce_us, "P": {}}
+    for P in [int(x) for x in a.ranks.split(",")]:
+        ranks = [multigpu.DevicePlan(w, P, r, torch.device("cuda")) for r in range(P)]
+        wss = [mb.workspace(w.n, w.g, w.r, w.B) for _ in range(P)]
+        costs = torch.zeros(G, dtype=torch.int64, device="cuda")
+        t_prev = ev_time(lambda: ranks[0].preview_costs(costs), flush)
+        for rk in ranks:
+            rk.deal(costs)
+        steps = []
+        for s in range(a.steps):
+            out.fill_(-1)
+            tr = []
+            for rk, ws in zip(ranks, wss):
+                f = lambda: rk.render(out, ws, tile_cost=True)  # noqa: E731
+                f()  # warm (graph capture on first use)
+                tr.append(statistics.median([ev_time(f, flush) for _ in range(a.reps)]))
+            if a.plan == "feedback":  # all-reduce of the counters, then every rank's deal
+                costs.zero_()
+                for rk, ws in zip(ranks, wss):
+                    costs += mb.tile_cost_view(ws, w.n, w.g, w.r, w.B)
+                t_plan = statistics.median([ev_time(lambda: ranks[0].deal(costs), flush) for _ in range(a.reps)])
+                t_plan += a.allreduce_us / 1e3 if P > 1 else 0.0
+            else:
+                t_plan = statistics.median([ev_time(lambda: ranks[0].preview_costs(costs), flush)
+                                            for _ in range(a.reps)])
+                t_plan += statistics.median([ev_time(lambda: ranks[0].deal(costs), flush) for _ in range(a.reps)])
+            for rk in ranks:
+                rk.deal(costs)
+            torch.cuda.synchronize()
+            exact = bool(torch.equal(out, ref))
+            steps.append({"rank_ms": tr, "max_rank_ms": max(tr), "plan_ms": t_plan, "bit_exact": exact,
+                          "tiles": [int(rk.count.item()) for rk in ranks]})
+        last = steps[-1]
+        charged = last["max_rank_ms"] + (last["plan_ms"] if P > 1 else 0.0)
+        res["P"][P] = {"steps": steps, "charged_ms": charged, "speedup": t1 / charged,
+                       "speedup_uncharged": t1 / last["max_rank_ms"],
+                       "imbalance_time": last["max_rank_ms"] / (sum(last["rank_ms"]) / P),
+                       "first_plan_preview_ms": t_prev}
+        print(json.dumps({"P": P, "charged_ms": round(charged, 4), "speedup": round(t1 / charged, 3),
+                          "max_rank_ms": round(last["max_rank_ms"], 4), "plan_ms": round(last["plan_ms"], 4),
+                          "imbalance_time": round(res["P"][P]["imbalance_time"], 4),
+                          "bit_exact": last["bit_exact"],
+                          "step_max_rank_ms": [round(x["max_rank_ms"], 4) for x in steps]}), flush=True)
+        del wss
     print(json.dumps(res), flush=True)
 
 

@@ -45,8 +45,10 @@ def main():
         mb.ask(region, n, md, g, r, B, out=buf, ws=ws, tiles=tiles)
         At, _ = oracle.ask(region, n, md, g, r, B, tiles=tiles)
         assert np.array_equal(buf.cpu().numpy(), At)
-        assert np.array_equal(mb.dp(region, n, md, g, r, B).cpu().numpy(), A)
-        n_ok += 2
+        n_ok += 1
+        if not os.environ.get("SANITIZE_NO_DP"):  # racecheck/synccheck/initcheck cannot follow CDP
+            assert np.array_equal(mb.dp(region, n, md, g, r, B).cpu().numpy(), A)
+            n_ok += 1
     A3, _ = oracle.ask3(W.DEFAULT_REGION3, 32, 128, 2, 2, 4)
     assert np.array_equal(m3.ask3d(W.DEFAULT_REGION3, 32, 128, 2, 2, 4).cpu().numpy(), A3)
     assert np.array_equal(m3.ask3d(W.DEFAULT_REGION3, 32, 128, 2, 2, 4, flat=True).cpu().numpy(), A3)
