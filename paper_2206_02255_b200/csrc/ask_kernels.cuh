@@ -95,11 +95,11 @@ struct WsHeader {
     uint32_t n_fill[MAXL];
     uint32_t n_leaf;
     uint32_t pad0;
-    // LPT ordering: subdivided parents / leaves whose ring reached
-    // maxdwell/2 ("hot": likely long pixels) fill their list from the front, the others
-    // ("cold") from the back, so the next kernel hands out hot work first.
-    uint32_t n_sub_hot[MAXL], n_sub_cold[MAXL];
-    uint32_t n_leaf_hot, n_leaf_cold;
+    // Longest-first ordering: subdivided parents and leaves are appended to 4
+    // length buckets by the share of their ring at maxdwell (bucket 3: >= 1/2, 2: >= 1/8, 1:
+    // ring max >= maxdwell/2, 0: the rest); the next kernel hands out bucket 3 first.
+    uint32_t n_sub_b[MAXL][4];
+    uint32_t n_leaf_b[4];
     uint32_t ngroups; // header of group 0: groups of the last call
     unsigned long long border_px[MAXL], border_iters[MAXL];
     unsigned long long leaf_px, leaf_iters;
@@ -171,6 +171,7 @@ struct LevelArgs {
     int fill_vec;            // SBR in-block fill: rows 16-byte aligned and d % 4 == 0
     unsigned long long *tile_cost; // MANDEL_FLAG_TILE_COST: iterations per level-0 tile
     int d0;                  // level-0 side
+    int d0_log2, g_log2;     // d0 = n/g and g are powers of two: tile of (x, y) by shifts
     // Column lines, transposed (B200 scheme, leaf side u >= 8): every pixel
     // on a column x with x mod u in {0, u-1} -- the only columns any region ring uses -- is
     // also stored at colT[(2 (x / u) + (x mod u != 0)) * colT_pitch + y], so classification
@@ -179,35 +180,70 @@ struct LevelArgs {
     int u_log2;
     long long colT_pitch;    // = n
     FastDiv fd[4];           // lane-refill index maps (host-computed divisors)
-    uint32_t capP;           // parent slots of an OLT buffer (= OLT entries / r^2)
-    uint32_t capL;           // leaf list entries
+    uint32_t capP;           // parent slots of one bucket block of an OLT buffer
+    uint32_t capL;           // leaf entries of one bucket block of the leaf list
     int ngroups;
 };
 
-// Hot/cold list addressing: the q-th subdivided parent of level l-1 (q < hot count: front
-// slot q; else back slot capP-1-(q-hot)), the ri-th region of this level, the li-th leaf.
-__device__ __forceinline__ uint32_t sub_hot(const LevelArgs &a)
+// Length-bucket list addressing.  A list (subdivided parents of a level, or
+// leaves) lives in two two-ended blocks of `cap` slots: bucket 3 from the front of block A,
+// bucket 2 from its back, bucket 1 from the front of block B, bucket 0 from its back.  A
+// consumer walks it in bucket order 3, 2, 1, 0 (longest work first); `slot(q)` is the slot of
+// the q-th entry in that order, `put(b, e)` the slot of the e-th entry appended to bucket b.
+struct BucketMap {
+    uint32_t e3, e32, e321; // prefix ends of buckets 3, 3+2, 3+2+1 in consumption order
+    uint32_t cap;
+    __device__ __forceinline__ uint32_t slot(uint32_t q) const
+    {
+        if (q < e3)
+            return q;
+        if (q < e32)
+            return cap - 1u - (q - e3);
+        if (q < e321)
+            return cap + (q - e32);
+        return 2u * cap - 1u - (q - e321);
+    }
+};
+__device__ __forceinline__ uint32_t bucket_put(int b, uint32_t e, uint32_t cap)
 {
-    return a.level > 0 ? *((volatile uint32_t *)&a.hdr->n_sub_hot[a.level - 1]) : 0u;
+    return b == 3 ? e : b == 2 ? cap - 1u - e : b == 1 ? cap + e : 2u * cap - 1u - e;
 }
-__device__ __forceinline__ uint32_t parent_slot(const LevelArgs &a, uint32_t q, uint32_t nh)
+__device__ __forceinline__ BucketMap bucket_map(const uint32_t *cnt, uint32_t cap)
 {
-    return q < nh ? q : a.capP - 1u - (q - nh);
+    const volatile uint32_t *c = cnt;
+    BucketMap m;
+    m.e3 = c[3];
+    m.e32 = m.e3 + c[2];
+    m.e321 = m.e32 + c[1];
+    m.cap = cap;
+    return m;
 }
-__device__ __forceinline__ uint32_t region_origin(const LevelArgs &a, uint32_t ri, uint32_t nh)
+// Parents of this level's regions (level > 0); level 0 reads the tile list in order.
+__device__ __forceinline__ BucketMap sub_buckets(const LevelArgs &a)
+{
+    if (a.level == 0) {
+        BucketMap m{0xffffffffu, 0xffffffffu, 0xffffffffu, a.capP};
+        return m;
+    }
+    return bucket_map(a.hdr->n_sub_b[a.level - 1], a.capP);
+}
+__device__ __forceinline__ BucketMap leaf_buckets(const LevelArgs &a) { return bucket_map(a.hdr->n_leaf_b, a.capL); }
+// The ri-th region of this level (children of the q-th parent are r^2 consecutive entries).
+__device__ __forceinline__ uint32_t region_origin(const LevelArgs &a, uint32_t ri, const BucketMap &bm)
 {
     if (a.level == 0)
         return a.olt_in[ri];
     const uint32_t rr = (uint32_t)(a.r * a.r), q = ri / rr;
-    return a.olt_in[(size_t)parent_slot(a, q, nh) * rr + (ri - q * rr)];
+    return a.olt_in[(size_t)bm.slot(q) * rr + (ri - q * rr)];
 }
-__device__ __forceinline__ uint32_t leaf_hot(const LevelArgs &a)
+// Length bucket of a region from its ring: nmax of its `ring` pixels sit at maxdwell, hi = max.
+__device__ __forceinline__ int length_bucket(const LevelArgs &a, int hi, int nmax, int ring)
 {
-    return *((volatile uint32_t *)&a.hdr->n_leaf_hot);
-}
-__device__ __forceinline__ uint32_t leaf_origin(const LevelArgs &a, uint32_t li, uint32_t nh)
-{
-    return a.leaf[li < nh ? li : a.capL - 1u - (li - nh)];
+    if (2 * nmax >= ring)
+        return 3;
+    if (8 * nmax >= ring)
+        return 2;
+    return ((long long)hi << MANDEL_HOT_SHIFT) >= a.maxdwell ? 1 : 0;
 }
 
 __device__ __forceinline__ bool on_col_line(const LevelArgs &a, int x)
@@ -230,10 +266,14 @@ __device__ __forceinline__ void store_ring(const LevelArgs &a, int x, int y, int
 
 // Per-level-0-tile executed-iteration counter (stats builds only; used by the multi-GPU
 // cost-ranked deal's preview run).
+__device__ __forceinline__ int tile_of(const LevelArgs &a, int x, int y)
+{
+    return ((y >> a.d0_log2) << a.g_log2) + (x >> a.d0_log2);
+}
 __device__ __forceinline__ void add_tile_cost(const LevelArgs &a, int x, int y, int v)
 {
     if (a.tile_cost)
-        atomicAdd(&a.tile_cost[(y / a.d0) * a.g + x / a.d0], (unsigned long long)v);
+        atomicAdd(&a.tile_cost[tile_of(a, x, y)], (unsigned long long)v);
 }
 
 // --------------------------------------------------------------------------- PDL
@@ -379,7 +419,31 @@ __global__ void __launch_bounds__(1024) k_deal_lpt(const unsigned long long *cos
             }
             __syncthreads();
         }
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && world <= 8) { // loads in registers (the usual case)
+        unsigned long long l[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            l[q] = q < world ? 0ull : ~0ull;
+        int n = 0;
+        for (int i = 0; i < G; ++i) {
+            const unsigned long long k = key[i];
+            const int id = 0xffff - (int)(k & 0xffffull);
+            int best = 0;
+            unsigned long long bl = l[0];
+#pragma unroll
+            for (int q = 1; q < 8; ++q)
+                if (l[q] < bl) {
+                    bl = l[q];
+                    best = q;
+                }
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                l[q] += q == best ? (k >> 16) : 0ull;
+            if (best == rank)
+                tiles_out[n++] = id;
+        }
+        *ntiles_out = n;
+    } else if (threadIdx.x == 0) {
         for (int q = 0; q < world; ++q)
             load[q] = 0ull;
         int n = 0;
@@ -389,7 +453,7 @@ __global__ void __launch_bounds__(1024) k_deal_lpt(const unsigned long long *cos
             for (int q = 1; q < world; ++q)
                 if (load[q] < load[best])
                     best = q;
-            load[best] += costs[id];
+            load[best] += key[i] >> 16;
             if (best == rank)
                 tiles_out[n++] = id;
         }
@@ -432,12 +496,13 @@ __global__ void k_init(LevelArgs a_)
 // --------------------------------------------------------------------------- decisions
 // Common tail of the per-region decision: uniform -> fill list;
 // non-uniform and d/r >= B -> reserve r^2 consecutive OLT slots with one atomicAdd on the
-// level's count (compact concurrent insertion; hot parents from the front of the
-// buffer, cold ones from the back); else -> leaf list.
+// level's count (compact concurrent insertion, in the region's length bucket); else
+// -> leaf list (length bucket).  nmax: ring pixels at maxdwell, ring: ring size.
 // Returns the reserved parent slot (or UINT_MAX) to the caller's lane/thread.
 // fill_list = false: the caller fills the region itself (ASK-SBR's Delta[T]) and
 // only the count is kept.
-__device__ __forceinline__ uint32_t decide(const LevelArgs &a, uint32_t off, int lo, int hi, bool fill_list = true)
+__device__ __forceinline__ uint32_t decide(const LevelArgs &a, uint32_t off, int lo, int hi, int nmax, int ring,
+                                           bool fill_list = true)
 {
     if (lo == hi) {
         const uint32_t e = atomicAdd(&a.hdr->n_fill[a.level], 1u);
@@ -445,18 +510,13 @@ __device__ __forceinline__ uint32_t decide(const LevelArgs &a, uint32_t off, int
             a.fill[e] = make_uint2(off, (uint32_t)lo);
         return UINT_MAX;
     }
-    const bool hot = ((long long)hi << MANDEL_HOT_SHIFT) >= a.maxdwell;
+    const int b = length_bucket(a, hi, nmax, ring);
     if (a.subdivide) {
         atomicAdd(&a.hdr->n_subdiv[a.level], 1u);
-        if (hot)
-            return atomicAdd(&a.hdr->n_sub_hot[a.level], 1u);
-        return a.capP - 1u - atomicAdd(&a.hdr->n_sub_cold[a.level], 1u);
+        return bucket_put(b, atomicAdd(&a.hdr->n_sub_b[a.level][b], 1u), a.capP);
     }
     atomicAdd(&a.hdr->n_leaf, 1u);
-    if (hot)
-        a.leaf[atomicAdd(&a.hdr->n_leaf_hot, 1u)] = off;
-    else
-        a.leaf[a.capL - 1u - atomicAdd(&a.hdr->n_leaf_cold, 1u)] = off;
+    a.leaf[bucket_put(b, atomicAdd(&a.hdr->n_leaf_b[b], 1u), a.capL)] = off;
     return UINT_MAX;
 }
 
@@ -492,18 +552,18 @@ template <int TPB, bool STATS, bool FILL = false>
 __global__ void __launch_bounds__(TPB) k_sbr_level(LevelArgs a_)
 {
     const LevelArgs a = with_params(a_);
-    __shared__ int s_lo[TPB / 32], s_hi[TPB / 32];
+    __shared__ int s_lo[TPB / 32], s_hi[TPB / 32], s_nm[TPB / 32];
     __shared__ unsigned long long s_sum[TPB / 32];
     __shared__ uint32_t s_base;
     __shared__ int s_fillv;
     const uint32_t count = level_count(a);
     const int d = a.d, ring = 4 * d - 4, s = d / a.r, rr = a.r * a.r;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    const uint32_t nh = sub_hot(a);
+    const BucketMap bm = sub_buckets(a);
     for (uint32_t ri = blockIdx.x; ri < count; ri += gridDim.x) {
-        const uint32_t off = region_origin(a, ri, nh);
+        const uint32_t off = region_origin(a, ri, bm);
         const int x0 = unpack_x(off), y0 = unpack_y(off);
-        int lo = INT_MAX, hi = INT_MIN;
+        int lo = INT_MAX, hi = INT_MIN, nm = 0;
         unsigned long long it = 0;
         for (int b = threadIdx.x; b < ring; b += TPB) {
             int x, y;
@@ -512,6 +572,7 @@ __global__ void __launch_bounds__(TPB) k_sbr_level(LevelArgs a_)
             a.out[(long long)y * a.pitch + x] = v;
             lo = min(lo, v);
             hi = max(hi, v);
+            nm += v == a.maxdwell;
             if (STATS) {
                 it += (unsigned long long)v;
                 add_tile_cost(a, x, y, v);
@@ -519,9 +580,11 @@ __global__ void __launch_bounds__(TPB) k_sbr_level(LevelArgs a_)
         }
         lo = __reduce_min_sync(0xffffffffu, lo);
         hi = __reduce_max_sync(0xffffffffu, hi);
+        nm = (int)__reduce_add_sync(0xffffffffu, (unsigned)nm);
         if (l == 0) {
             s_lo[w] = lo;
             s_hi[w] = hi;
+            s_nm[w] = nm;
         }
         if (STATS)
             it = block_sum_u64<TPB>(it, s_sum);
@@ -530,8 +593,9 @@ __global__ void __launch_bounds__(TPB) k_sbr_level(LevelArgs a_)
             for (int i = 1; i < TPB / 32; ++i) {
                 lo = min(lo, s_lo[i]);
                 hi = max(hi, s_hi[i]);
+                nm += s_nm[i];
             }
-            s_base = decide(a, off, lo, hi, !FILL);
+            s_base = decide(a, off, lo, hi, nm, ring, !FILL);
             s_fillv = (lo == hi) ? lo : INT_MIN;
             if (STATS) {
                 atomicAdd(&a.hdr->border_px[a.level], (unsigned long long)ring);
@@ -558,9 +622,9 @@ __global__ void __launch_bounds__(TPB) k_sbr_leaf(LevelArgs a_)
     __shared__ unsigned long long s_sum[TPB / 32];
     const uint32_t count = *((volatile uint32_t *)&a.hdr->n_leaf);
     const int d = a.d, m = d - 2, I = m * m;
-    const uint32_t nh = leaf_hot(a);
+    const BucketMap lb = leaf_buckets(a);
     for (uint32_t li = blockIdx.x; li < count; li += gridDim.x) {
-        const uint32_t off = leaf_origin(a, li, nh);
+        const uint32_t off = a.leaf[lb.slot(li)];
         const int x0 = unpack_x(off) + 1, y0 = unpack_y(off) + 1;
         unsigned long long it = 0;
         for (int p = threadIdx.x; p < I; p += TPB) {
@@ -648,7 +712,7 @@ __global__ void __launch_bounds__(256) k_b200_border(LevelArgs a_)
         total = per * (unsigned long long)(*((volatile uint32_t *)&a.hdr->n_subdiv[a.level - 1]));
     }
     const int rr = a.r * a.r;
-    const uint32_t nh = sub_hot(a);
+    const BucketMap bm = sub_buckets(a);
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     unsigned long long it = 0, px = 0;
     for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
@@ -659,7 +723,7 @@ __global__ void __launch_bounds__(256) k_b200_border(LevelArgs a_)
             const uint32_t off = a.olt_in[p];
             ring_pixel(loc, d, unpack_x(off), unpack_y(off), x, y);
         } else {
-            const uint32_t off = a.olt_in[(size_t)parent_slot(a, p, nh) * rr]; // first child = parent origin
+            const uint32_t off = a.olt_in[(size_t)bm.slot(p) * rr]; // first child = parent origin
             const int x0 = unpack_x(off), y0 = unpack_y(off);
             const int pv = 2 * (a.r - 1) * (D - 2);
             if (loc < pv) {
@@ -706,20 +770,20 @@ __global__ void __launch_bounds__(256) k_b200_classify(LevelArgs a_)
     // warp at the deep levels), a warp, or WPR warps
     constexpr int TPR = WPR == 0 ? 16 : 32 * WPR;
     constexpr int RPB = 256 / TPR; // regions per block round
-    __shared__ int s_lo[8], s_hi[8];
+    __shared__ int s_lo[8], s_hi[8], s_nm[8];
     __shared__ uint32_t s_base[RPB];
     const unsigned gmask = TPR == 16 ? ((threadIdx.x & 16) ? 0xffff0000u : 0x0000ffffu) : 0xffffffffu;
     const uint32_t count = level_count(a);
     const int d = a.d, ring = 4 * d - 4, s = d / a.r, rr = a.r * a.r;
     const int t = threadIdx.x % TPR, w = threadIdx.x >> 5, slot = threadIdx.x / TPR;
     const uint32_t per_block = 256 / TPR;
-    const uint32_t nh = sub_hot(a);
+    const BucketMap bm = sub_buckets(a);
     for (uint32_t ri0 = blockIdx.x * per_block; ri0 < count; ri0 += gridDim.x * per_block) {
         const uint32_t ri = ri0 + slot;
         const bool valid = ri < count;
-        const uint32_t off = valid ? region_origin(a, ri, nh) : 0u;
+        const uint32_t off = valid ? region_origin(a, ri, bm) : 0u;
         const int x0 = unpack_x(off), y0 = unpack_y(off);
-        int lo = INT_MAX, hi = INT_MIN;
+        int lo = INT_MAX, hi = INT_MIN, nm = 0; // nm: ring pixels at maxdwell (length bucket)
         if (valid) {
             // batches of 8 independent loads in flight per thread (the ring of a level-0
             // region is 8188 pixels: latency, not bandwidth, bounds this loop)
@@ -738,54 +802,61 @@ __global__ void __launch_bounds__(256) k_b200_classify(LevelArgs a_)
                 for (int j = 0; j < 8; ++j) {
                     lo = min(lo, v[j]);
                     hi = max(hi, v[j]);
+                    nm += (b0 + j * TPR < ring) && v[j] == a.maxdwell;
                 }
             }
         }
         lo = __reduce_min_sync(gmask, lo);
         hi = __reduce_max_sync(gmask, hi);
+        nm = (int)__reduce_add_sync(gmask, (unsigned)nm);
         if (WPR > 1) {
             if ((threadIdx.x & 31) == 0) {
                 s_lo[w] = lo;
                 s_hi[w] = hi;
+                s_nm[w] = nm;
             }
             __syncthreads();
             if (t == 0) {
                 for (int k = 1; k < WPR; ++k) {
                     lo = min(lo, s_lo[k]);
                     hi = max(hi, s_hi[k]);
+                    nm += s_nm[k];
                 }
-                s_base[slot] = valid ? decide(a, off, lo, hi) : UINT_MAX;
+                s_base[slot] = valid ? decide(a, off, lo, hi, nm, ring) : UINT_MAX;
             }
             __syncthreads();
         } else {
             // Block-aggregated appends: one atomicAdd per outcome per block of 8 or 16 regions
             // instead of two per region (the deep levels hold ~10^5 regions, and per-region
             // atomics on a handful of counters serialise in L2).  Same outcomes and slot
-            // addressing as decide(): hot parents / leaves from the front, cold from the back.
+            // addressing as decide(): subdivided parents and leaves by length bucket.
             __shared__ int s_cat[RPB];
-            __shared__ uint32_t s_cb[6];
+            __shared__ uint32_t s_cb[10];
             if (t == 0) {
-                int cat = 0; // 0 none, 1 fill, 2/3 subdivide hot/cold, 4/5 leaf hot/cold
-                if (valid) {
-                    const bool hot = ((long long)hi << MANDEL_HOT_SHIFT) >= a.maxdwell;
-                    cat = lo == hi ? 1 : a.subdivide ? (hot ? 2 : 3) : (hot ? 4 : 5);
-                }
+                int cat = 0; // 0 none, 1 fill, 2+b subdivide (bucket b), 6+b leaf (bucket b)
+                if (valid)
+                    cat = lo == hi ? 1 : (a.subdivide ? 2 : 6) + length_bucket(a, hi, nm, ring);
                 s_cat[slot] = cat;
             }
             __syncthreads();
             if (threadIdx.x == 0) {
-                uint32_t c[6] = {0u, 0u, 0u, 0u, 0u, 0u};
+                uint32_t c[10];
+#pragma unroll
+                for (int k = 0; k < 10; ++k)
+                    c[k] = 0u;
                 for (int k = 0; k < RPB; ++k)
                     ++c[s_cat[k]];
                 s_cb[1] = c[1] ? atomicAdd(&a.hdr->n_fill[a.level], c[1]) : 0u;
-                if (c[2] + c[3])
-                    atomicAdd(&a.hdr->n_subdiv[a.level], c[2] + c[3]);
-                s_cb[2] = c[2] ? atomicAdd(&a.hdr->n_sub_hot[a.level], c[2]) : 0u;
-                s_cb[3] = c[3] ? atomicAdd(&a.hdr->n_sub_cold[a.level], c[3]) : 0u;
-                if (c[4] + c[5])
-                    atomicAdd(&a.hdr->n_leaf, c[4] + c[5]);
-                s_cb[4] = c[4] ? atomicAdd(&a.hdr->n_leaf_hot, c[4]) : 0u;
-                s_cb[5] = c[5] ? atomicAdd(&a.hdr->n_leaf_cold, c[5]) : 0u;
+                const uint32_t ns = c[2] + c[3] + c[4] + c[5], nl = c[6] + c[7] + c[8] + c[9];
+                if (ns)
+                    atomicAdd(&a.hdr->n_subdiv[a.level], ns);
+                if (nl)
+                    atomicAdd(&a.hdr->n_leaf, nl);
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    s_cb[2 + b] = c[2 + b] ? atomicAdd(&a.hdr->n_sub_b[a.level][b], c[2 + b]) : 0u;
+                    s_cb[6 + b] = c[6 + b] ? atomicAdd(&a.hdr->n_leaf_b[b], c[6 + b]) : 0u;
+                }
             }
             __syncthreads();
             if (t == 0) {
@@ -797,14 +868,10 @@ __global__ void __launch_bounds__(256) k_b200_classify(LevelArgs a_)
                 uint32_t base = UINT_MAX;
                 if (cat == 1)
                     a.fill[e] = make_uint2(off, (uint32_t)lo);
-                else if (cat == 2)
-                    base = e;
-                else if (cat == 3)
-                    base = a.capP - 1u - e;
-                else if (cat == 4)
-                    a.leaf[e] = off;
-                else if (cat == 5)
-                    a.leaf[a.capL - 1u - e] = off;
+                else if (cat >= 2 && cat < 6)
+                    base = bucket_put(cat - 2, e, a.capP);
+                else if (cat >= 6)
+                    a.leaf[bucket_put(cat - 6, e, a.capL)] = off;
                 s_base[slot] = base;
             }
             __syncthreads();
@@ -827,12 +894,12 @@ __global__ void __launch_bounds__(256) k_b200_leaf(LevelArgs a_)
     const unsigned long long I = (unsigned long long)m * m;
     const unsigned long long total = I * (unsigned long long)(*((volatile uint32_t *)&a.hdr->n_leaf));
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    const uint32_t nh = leaf_hot(a);
+    const BucketMap lb = leaf_buckets(a);
     unsigned long long it = 0, px = 0;
     for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
         const uint32_t li = (uint32_t)(t / I);
         const int loc = (int)(t - (unsigned long long)li * I);
-        const uint32_t off = leaf_origin(a, li, nh);
+        const uint32_t off = a.leaf[lb.slot(li)];
         const int x = unpack_x(off) + 1 + loc % m, y = unpack_y(off) + 1 + loc / m;
         const int v = dwell<DWELL_K>(pix_re(a.map, x), pix_im(a.map, y), a.maxdwell);
         a.out[(long long)y * a.pitch + x] = v;
@@ -860,12 +927,12 @@ __global__ void __launch_bounds__(256) k_b200_leaf(LevelArgs a_)
 // Leaf interiors: t = leaf * (d-2)^2 + row-major interior offset.
 struct LeafMap {
     const uint32_t *leaf;
-    uint32_t nh, capL; // hot leaves at the front, cold ones at the back (leaf_origin)
+    BucketMap lb;      // leaves in length-bucket order (longest first)
     FastDiv fI, fm;    // I = (d-2)^2, m = d-2
     __device__ __forceinline__ void operator()(uint32_t t, int &x, int &y) const
     {
         const uint32_t li = fdiv(t, fI), loc = t - li * fI.d;
-        const uint32_t off = leaf[li < nh ? li : capL - 1u - (li - nh)];
+        const uint32_t off = leaf[lb.slot(li)];
         const uint32_t row = fdiv(loc, fm);
         x = unpack_x(off) + 1 + (int)(loc - row * fm.d);
         y = unpack_y(off) + 1 + (int)row;
@@ -875,7 +942,7 @@ struct LeafMap {
 // New border pixels of a level (same enumeration as k_b200_border).
 struct BorderMap {
     const uint32_t *olt;
-    uint32_t nh, capP; // hot parents at the front, cold ones at the back (parent_slot)
+    BucketMap bm;      // parents in length-bucket order (longest first)
     int level, d, r, D;
     FastDiv fper, fcol, fseg, flen; // per, D-2, d-2, r*(d-2)
     __device__ __forceinline__ void operator()(uint32_t t, int &x, int &y) const
@@ -886,7 +953,7 @@ struct BorderMap {
             ring_pixel((int)loc, d, unpack_x(off), unpack_y(off), x, y);
             return;
         }
-        const uint32_t slot = p < nh ? p : capP - 1u - (p - nh);
+        const uint32_t slot = bm.slot(p);
         const uint32_t off = olt[(size_t)slot * (uint32_t)(r * r)]; // first child = parent origin
         const int x0 = unpack_x(off), y0 = unpack_y(off);
         const uint32_t pv = (uint32_t)(2 * (r - 1)) * fcol.d;
@@ -904,11 +971,30 @@ struct BorderMap {
     }
 };
 
+// Per-block tile-cost counters in shared memory (MANDEL_FLAG_TILE_COST in the refill kernels):
+// a 32-bit low word per tile, updated with native shared atomics, and a carry word bumped
+// when the low word wraps (exact for any total); flushed once per block.  A 64-bit shared
+// atomicAdd compiles to a CAS spin loop on sm_100 (measured: the counting pass cost 30% more
+// than the plain step with it).
+constexpr int TC_SMEM = 1024;
+struct TileCostSmem {
+    unsigned lo[TC_SMEM], hi[TC_SMEM];
+};
+template <bool STATS>
+struct TcStorage { // the counters only in the STATS instantiation of a kernel
+    TileCostSmem t;
+    __device__ __forceinline__ TileCostSmem *ptr() { return &t; }
+};
+template <>
+struct TcStorage<false> {
+    __device__ __forceinline__ TileCostSmem *ptr() { return nullptr; }
+};
+
 template <bool STATS, bool RING>
 struct StoreSink {
     const LevelArgs *a;
     unsigned long long iters, px;
-    unsigned long long *s_tc; // per-block tile costs in shared memory (NULL: global atomics)
+    TileCostSmem *s_tc; // per-block tile costs in shared memory (NULL: global atomics)
     __device__ __forceinline__ void operator()(int x, int y, int v)
     {
         if (RING)
@@ -918,34 +1004,39 @@ struct StoreSink {
         if (STATS) {
             iters += (unsigned long long)v;
             px += 1;
-            if (s_tc && a->tile_cost)
-                atomicAdd(&s_tc[(y / a->d0) * a->g + x / a->d0], (unsigned long long)v);
-            else
+            if (s_tc) {
+                const int t = tile_of(*a, x, y);
+                const unsigned old = atomicAdd(&s_tc->lo[t], (unsigned)v);
+                if (old + (unsigned)v < old)
+                    atomicAdd(&s_tc->hi[t], 1u);
+            } else {
                 add_tile_cost(*a, x, y, v);
+            }
         }
     }
 };
 
-// MANDEL_FLAG_TILE_COST in the refill kernels: the preview's per-pixel cost atomics on g^2
-// global counters serialise in L2 (C3's n/8 preview: 1.07 vs 0.65 ms without them), so a
-// block accumulates them in shared memory (g^2 <= TC_SMEM) and flushes once.
-constexpr int TC_SMEM = 1024;
-__device__ __forceinline__ unsigned long long *tc_begin(const LevelArgs &a, unsigned long long *s_tc)
+// MANDEL_FLAG_TILE_COST in the refill kernels: per-pixel atomics on g^2 global counters
+// serialise in L2, so a block accumulates them in shared memory (g^2 <= TC_SMEM) and flushes
+// once.
+__device__ __forceinline__ TileCostSmem *tc_begin(const LevelArgs &a, TileCostSmem *s_tc)
 {
     const bool use = a.tile_cost && a.g * a.g <= TC_SMEM;
     if (use)
         for (int i = threadIdx.x; i < a.g * a.g; i += blockDim.x)
-            s_tc[i] = 0ull;
+            s_tc->lo[i] = s_tc->hi[i] = 0u;
     __syncthreads();
     return use ? s_tc : nullptr;
 }
-__device__ __forceinline__ void tc_flush(const LevelArgs &a, unsigned long long *s_tc)
+__device__ __forceinline__ void tc_flush(const LevelArgs &a, TileCostSmem *s_tc)
 {
     __syncthreads();
     if (s_tc)
-        for (int i = threadIdx.x; i < a.g * a.g; i += blockDim.x)
-            if (s_tc[i])
-                atomicAdd(&a.tile_cost[i], s_tc[i]);
+        for (int i = threadIdx.x; i < a.g * a.g; i += blockDim.x) {
+            const unsigned long long v = ((unsigned long long)s_tc->hi[i] << 32) | s_tc->lo[i];
+            if (v)
+                atomicAdd(&a.tile_cost[i], v);
+        }
 }
 
 template <bool STATS, bool RING>
@@ -974,8 +1065,7 @@ __global__ void __launch_bounds__(RF_TPB, RFB_MINB) k_b200_border_rf(LevelArgs a
 #endif
     BorderMap map;
     map.olt = a.olt_in;
-    map.nh = sub_hot(a);
-    map.capP = a.capP;
+    map.bm = sub_buckets(a);
     map.level = a.level;
     map.d = a.d;
     map.r = a.r;
@@ -987,8 +1077,8 @@ __global__ void __launch_bounds__(RF_TPB, RFB_MINB) k_b200_border_rf(LevelArgs a
     uint32_t count = (a.level == 0) ? (uint32_t)a.ntiles
                                     : *((volatile uint32_t *)&a.hdr->n_subdiv[a.level - 1]);
     const uint32_t total = map.fper.d * count;
-    __shared__ unsigned long long s_tc[STATS ? TC_SMEM : 1];
-    StoreSink<STATS, true> sink{&a, 0ull, 0ull, STATS ? tc_begin(a, s_tc) : nullptr};
+    __shared__ TcStorage<STATS> s_tc;
+    StoreSink<STATS, true> sink{&a, 0ull, 0ull, STATS ? tc_begin(a, s_tc.ptr()) : nullptr};
 #if MANDEL_RFB_PACK && MANDEL_RFB_PRE > 0
     refill_loop2<MANDEL_RFB_K, MANDEL_RFB2_T, MANDEL_RFB_CH, BorderMap, StoreSink<STATS, true>, MANDEL_RFB_PRE>(
         a.map, a.maxdwell, total, &a.hdr->cursor[a.level], map, sink, s_q[threadIdx.x >> 5], a.level,
@@ -1023,13 +1113,12 @@ __global__ void __launch_bounds__(RF_TPB, RFL_MINB) k_b200_leaf_rf(LevelArgs a_)
 #endif
     LeafMap map;
     map.leaf = a.leaf;
-    map.nh = leaf_hot(a);
-    map.capL = a.capL;
+    map.lb = leaf_buckets(a);
     map.fI = a.fd[0];
     map.fm = a.fd[1];
     const uint32_t total = map.fI.d * *((volatile uint32_t *)&a.hdr->n_leaf);
-    __shared__ unsigned long long s_tc[STATS ? TC_SMEM : 1];
-    StoreSink<STATS, false> sink{&a, 0ull, 0ull, STATS ? tc_begin(a, s_tc) : nullptr};
+    __shared__ TcStorage<STATS> s_tc;
+    StoreSink<STATS, false> sink{&a, 0ull, 0ull, STATS ? tc_begin(a, s_tc.ptr()) : nullptr};
     if (map.fI.d > 0)
 #if MANDEL_RFL_PACK
 #if MANDEL_RFL_PRE > 0

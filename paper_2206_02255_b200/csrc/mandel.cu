@@ -103,14 +103,15 @@ bool make_layout(int64_t n, int32_t g, int32_t r, int32_t B, Layout &lay)
     lay.prm = o;
     lay.prm_bytes = PRM_TILES + (size_t)g * g * 4;
     o = align256(o + lay.prm_bytes);
+    // OLT ping-pong and leaf list: two two-ended bucket blocks each (length buckets, §4.8)
     lay.olt[0] = o;
-    o = align256(o + capmax * 4);
+    o = align256(o + 2 * capmax * 4);
     lay.olt[1] = o;
-    o = align256(o + capmax * 4);
+    o = align256(o + 2 * capmax * 4);
     lay.fill = o;
     o = align256(o + fsum * 8);
     lay.leaf = o;
-    o = align256(o + capmax * 4);
+    o = align256(o + 2 * capmax * 4);
     lay.tile_cost = o;
     o = align256(o + (size_t)g * g * 8);
     // transposed column lines (used when the leaf side u >= 8): 2 n/u columns of n rows
@@ -349,7 +350,7 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
     a.pitch = k.pitch;
     a.out = k.out;
     a.hdr = (WsHeader *)(ws + grp.hdr);
-    a.leaf = (uint32_t *)(ws + lay.leaf) + grp.unit0 * lay.per_tile[Lm];
+    a.leaf = (uint32_t *)(ws + lay.leaf) + 2 * grp.unit0 * lay.per_tile[Lm];
     a.tiles = grp.tiles;
     a.ngroups = ngroups;
     a.r = k.r;
@@ -359,6 +360,8 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
     a.levels = lay.L;
     a.scheme = k.scheme;
     a.d0 = (int)(k.n / k.g);
+    a.d0_log2 = ilog2(k.n / k.g);
+    a.g_log2 = ilog2(k.g);
     a.capL = (uint32_t)((size_t)ntiles * lay.per_tile[Lm]);
     a.capP = (uint32_t)((size_t)ntiles * lay.per_tile[Lm] / ((size_t)k.r * k.r));
     a.tile_cost = (k.flags & MANDEL_FLAG_TILE_COST) ? (unsigned long long *)(ws + lay.tile_cost) : nullptr;
@@ -375,8 +378,8 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
     // init: level-0 OLT + zeroed counters
     a.level = 0;
     a.d = d0;
-    uint32_t *olt_g[2] = {(uint32_t *)(ws + lay.olt[0]) + grp.unit0 * lay.per_tile[Lm],
-                          (uint32_t *)(ws + lay.olt[1]) + grp.unit0 * lay.per_tile[Lm]};
+    uint32_t *olt_g[2] = {(uint32_t *)(ws + lay.olt[0]) + 2 * grp.unit0 * lay.per_tile[Lm],
+                          (uint32_t *)(ws + lay.olt[1]) + 2 * grp.unit0 * lay.per_tile[Lm]};
     a.olt_in = olt_g[0];
     {
         int nthr = ntiles > 1024 ? ntiles : 1024;

@@ -102,16 +102,17 @@ def test_levels_and_workspace(lib):
     assert mb.levels(32768, 16, 4, 32) == 4    # C5: 2048,512,128,32
     assert mb.levels(8192, 2, 4, 32) == 4      # non-exact tiling: 4096,1024,256,64
     assert mb.levels(64, 8, 2, 8) == 1
-    # worst case: 2 OLTs + leaf list of (n/B_last)^2 u32 + 4/3 of it as 8-byte fill entries,
-    # plus the transposed column lines (2 n/u columns of n int32, leaf side u >= 8), plus the
-    # headers and the device parameter block (256 B + 4 B per level-0 tile)
+    # worst case: 2 OLTs + leaf list of (n/B_last)^2 u32, each in two bucket blocks (length
+    # buckets), + 4/3 of it as 8-byte fill entries, plus the transposed column
+    # lines (2 n/u columns of n int32, leaf side u >= 8), plus the headers and the device
+    # parameter block (256 B + 4 B per level-0 tile)
     ws = mb.workspace_bytes(65536, 16, 2, 32)
     M = (65536 // 32) ** 2
     colT = 2 * (65536 // 32) * 65536 * 4
-    assert 3 * 4 * M + 8 * M + colT < ws < 3 * 4 * M + 8 * M * 4 // 3 + colT + (1 << 20)
+    assert 6 * 4 * M + 8 * M + colT < ws < 6 * 4 * M + 8 * M * 4 // 3 + colT + (1 << 20)
     # leaf side 4 (< 8): no column copy
     M4 = (1024 // 4) ** 2
-    assert mb.workspace_bytes(1024, 4, 2, 4) < 3 * 4 * M4 + 8 * M4 * 4 // 3 + (1 << 20)
+    assert mb.workspace_bytes(1024, 4, 2, 4) < 6 * 4 * M4 + 8 * M4 * 4 // 3 + (1 << 20)
     assert mb.kernel_count(32768, 16, 2, 32, "b200") == 1 + 7 * 3 + 1
     assert mb.kernel_count(32768, 16, 2, 32, "sbr") == 1 + 7 * 1 + 1   # fills inside the level kernel
     assert mb.kernel_count(32768, 16, 2, 32, "mbr") == 1 + 7 * 2 + 1   # + flat fill per level

@@ -76,10 +76,13 @@ def worker(name, workloads, reps, check):
         res = {"variant": name, "w": wl, "ms": statistics.median(ts), "ms_min": min(ts)}
         mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, tiles=tiles, timing=True)
         torch.cuda.synchronize()
-        kt = {}
+        kt, lv = {}, {}
         for k in mb.kernel_times():
             kt[k["kind"]] = kt.get(k["kind"], 0.0) + k["ms"]
+            if k["kind"] in ("b200_border", "b200_classify", "b200_leaf"):
+                lv[f"{k['kind'][5:]}{k['level']}"] = round(k["ms"], 4)
         res["kernels"] = {k: round(v, 4) for k, v in kt.items()}
+        res["levels"] = lv
         if check and not share:
             from oracle import cache
             rec = cache.tile_records(w.region, w.n, w.maxdwell, w.g, w.r, w.B)
