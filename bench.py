@@ -167,9 +167,11 @@ def _config(w: W.Workload, args, world: int):
                         f"ASK g={w.g} r={w.r} B={w.B}",
             "n": w.n, "maxdwell": w.maxdwell, "g": w.g, "r": w.r, "B": w.B, "region": list(w.region),
             "scheme": args.scheme, "deal": "lpt (device)" if world > 1 else "all tiles",
-            "deal_plan": ("charged to every timed step: per-tile cost counters of this step's render, "
-                          "NCCL all-reduce of the g*g counters, device LPT deal (mandel_deal_lpt) for the next "
-                          "step; the first, untimed step is dealt on an n/32, maxdwell/8 preview")
+            "deal_plan": ("inside every timed step: sampled per-tile cost counters of this step's render "
+                          "(1/64 pixel lattice), then on a side stream overlapping the next step's render: NCCL "
+                          "all-reduce of the g*g counters and the device LPT deal (mandel_deal_lpt) of the step "
+                          "after next, which waits for it on the main stream; the first steps are dealt on an "
+                          "n/32, maxdwell/8 preview")
             if world > 1 else None,
             "parallelism": f"tiles{world}",
             "l2": "output image 4*n^2 B >> 126 MB L2, rewritten every step; plus a 256 MiB L2 flush "
@@ -221,10 +223,12 @@ def main():
     n = w.n
 
     # ---- partition.  N > 1: a device-resident LPT deal of the level-0 tiles
-    # (multigpu.DevicePlan).  Every timed step renders this rank's tiles with per-tile cost
-    # counters on, all-reduces the g*g counters across ranks and re-deals for the next step on
-    # the device (mandel_deal_lpt) -- all inside the step's events, so the plan is charged to
-    # every step.  The first (untimed) step is dealt on an n/32, maxdwell/8 preview.
+    # (multigpu.DevicePlan).  Every timed step renders this rank's tiles with sampled per-tile
+    # cost counters (MANDEL_FLAG_TILE_COST_SAMPLED) and hands them to a side stream, which
+    # all-reduces them across ranks and re-deals on the device (mandel_deal_lpt) for the step
+    # after next while the next step renders: the plan is inside the timed region's wall time
+    # (its events sit on the main stream, which waits for the plan a step uses), off the
+    # critical path.  The first steps are dealt on an n/32, maxdwell/8 preview.
     out = torch.empty((n, n), dtype=torch.int32, device=dev)
     ws = mb.workspace(n, w.g, w.r, w.B, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
@@ -233,25 +237,23 @@ def main():
         plan = multigpu.DevicePlan(w, world, rank, dev)
         costs0 = torch.zeros(w.g * w.g, dtype=torch.int64, device=dev)
         plan.preview_costs(costs0)
-        plan.deal(costs0)
-        cview = mb.tile_cost_view(ws, n, w.g, w.r, w.B)
+        plan.deal(costs0, both=True)
 
-    def allreduce_costs():
+    def allreduce_costs(t):
         if backend == "nccl":
-            dist.all_reduce(cview, op=dist.ReduceOp.SUM)
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
         else:  # gloo test mode: host-side collective
-            h = cview.cpu()
+            h = t.cpu()
             dist.all_reduce(h, op=dist.ReduceOp.SUM)
-            cview.copy_(h)
+            t.copy_(h)
 
     # ---- per-kernel algorithmic work from one untimed counter pass (deterministic)
     if plan is None:
         mb.ask(w.region, n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, scheme=args.scheme, stats=True)
     else:  # converge the deal first (the timed steps run the steady state), then count
-        for _ in range(2):
-            plan.render(out, ws, tile_cost=True)
-            allreduce_costs()
-            plan.deal(cview)
+        for _ in range(4):
+            plan.step(out, ws, allreduce_costs)
+        torch.cuda.synchronize()
         mb.ask(w.region, n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, dtiles=(plan.tiles, plan.count),
                scheme=args.scheme, stats=True)
     lstats = mb.ask_stats(ws)
@@ -267,9 +269,7 @@ def main():
         if plan is None:
             mb.ask(w.region, n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, scheme=args.scheme, timing=timing)
         else:
-            plan.render(out, ws, tile_cost=True, timing=timing)
-            allreduce_costs()
-            plan.deal(cview)
+            plan.step(out, ws, allreduce_costs, timing=timing)
 
     for _ in range(max(3, args.warmup)):
         step()

@@ -130,7 +130,9 @@ def ask(region: Sequence[float], n: int, maxdwell: int, g: int, r: int, B: int, 
     border/leaf kernels instead of the lane-refill ones; serial: fills on the main stream
     instead of concurrent graph branches (A/B comparisons, same image); groups: independent
     level-synchronous chains over round-robin subsets of the tiles, run as parallel graph
-    branches."""
+    branches.  tile_cost: True counts every level-0 tile's executed iterations exactly;
+    "sampled" estimates them from the 1/64 pixel lattice (x + y) % 64 == 0 (B200 scheme; the
+    multi-GPU deal's per-step feedback)."""
     out = _image(n, out)
     _check_device(out, ws, stream=stream)
     if ws is None:
@@ -138,7 +140,7 @@ def ask(region: Sequence[float], n: int, maxdwell: int, g: int, r: int, B: int, 
     t_ptr, t_n, _keep = _lib.tiles_arg(tiles)
     flags = ((_lib.FLAG_STATS if stats else 0)
              | (_lib.FLAG_TIMING_LEAF if timing == "leaf" else _lib.FLAG_TIMING if timing else 0)
-             | (_lib.FLAG_TILE_COST if tile_cost else 0)
+             | (_lib.FLAG_TILE_COST_SAMPLED if tile_cost == "sampled" else _lib.FLAG_TILE_COST if tile_cost else 0)
              | (_lib.FLAG_FLAT if flat else 0)
              | (_lib.FLAG_SERIAL if serial else 0)
              | _lib.flag_groups(DEFAULT_GROUPS if groups is None else groups))

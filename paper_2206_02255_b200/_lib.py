@@ -23,6 +23,7 @@ FLAG_TIMING = 2
 FLAG_TILE_COST = 4
 FLAG_FLAT = 8
 FLAG_SERIAL = 16
+FLAG_TILE_COST_SAMPLED = 32
 FLAG_TIMING_LEAF = 128
 MAX_GROUPS = 8
 

@@ -165,6 +165,9 @@ struct LevelArgs {
     uint2 *fill;             // this level's fill segment
     uint32_t *leaf;
     const int32_t *tiles;    // k_init only: the group's tile list in the parameter block (NULL: canonical)
+    const int32_t *src_tiles, *src_ntiles; // k_init only: the caller's device tile list and length
+                                           // (mandel_ask_dtiles, one group), copied by k_init
+    int zero_costs;          // k_init only: zero the g*g tile-cost counters (one group)
     int level, d, r, B, g, ntiles, levels, scheme; // ntiles < 0: read prm->ntiles (device list)
     int subdivide;           // d / r >= B
     int log2_q4, log2_row4;  // fill: log2(d*d/4), log2(d/4)
@@ -467,8 +470,17 @@ __global__ void __launch_bounds__(1024) k_deal_lpt(const unsigned long long *cos
 __global__ void k_init(LevelArgs a_)
 {
     pdl_entry();
-    const LevelArgs a = with_params(a_);
+    LevelArgs a = with_params(a_);
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a.src_ntiles) { // device tile list: length and ids straight from the caller's buffers;
+        // the length also goes to the parameter block for the later kernels (with_params)
+        a.ntiles = *a.src_ntiles;
+        a.tiles = a.src_tiles;
+        if (t == 0)
+            const_cast<DevParams *>(a.prm)->ntiles = a.ntiles;
+    }
+    if (a.zero_costs && a.tile_cost && t < a.g * a.g)
+        a.tile_cost[t] = 0ull;
     constexpr int hdr_words = sizeof(WsHeader) / 4;
     uint32_t *hw = reinterpret_cast<uint32_t *>(a.hdr);
     constexpr int ng_word = (int)(offsetof(WsHeader, ngroups) / 4);
@@ -990,28 +1002,45 @@ struct TcStorage<false> {
     __device__ __forceinline__ TileCostSmem *ptr() { return nullptr; }
 };
 
-template <bool STATS, bool RING>
+// Count modes of the refill kernels: CM_NONE, CM_STATS (per-level pixel/iteration counters
+// and exact per-tile costs), CM_SAMPLE (MANDEL_FLAG_TILE_COST_SAMPLED: per-tile costs from
+// the pixels on the diagonal lattice (x + y) mod 64 == 0 only, weighted by 64 -- the
+// multi-GPU deal's every-step feedback).  CM_SAMPLE adds its samples with global reductions
+// straight from the sink: shared counters would need block barriers, and a kernel with
+// __syncthreads gets divergence checks around every ballot of the engine (measured: +4% on
+// the C3 step even with the counting itself removed).
+constexpr int CM_NONE = 0, CM_STATS = 1, CM_SAMPLE = 2;
+constexpr int TC_SAMPLE_LOG2 = 6;
+
+template <int CM, bool RING>
 struct StoreSink {
     const LevelArgs *a;
     unsigned long long iters, px;
     TileCostSmem *s_tc; // per-block tile costs in shared memory (NULL: global atomics)
+    __device__ __forceinline__ void count_tile(int x, int y, int v)
+    {
+        if (s_tc) {
+            const int t = tile_of(*a, x, y);
+            const unsigned old = atomicAdd(&s_tc->lo[t], (unsigned)v);
+            if (old + (unsigned)v < old)
+                atomicAdd(&s_tc->hi[t], 1u);
+        } else {
+            add_tile_cost(*a, x, y, v);
+        }
+    }
     __device__ __forceinline__ void operator()(int x, int y, int v)
     {
         if (RING)
             store_ring(*a, x, y, v);
         else
             a->out[(long long)y * a->pitch + x] = v;
-        if (STATS) {
+        if (CM == CM_STATS) {
             iters += (unsigned long long)v;
             px += 1;
-            if (s_tc) {
-                const int t = tile_of(*a, x, y);
-                const unsigned old = atomicAdd(&s_tc->lo[t], (unsigned)v);
-                if (old + (unsigned)v < old)
-                    atomicAdd(&s_tc->hi[t], 1u);
-            } else {
-                add_tile_cost(*a, x, y, v);
-            }
+            count_tile(x, y, v);
+        } else if (CM == CM_SAMPLE) { // 1/64 of the pixels: global reductions (no return value)
+            if (((x + y) & ((1 << TC_SAMPLE_LOG2) - 1)) == 0)
+                atomicAdd(&a->tile_cost[tile_of(*a, x, y)], (unsigned long long)v << TC_SAMPLE_LOG2);
         }
     }
 };
@@ -1039,11 +1068,11 @@ __device__ __forceinline__ void tc_flush(const LevelArgs &a, TileCostSmem *s_tc)
         }
 }
 
-template <bool STATS, bool RING>
-__device__ __forceinline__ void sink_flush(const StoreSink<STATS, RING> &sk, unsigned long long *it_dst,
+template <int CM, bool RING>
+__device__ __forceinline__ void sink_flush(const StoreSink<CM, RING> &sk, unsigned long long *it_dst,
                                            unsigned long long *px_dst)
 {
-    if (!STATS)
+    if (CM != CM_STATS)
         return;
     __shared__ unsigned long long s_sum[RF_TPB / 32];
     const unsigned long long it = block_sum_u64<RF_TPB>(sk.iters, s_sum);
@@ -1054,7 +1083,7 @@ __device__ __forceinline__ void sink_flush(const StoreSink<STATS, RING> &sk, uns
         atomicAdd(px_dst, px);
 }
 
-template <bool STATS>
+template <int CM>
 __global__ void __launch_bounds__(RF_TPB, RFB_MINB) k_b200_border_rf(LevelArgs a_)
 {
     pdl_entry();
@@ -1077,10 +1106,10 @@ __global__ void __launch_bounds__(RF_TPB, RFB_MINB) k_b200_border_rf(LevelArgs a
     uint32_t count = (a.level == 0) ? (uint32_t)a.ntiles
                                     : *((volatile uint32_t *)&a.hdr->n_subdiv[a.level - 1]);
     const uint32_t total = map.fper.d * count;
-    __shared__ TcStorage<STATS> s_tc;
-    StoreSink<STATS, true> sink{&a, 0ull, 0ull, STATS ? tc_begin(a, s_tc.ptr()) : nullptr};
+    __shared__ TcStorage<CM == CM_STATS> s_tc; // sampled costs: no shared memory, no block barrier
+    StoreSink<CM, true> sink{&a, 0ull, 0ull, CM == CM_STATS ? tc_begin(a, s_tc.ptr()) : nullptr};
 #if MANDEL_RFB_PACK && MANDEL_RFB_PRE > 0
-    refill_loop2<MANDEL_RFB_K, MANDEL_RFB2_T, MANDEL_RFB_CH, BorderMap, StoreSink<STATS, true>, MANDEL_RFB_PRE>(
+    refill_loop2<MANDEL_RFB_K, MANDEL_RFB2_T, MANDEL_RFB_CH, BorderMap, StoreSink<CM, true>, MANDEL_RFB_PRE>(
         a.map, a.maxdwell, total, &a.hdr->cursor[a.level], map, sink, s_q[threadIdx.x >> 5], a.level,
         s_sv[threadIdx.x >> 5]);
 #elif MANDEL_RFB_PACK
@@ -1089,7 +1118,7 @@ __global__ void __launch_bounds__(RF_TPB, RFB_MINB) k_b200_border_rf(LevelArgs a
 #else
 #if MANDEL_RFB_SPRE > 0
     __shared__ SvPoint s_sv[RF_TPB / 32][MANDEL_RFB_CH];
-    refill_loop<MANDEL_RFB_K, MANDEL_RFB_T, MANDEL_RFB_CH, BorderMap, StoreSink<STATS, true>, MANDEL_RFB_SPRE>(
+    refill_loop<MANDEL_RFB_K, MANDEL_RFB_T, MANDEL_RFB_CH, BorderMap, StoreSink<CM, true>, MANDEL_RFB_SPRE>(
         a.map, a.maxdwell, total, &a.hdr->cursor[a.level], map, sink, s_q[threadIdx.x >> 5], a.level,
         s_sv[threadIdx.x >> 5]);
 #else
@@ -1097,12 +1126,12 @@ __global__ void __launch_bounds__(RF_TPB, RFB_MINB) k_b200_border_rf(LevelArgs a
                                                            sink, s_q[threadIdx.x >> 5], a.level);
 #endif
 #endif
-    if (STATS)
+    if (CM == CM_STATS)
         tc_flush(a, sink.s_tc);
-    sink_flush<STATS, true>(sink, &a.hdr->border_iters[a.level], &a.hdr->border_px[a.level]);
+    sink_flush<CM, true>(sink, &a.hdr->border_iters[a.level], &a.hdr->border_px[a.level]);
 }
 
-template <bool STATS>
+template <int CM>
 __global__ void __launch_bounds__(RF_TPB, RFL_MINB) k_b200_leaf_rf(LevelArgs a_)
 {
     pdl_entry();
@@ -1117,12 +1146,12 @@ __global__ void __launch_bounds__(RF_TPB, RFL_MINB) k_b200_leaf_rf(LevelArgs a_)
     map.fI = a.fd[0];
     map.fm = a.fd[1];
     const uint32_t total = map.fI.d * *((volatile uint32_t *)&a.hdr->n_leaf);
-    __shared__ TcStorage<STATS> s_tc;
-    StoreSink<STATS, false> sink{&a, 0ull, 0ull, STATS ? tc_begin(a, s_tc.ptr()) : nullptr};
+    __shared__ TcStorage<CM == CM_STATS> s_tc; // sampled costs: no shared memory, no block barrier
+    StoreSink<CM, false> sink{&a, 0ull, 0ull, CM == CM_STATS ? tc_begin(a, s_tc.ptr()) : nullptr};
     if (map.fI.d > 0)
 #if MANDEL_RFL_PACK
 #if MANDEL_RFL_PRE > 0
-        refill_loop2<MANDEL_RFL_K, MANDEL_RFL2_T, MANDEL_RFL_CH, LeafMap, StoreSink<STATS, false>, MANDEL_RFL_PRE>(
+        refill_loop2<MANDEL_RFL_K, MANDEL_RFL2_T, MANDEL_RFL_CH, LeafMap, StoreSink<CM, false>, MANDEL_RFL_PRE>(
             a.map, a.maxdwell, total, &a.hdr->cursor[MAXL], map, sink, s_q[threadIdx.x >> 5], 15,
             s_sv[threadIdx.x >> 5]);
 #else
@@ -1133,9 +1162,9 @@ __global__ void __launch_bounds__(RF_TPB, RFL_MINB) k_b200_leaf_rf(LevelArgs a_)
         refill_loop<MANDEL_RFL_K, MANDEL_RFL_T, MANDEL_RFL_CH>(a.map, a.maxdwell, total, &a.hdr->cursor[MAXL], map,
                                                                sink, s_q[threadIdx.x >> 5], 15);
 #endif
-    if (STATS)
+    if (CM == CM_STATS)
         tc_flush(a, sink.s_tc);
-    sink_flush<STATS, false>(sink, &a.hdr->leaf_iters, &a.hdr->leaf_px);
+    sink_flush<CM, false>(sink, &a.hdr->leaf_iters, &a.hdr->leaf_px);
 }
 
 } // namespace mandel

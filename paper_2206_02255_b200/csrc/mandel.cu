@@ -364,8 +364,12 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
     a.g_log2 = ilog2(k.g);
     a.capL = (uint32_t)((size_t)ntiles * lay.per_tile[Lm]);
     a.capP = (uint32_t)((size_t)ntiles * lay.per_tile[Lm] / ((size_t)k.r * k.r));
-    a.tile_cost = (k.flags & MANDEL_FLAG_TILE_COST) ? (unsigned long long *)(ws + lay.tile_cost) : nullptr;
+    a.tile_cost = (k.flags & (MANDEL_FLAG_TILE_COST | MANDEL_FLAG_TILE_COST_SAMPLED))
+                      ? (unsigned long long *)(ws + lay.tile_cost)
+                      : nullptr;
     const bool stats = (k.flags & (MANDEL_FLAG_STATS | MANDEL_FLAG_TILE_COST)) != 0;
+    // refill kernels' count mode (SAMPLED reaches here only for the B200 refill path)
+    const int cm = stats ? CM_STATS : (k.flags & MANDEL_FLAG_TILE_COST_SAMPLED) ? CM_SAMPLE : CM_NONE;
     const bool flat = (k.flags & MANDEL_FLAG_FLAT) != 0;
     if (k.scheme == MANDEL_SCHEME_B200 && lay.colT_bytes) {
         a.colT = (int *)(ws + lay.colT);
@@ -382,7 +386,13 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
                           (uint32_t *)(ws + lay.olt[1]) + 2 * grp.unit0 * lay.per_tile[Lm]};
     a.olt_in = olt_g[0];
     {
+        if (ngroups == 1 && k.dtiles) { // device list: k_init copies it (no memcpy graph nodes)
+            a.src_tiles = (const int32_t *)k.dtiles;
+            a.src_ntiles = (const int32_t *)k.dntiles;
+        }
+        a.zero_costs = ngroups == 1; // else a memset node before the group branches
         int nthr = ntiles > 1024 ? ntiles : 1024;
+        nthr = nthr > k.g * k.g ? nthr : k.g * k.g;
         TBEGIN(s);
         k_init<<<(nthr + 255) / 256, 256, 0, s>>>(a);
         CK(cudaGetLastError());
@@ -455,12 +465,15 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
                 a.fd[1] = fastdiv_nz((uint32_t)(d * k.r - 2));
                 a.fd[2] = fastdiv_nz((uint32_t)(d - 2));
                 a.fd[3] = fastdiv_nz((uint32_t)(k.r * (d - 2)));
-                if (stats) {
-                    int gsz = resident_grid(k_b200_border_rf<true>, RF_TPB, sms, rf_blocks);
-                    CK(launch_pdl(k_b200_border_rf<true>, gsz, RF_TPB, s, a));
+                if (cm == CM_STATS) {
+                    int gsz = resident_grid(k_b200_border_rf<CM_STATS>, RF_TPB, sms, rf_blocks);
+                    CK(launch_pdl(k_b200_border_rf<CM_STATS>, gsz, RF_TPB, s, a));
+                } else if (cm == CM_SAMPLE) {
+                    int gsz = resident_grid(k_b200_border_rf<CM_SAMPLE>, RF_TPB, sms, rf_blocks);
+                    CK(launch_pdl(k_b200_border_rf<CM_SAMPLE>, gsz, RF_TPB, s, a));
                 } else {
-                    int gsz = resident_grid(k_b200_border_rf<false>, RF_TPB, sms, rf_blocks);
-                    CK(launch_pdl(k_b200_border_rf<false>, gsz, RF_TPB, s, a));
+                    int gsz = resident_grid(k_b200_border_rf<CM_NONE>, RF_TPB, sms, rf_blocks);
+                    CK(launch_pdl(k_b200_border_rf<CM_NONE>, gsz, RF_TPB, s, a));
                 }
             }
             CK(cudaGetLastError());
@@ -556,12 +569,15 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
             } else {
                 a.fd[0] = fastdiv_nz((uint32_t)((d - 2) * (d - 2)));
                 a.fd[1] = fastdiv_nz((uint32_t)(d - 2));
-                if (stats) {
-                    int gsz = resident_grid(k_b200_leaf_rf<true>, RF_TPB, sms, blocks * (256 / RF_TPB));
-                    CK(launch_pdl(k_b200_leaf_rf<true>, gsz, RF_TPB, s, a));
+                if (cm == CM_STATS) {
+                    int gsz = resident_grid(k_b200_leaf_rf<CM_STATS>, RF_TPB, sms, blocks * (256 / RF_TPB));
+                    CK(launch_pdl(k_b200_leaf_rf<CM_STATS>, gsz, RF_TPB, s, a));
+                } else if (cm == CM_SAMPLE) {
+                    int gsz = resident_grid(k_b200_leaf_rf<CM_SAMPLE>, RF_TPB, sms, blocks * (256 / RF_TPB));
+                    CK(launch_pdl(k_b200_leaf_rf<CM_SAMPLE>, gsz, RF_TPB, s, a));
                 } else {
-                    int gsz = resident_grid(k_b200_leaf_rf<false>, RF_TPB, sms, blocks * (256 / RF_TPB));
-                    CK(launch_pdl(k_b200_leaf_rf<false>, gsz, RF_TPB, s, a));
+                    int gsz = resident_grid(k_b200_leaf_rf<CM_NONE>, RF_TPB, sms, blocks * (256 / RF_TPB));
+                    CK(launch_pdl(k_b200_leaf_rf<CM_NONE>, gsz, RF_TPB, s, a));
                 }
             }
         }
@@ -721,9 +737,15 @@ int ask_launch(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, int32_
     if (!valid_grb(n, g, r, B) || !d_ws ||
         (scheme != MANDEL_SCHEME_SBR && scheme != MANDEL_SCHEME_B200 && scheme != MANDEL_SCHEME_MBR) ||
         (flags & ~(MANDEL_FLAG_STATS | MANDEL_FLAG_TIMING | MANDEL_FLAG_TILE_COST | MANDEL_FLAG_FLAT |
-                   MANDEL_FLAG_SERIAL | MANDEL_FLAG_GROUPS_MASK | MANDEL_FLAG_TIMING_LEAF)) != 0 ||
+                   MANDEL_FLAG_SERIAL | MANDEL_FLAG_GROUPS_MASK | MANDEL_FLAG_TIMING_LEAF |
+                   MANDEL_FLAG_TILE_COST_SAMPLED)) != 0 ||
         MANDEL_FLAG_GROUPS_OF(flags) > MAXG)
         return MANDEL_EINVAL;
+    // sampled costs exist only in the B200 refill kernels; elsewhere (and next to the exact
+    // counters) the call counts exactly
+    if ((flags & MANDEL_FLAG_TILE_COST_SAMPLED) &&
+        (scheme != MANDEL_SCHEME_B200 || (flags & (MANDEL_FLAG_FLAT | MANDEL_FLAG_STATS | MANDEL_FLAG_TILE_COST))))
+        flags = (flags & ~MANDEL_FLAG_TILE_COST_SAMPLED) | MANDEL_FLAG_TILE_COST;
     Layout lay;
     if (!make_layout(n, g, r, B, lay))
         return MANDEL_EINVAL;
@@ -815,12 +837,13 @@ int ask_launch(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, int32_
         tm.on = (flags & (MANDEL_FLAG_TIMING | MANDEL_FLAG_TIMING_LEAF)) != 0;
         tm.leaf_only = (flags & MANDEL_FLAG_TIMING) == 0;
         int erc = MANDEL_OK;
-        if (flags & MANDEL_FLAG_TILE_COST) { // every g*g counter starts at 0 (a memset node)
+        if ((flags & (MANDEL_FLAG_TILE_COST | MANDEL_FLAG_TILE_COST_SAMPLED)) && ngroups > 1) {
+            // every g*g counter starts at 0 (one group: k_init zeroes them)
             ce = cudaMemsetAsync((char *)d_ws + lay.tile_cost, 0, (size_t)G * 8, di->cap);
             if (ce != cudaSuccess)
                 erc = cuda_fail(ce, "cudaMemsetAsync(tile_cost)");
         }
-        if (dlist && !erc) { // the device tile list and its length into the parameter block
+        if (dlist && ngroups > 1 && !erc) { // the device tile list and its length into the parameter block
             char *pb = (char *)d_ws + lay.prm;
             ce = cudaMemcpyAsync(pb + offsetof(DevParams, ntiles), d_ntiles, 4, cudaMemcpyDeviceToDevice, di->cap);
             if (ce == cudaSuccess)

@@ -85,6 +85,12 @@ constexpr int RF_QCAP = 64; // per-warp queue entries (< 32 left over + < 32 new
 #ifndef MANDEL_RF_EXACT
 #define MANDEL_RF_EXACT 1
 #endif
+// Scalar engine: CKPT sub-chunks per K-step chunk.  The orbit is kept at every sub-chunk
+// boundary, so a parked point's first escape is located to one sub-chunk from the saved
+// points' |z|^2 and the replay bisects K/CKPT steps instead of K (1: plain chunks).
+#ifndef MANDEL_RF_CKPT
+#define MANDEL_RF_CKPT 2
+#endif
 #ifndef MANDEL_RF_EXACT_PPW
 #define MANDEL_RF_EXACT_PPW 1024u // scalar engine: exact grabs below this many pixels per warp
 #endif
@@ -268,30 +274,59 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
     uint32_t sv_pos = 0, sv_end = 0; // warp-uniform survivor buffer window
     int pre_esc = 0;
 
-    bool has = false, fin = false;
+    constexpr int CKP = MANDEL_RF_CKPT, KS = K / CKP; // sub-chunks and their length
+    static_assert(CKP >= 1 && K % CKP == 0 && (KS & (KS - 1)) == 0, "CKPT must split K into powers of two");
+    bool has = false, fin = false, endok = false;
     int px = 0, py = 0;
     float cr = 0.f, ci = 0.f, x = 0.f, y = 0.f, x2 = 0.f, y2 = 0.f, sx = 0.f, sy = 0.f;
+    float ckx[CKP > 1 ? CKP - 1 : 1], cky[CKP > 1 ? CKP - 1 : 1];
+#pragma unroll
+    for (int c = 0; c < (CKP > 1 ? CKP - 1 : 1); ++c)
+        ckx[c] = cky[c] = 0.f;
     unsigned it = 0, sit = 0;
 
     while (true) {
         // ---------------------------------------------------------------- park + refill
         const unsigned f = __ballot_sync(FULL, fin);
         if (f) {
-            if (fin) {
-                ParkedPoint &e = q[qn + __popc(f & lt)];
+            // a lane that reached maxdwell unescaped (|z|^2 <= 4 at the chunk end, escape is
+            // permanent) has dwell maxdwell: stored at once, no replay
+            const bool direct = fin && endok;
+            if (direct)
+                sink(px, py, (int)md);
+            const bool enq = fin && !direct;
+            const unsigned fq = __ballot_sync(FULL, enq);
+            if (enq) {
+                // the replay window: the sub-chunk after the last kept point not yet past
+                // the first escape (or maxdwell), P(j) = escaped by j || sit + j >= md
+                float bx = sx, by = sy;
+                unsigned bit = sit;
+#pragma unroll
+                for (int c = 0; c < CKP - 1; ++c) {
+                    const unsigned jc = sit + (unsigned)((c + 1) * KS);
+                    const float m = __fadd_rn(__fmul_rn(ckx[c], ckx[c]), __fmul_rn(cky[c], cky[c]));
+                    if (bit + (unsigned)KS == jc && m <= 4.0f && jc < md) {
+                        bx = ckx[c];
+                        by = cky[c];
+                        bit = jc;
+                    }
+                }
+                ParkedPoint &e = q[qn + __popc(fq & lt)];
                 e.px = px;
                 e.py = py;
-                e.x = sx;
-                e.y = sy;
-                e.it = sit;
+                e.x = bx;
+                e.y = by;
+                e.it = bit;
+            }
+            if (fin) {
                 has = false;
                 fin = false;
             }
-            qn += __popc(f);
+            qn += __popc(fq);
             __syncwarp();
             if (qn >= 32) {
                 qn -= 32;
-                replay_batch<K>(q + qn, 32, pm, md, sink);
+                replay_batch<KS>(q + qn, 32, pm, md, sink);
             }
         }
         unsigned need = __ballot_sync(FULL, !has);
@@ -392,10 +427,19 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
             sy = keep ? sy : y;
             sit = keep ? sit : it;
 #pragma unroll
-            for (int k = 0; k < K; ++k)
-                MANDEL_STEP(x, y, x2, y2, cr, ci);
+            for (int c = 0; c < CKP; ++c) {
+#pragma unroll
+                for (int k = 0; k < KS; ++k)
+                    MANDEL_STEP(x, y, x2, y2, cr, ci);
+                if (c < CKP - 1) {
+                    ckx[c] = keep ? ckx[c] : x;
+                    cky[c] = keep ? cky[c] : y;
+                }
+            }
             it += K;
-            fin = live && (fin || !(__fadd_rn(x2, y2) <= 4.0f) || it >= md);
+            const bool inside = __fadd_rn(x2, y2) <= 4.0f;
+            endok = fin ? endok : inside;
+            fin = live && (fin || !inside || it >= md);
             const unsigned fm = __ballot_sync(FULL, fin);
             if (fm == active || __popc(fm) >= thresh)
                 break;
@@ -403,7 +447,7 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
     }
     // drain the queue
     if (qn > 0)
-        replay_batch<K>(q, qn, pm, md, sink);
+        replay_batch<KS>(q, qn, pm, md, sink);
 #ifdef MANDEL_RF_TRACE
     if (lane == 0 && wrank < 8192 && tslot >= 0 && tslot < 16) {
         g_rf_trace[tslot][wrank][0] = tr_start;

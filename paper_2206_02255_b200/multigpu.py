@@ -112,9 +112,13 @@ PREVIEW_SHRINK, PREVIEW_DWELL_SHRINK = 32, 8  # n/32, maxdwell/8 (profiles/r02_p
 class DevicePlan:
     """One rank's device-resident level-0 deal for workload `w`.
 
-    tiles / count are int32 cuda tensors that mandel_ask_dtiles reads when a step executes;
-    deal(costs) overwrites them on the stream with this rank's share of an LPT schedule of the
-    g*g per-tile costs (mandel_deal_lpt: identical on every rank for identical costs)."""
+    Two device tile lists (int32 cuda tensors, read by mandel_ask_dtiles when a step executes)
+    alternate between steps.  deal(costs) overwrites the current one with this rank's share of
+    an LPT schedule of the g*g per-tile costs (mandel_deal_lpt: identical on every rank for
+    identical costs).  step() is the frame loop of bench.py: render with sampled per-tile cost
+    counters, then -- on a side stream, overlapped with the NEXT step's render -- all-reduce
+    the counters and deal the step after next (a one-step-lagged feedback plan, so the plan is
+    off the critical path but still inside the timed region's wall time)."""
 
     def __init__(self, w, world: int, rank: int, device, shrink: int = PREVIEW_SHRINK,
                  dwell_shrink: int = PREVIEW_DWELL_SHRINK):
@@ -122,8 +126,12 @@ class DevicePlan:
         from . import ask, workspace
         self.w, self.world, self.rank, self.device = w, world, rank, device
         G = w.g * w.g
-        self.tiles = torch.arange(G, dtype=torch.int32, device=device)
-        self.count = torch.tensor([G], dtype=torch.int32, device=device)
+        self.tiles2 = [torch.arange(G, dtype=torch.int32, device=device) for _ in range(2)]
+        self.count2 = [torch.tensor([G], dtype=torch.int32, device=device) for _ in range(2)]
+        self.cbuf2 = [torch.zeros(G, dtype=torch.int64, device=device) for _ in range(2)]
+        self.cur = 0
+        self.side = torch.cuda.Stream(device=device)
+        self.ev_plan = [None, None]
         self.pn = max(2 * w.g, w.n // shrink)
         self.pB = max(2, w.B // shrink)
         while w.g * self.pB > self.pn:
@@ -133,24 +141,62 @@ class DevicePlan:
         self.pout = torch.empty((self.pn, self.pn), dtype=torch.int32, device=device)
         self._ask = ask
 
+    @property
+    def tiles(self):
+        return self.tiles2[self.cur]
+
+    @property
+    def count(self):
+        return self.count2[self.cur]
+
     def preview_costs(self, costs_out):
         """Per-tile executed iterations of ASK on the n/shrink, maxdwell/dwell_shrink preview
-        (the first step's cost estimate), copied into the int64 tensor costs_out."""
+        (the first steps' cost estimate), copied into the int64 tensor costs_out."""
         from . import tile_cost_view
         w = self.w
         self._ask(w.region, self.pn, self.pmd, w.g, w.r, self.pB, out=self.pout, ws=self.pws, tile_cost=True)
         costs_out.copy_(tile_cost_view(self.pws, self.pn, w.g, w.r, self.pB))
 
-    def deal(self, costs):
+    def deal(self, costs, both: bool = False):
+        """Deal the current tile list (both: both lists) on the current stream."""
         from . import deal_lpt
-        deal_lpt(costs, self.world, self.rank, self.tiles, self.count)
+        for k in ((0, 1) if both else (self.cur,)):
+            deal_lpt(costs, self.world, self.rank, self.tiles2[k], self.count2[k])
 
-    def render(self, out, ws, tile_cost: bool = True, timing=False):
-        """This rank's ASK over its current tiles (device list), counting per-tile work."""
+    def render(self, out, ws, tile_cost="sampled", timing=False):
+        """This rank's ASK over its current tiles (device list), estimating per-tile work
+        (MANDEL_FLAG_TILE_COST_SAMPLED) for a later step's deal."""
         w = self.w
         return self._ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws,
                          dtiles=(self.tiles, self.count), tile_cost=tile_cost, timing=timing)
 
-    def host_tiles(self):
-        """This rank's current tile list on the host (synchronises; verification only)."""
-        return self.tiles[: int(self.count.item())].tolist()
+    def step(self, out, ws, allreduce, timing=False):
+        """One frame: wait for the plan that chose this step's tiles, render them, hand the
+        sampled counters to the side stream, which all-reduces them (`allreduce(t)`: in place,
+        sum over ranks) and deals the step after next into the list this step just used."""
+        import torch
+        from . import deal_lpt, tile_cost_view
+        w, k = self.w, self.cur
+        main = torch.cuda.current_stream(self.device)
+        if self.ev_plan[k] is not None:
+            main.wait_event(self.ev_plan[k])
+        self.render(out, ws, timing=timing)
+        cb = self.cbuf2[k]
+        cb.copy_(tile_cost_view(ws, w.n, w.g, w.r, w.B))
+        ev = torch.cuda.Event()
+        ev.record(main)
+        with torch.cuda.stream(self.side):
+            self.side.wait_event(ev)
+            allreduce(cb)
+            deal_lpt(cb, self.world, self.rank, self.tiles2[k], self.count2[k], stream=self.side)
+            ev_p = torch.cuda.Event()
+            ev_p.record(self.side)
+        self.ev_plan[k] = ev_p
+        self.cur = 1 - k
+
+    def host_tiles(self, which: int = None):
+        """Tile list `which` (default: the next step's) on the host (synchronises)."""
+        import torch
+        k = self.cur if which is None else which
+        torch.cuda.synchronize(self.device)
+        return self.tiles2[k][: int(self.count2[k].item())].tolist()

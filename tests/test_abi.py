@@ -149,7 +149,7 @@ def test_validation_before_any_launch(lib):
     assert lib.mandel_ask_tiles(*args, None, 0, 1, 64, fake, 64, fake, ws_need, None) == 1       # unknown flag bit
     assert lib.mandel_ask_tiles(*args, None, 0, 1, 1 << 28, fake, 64, fake, ws_need, None) == 1
     assert lib.mandel_ask_tiles(*args, None, 0, 3, 0, fake, 64, fake, ws_need, None) == 1        # no scheme 3
-    assert lib.mandel_ask_tiles(*args, None, 0, 1, 32, fake, 64, fake, ws_need, None) == 1       # no flag 32
+    assert lib.mandel_ask_tiles(*args, None, 0, 1, 1 << 12, fake, 64, fake, ws_need, None) == 1  # no flag 4096
     # more than 8 groups (MANDEL_FLAG_GROUPS bits 8-11 hold G-1)
     assert lib.mandel_ask_tiles(*args, None, 0, 1, 8 << 8, fake, 64, fake, ws_need, None) == 1
     assert _lib.flag_groups(1) == 0 and _lib.flag_groups(8) == 7 << 8

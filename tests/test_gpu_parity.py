@@ -396,6 +396,77 @@ def test_tile_costs_match_oracle(mb, n, g, r, B, md, region):
     assert got == want
 
 
+@pytest.mark.parametrize("n,g,r,B,md,region", [
+    (256, 4, 2, 8, 500, W.DEFAULT_REGION),
+    (512, 8, 2, 16, 900, W.SEAHORSE_REGION),
+    (1024, 16, 4, 8, 700, W.NONDYADIC_REGIONS[0]),
+])
+def test_tile_costs_sampled_match_oracle(mb, n, g, r, B, md, region):
+    """MANDEL_FLAG_TILE_COST_SAMPLED (the multi-GPU deal's per-step feedback): the same pixel
+    set as the exact counters, but only pixels with (x + y) % 64 == 0, each weighted 64 -- an
+    exact identity against the oracle; the image is unchanged; and the estimate ranks tiles
+    like the exact cost (checked loosely: it is a 1/64 lattice sample)."""
+    ws = mb.workspace(n, g, r, B)
+    out = mb.ask(region, n, md, g, r, B, ws=ws, tile_cost="sampled")
+    got = mb.tile_costs(ws, g)
+    A, _, recs = oracle.ask(region, n, md, g, r, B, want_regions=True)
+    assert np.array_equal(out.cpu().numpy(), A)
+    E = oracle.exhaustive(region, n, md).astype(np.int64)
+    inner = np.zeros((n, n), dtype=bool)
+    for x, y, d, kind, _v, _l in recs.tolist():
+        if kind == 0 and d > 2:
+            inner[y + 1:y + d - 1, x + 1:x + d - 1] = True
+    yy, xx = np.indices((n, n))
+    lattice = (xx + yy) % 64 == 0
+    d0 = n // g
+    sl = lambda M, gy, gx: M[gy * d0:(gy + 1) * d0, gx * d0:(gx + 1) * d0]  # noqa: E731
+    want = [64 * int(sl(E, gy, gx)[~sl(inner, gy, gx) & sl(lattice, gy, gx)].sum())
+            for gy in range(g) for gx in range(g)]
+    assert got == want
+    exact = [int(sl(E, gy, gx)[~sl(inner, gy, gx)].sum()) for gy in range(g) for gx in range(g)]
+    assert abs(sum(got) - sum(exact)) <= 0.1 * sum(exact)
+
+
+def test_device_plan_frame_loop(mb):
+    """DevicePlan.step, bench.py's N > 1 frame loop with the one-step-lagged side-stream plan,
+    run for every rank of a P-way deal on one GPU: each frame the ranks together render the
+    oracle's image (no tile twice, none missing) and from the third frame on the partition is
+    the LPT deal of the sampled costs."""
+    from paper_2206_02255_b200 import deal, multigpu
+    w = W.Workload("fl", W.DEFAULT_REGION, 1024, 1000, 16, 2, 16)
+    A, _ = oracle.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B)
+    P = 4
+    plans = [multigpu.DevicePlan(w, P, r, torch.device("cuda")) for r in range(P)]
+    c0 = torch.zeros(w.g * w.g, dtype=torch.int64, device="cuda")
+    plans[0].preview_costs(c0)
+    for p in plans:
+        p.deal(c0, both=True)
+    wss = [mb.workspace(w.n, w.g, w.r, w.B) for _ in range(P)]
+    out = torch.full((w.n, w.n), -1, dtype=torch.int32, device="cuda")
+    for frame in range(4):
+        out.fill_(-1)
+        lists = [p.host_tiles() for p in plans]
+        assert sorted(k for l in lists for k in l) == list(range(w.g * w.g)), frame
+        views = []
+        for p, ws in zip(plans, wss):
+            p.step(out, ws, lambda t: views.append(t))
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), A), frame
+        # the side streams dealt on each rank's own counters; redo it on what the NCCL
+        # all-reduce would have left in every rank's buffer: the sum over the ranks
+        total = sum(views)
+        for v in views:
+            v.copy_(total)
+        for p in plans:
+            k = 1 - p.cur
+            mb.deal_lpt(p.cbuf2[k], P, p.rank, p.tiles2[k], p.count2[k])
+        torch.cuda.synchronize()
+        want = deal.lpt(total.tolist(), P)
+        for p in plans:
+            k = 1 - p.cur
+            assert p.tiles2[k][: int(p.count2[k].item())].tolist() == want[p.rank]
+
+
 def test_timing_modes(mb):
     """bench.py's timed steps use MANDEL_FLAG_TIMING_LEAF: events around the leaf kernel only
     (the level chain keeps its programmatic-dependent-launch edges); MANDEL_FLAG_TIMING times

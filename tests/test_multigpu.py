@@ -111,15 +111,17 @@ def test_gather_and_reductions_world(world):
 def _worker_feedback(rank, world, port, q):
     """The host-visible logic of bench.py's N > 1 frame loop on gloo: every rank renders its
     tiles (oracle, per tile), reports their executed iterations in a g*g vector, all-reduces it,
-    and re-deals with LPT; all ranks must derive the same partition, the partition must be
-    complete, and the gathered image must equal the single-process image."""
+    and re-deals with LPT for the frame after next (DevicePlan.step's one-step lag: the deal of
+    frame f + 2 overlaps frame f + 1); all ranks must derive the same partition, the partition
+    must be complete, and the gathered image must equal the single-process image."""
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         n, md, g, r, B = 256, 500, 8, 2, 8
         region = W.NONDYADIC_REGIONS[0]
-        parts = deal.diagonal(g, world)  # the first frame's deal (any static deal)
-        for frame in range(2):
+        plans = [deal.diagonal(g, world), deal.cyclic(g, world)]  # frames 0, 1: static deals
+        for frame in range(4):
+            parts = plans[frame]
             mine = parts[rank]
             img = np.full((n, n), -1, np.int32)
             costs = torch.zeros(g * g, dtype=torch.int64)
@@ -139,7 +141,8 @@ def _worker_feedback(rank, world, port, q):
             if rank == 0:
                 ref, _ = oracle.ask(region, n, md, g, r, B)
                 assert np.array_equal(full.numpy(), ref), frame
-            parts = nxt
+            plans.append(nxt)  # frame + 2's deal
+        parts = plans[-1]
         q.put(("ok", True, deal.imbalance(parts, costs.tolist()), None))
     except Exception as e:  # pragma: no cover - reported to the parent
         q.put(("err", repr(e), None, None))

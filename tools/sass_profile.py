@@ -30,6 +30,8 @@ def sass_page(rep, launch):
     h = rows[0]
     ia, isrc, iex = h.index("Address"), h.index("Source"), h.index("Instructions Executed")
     ith = h.index("Predicated-On Thread Instructions Executed")
+    isamp = h.index("Warp Stall Sampling (All Samples)") if "Warp Stall Sampling (All Samples)" in h else None
+    stall_cols = [(i, c[len("stall_"):]) for i, c in enumerate(h) if c.startswith("stall_") and "Not Issued" not in c]
     res, seen = [], set()
     for r in rows[1:]:
         if r and r[ia] in seen:  # ncu prints the page once per view: keep the first
@@ -39,7 +41,9 @@ def sass_page(rep, launch):
         if len(r) <= ith:
             continue
         try:
-            res.append((int(r[ia], 16), r[isrc].strip(), int(float(r[iex] or 0)), int(float(r[ith] or 0))))
+            st = {c: int(float(r[i] or 0)) for i, c in stall_cols if i < len(r) and r[i] not in ("", "0", "-")}
+            samp = int(float(r[isamp] or 0)) if isamp is not None and r[isamp] not in ("", "-") else 0
+            res.append((int(r[ia], 16), r[isrc].strip(), int(float(r[iex] or 0)), int(float(r[ith] or 0)), samp, st))
         except ValueError:
             continue
     return kname, res
@@ -47,7 +51,7 @@ def sass_page(rep, launch):
 
 def line_table(lib, mangled):
     d = tempfile.mkdtemp()
-    subprocess.run(["cuobjdump", "-xelf", "all", lib], cwd=d, capture_output=True)
+    subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=d, capture_output=True)
     cub = [os.path.join(d, f) for f in os.listdir(d) if f.endswith(".cubin")][0]
     txt = subprocess.run(["nvdisasm", "-g", "-c", cub], capture_output=True, text=True).stdout
     start = txt.index(f".text.{mangled}:")
@@ -86,13 +90,21 @@ def main():
     per_line = collections.Counter()
     per_line_fp = collections.Counter()
     per_op = collections.Counter()
-    tot = fp = 0
-    for addr, src, ex, th in rows:
+    per_line_samp = collections.Counter()
+    per_line_stall = collections.defaultdict(collections.Counter)
+    stall_tot = collections.Counter()
+    tot = fp = samp_tot = 0
+    for addr, src, ex, th, samp, st in rows:
         key = table.get(addr - base_addr, ("?", 0))
         op = src.split()[0] if src else "?"
         if op.startswith("@"):
             op = src.split()[1]
         per_line[key] += ex
+        per_line_samp[key] += samp
+        samp_tot += samp
+        for c, v in st.items():
+            per_line_stall[key][c] += v
+            stall_tot[c] += v
         per_op[op.split(".")[0]] += ex
         tot += ex
         if FP32.match(op):
@@ -103,6 +115,12 @@ def main():
     for key, v in per_line.most_common(a.top):
         print(f"{key[0]:>18}:{key[1]:<5} {v:12.4e} {v / tot:7.3f} {per_line_fp[key] / max(v, 1):7.2f}")
     print("opcodes:", ", ".join(f"{k} {v / tot:.3f}" for k, v in per_op.most_common(25)))
+    if samp_tot:
+        print(f"stall samples {samp_tot}:", ", ".join(f"{k} {v / samp_tot:.3f}" for k, v in stall_tot.most_common(12)))
+        print(f"{'file:line':>24} {'samples':>8} {'share':>7}  top stalls")
+        for key, v in per_line_samp.most_common(a.top):
+            top = ", ".join(f"{c} {n / max(v, 1):.2f}" for c, n in per_line_stall[key].most_common(4))
+            print(f"{key[0]:>18}:{key[1]:<5} {v:8d} {v / samp_tot:7.3f}  {top}")
     if a.json:
         json.dump({"kernel": kname, "total": tot, "fp32": fp,
                    "lines": [[f"{k[0]}:{k[1]}", v, per_line_fp[k]] for k, v in per_line.most_common()],
