@@ -41,7 +41,8 @@ if ROOT not in sys.path:
 import workloads as W  # noqa: E402
 
 METRIC = "Mpixel/s & Giter/s, n=32768 ASK, 1/2/4/8 B200; speedup vs exhaustive; % FP32 peak"
-FLOPS_PER_ITER = 7          # 3 FMUL + 4 FADD (no FMA possible: DESIGN.md R4)
+FLOPS_PER_ITER = 6          # FP32 instructions per dwell iteration: 3 FMUL + 2 FADD + 1 FFMA(xy, 2, ci)
+PAPER_OPS_PER_ITER = 7      # the literal step's 3 FMUL + 4 FADD (R4; R4' fuses (xy+xy)+ci exactly)
 N_SM, LANES = 148, 128      # B200: FP32 lanes per SM (one FADD/FMUL per lane per clock)
 L2_FLUSH_BYTES = 256 << 20
 
@@ -398,7 +399,8 @@ def main():
         return
 
     # ---- roofline of the dominant kernel (ALU-bound dwell loops).  peak = the MEASURED FP32
-    # rate of the dwell step on this GPU (mandel_fp32_peak_probe: 7-op step, no escape test);
+    # rate of the dwell step on this GPU (mandel_fp32_peak_probe: the 6-instruction step, no
+    # escape test);
     # MEASURED_PEAKS.json has no FP32 entry.  The nominal 148 x 128 x f_max is reported beside.
     clocks = clk.summary()
     f_max = (clocks.get("sm_max_mhz") or 1965.0) * 1e6
@@ -423,10 +425,13 @@ def main():
                 "frac": achieved / peak_ops, "traffic": traffic,
                 "peak_nominal": nominal, "frac_nominal": achieved / nominal,
                 "launches_per_step": kt_launches[dom], "kernel_ms_per_step": kt_sum[dom],
-                "peak_basis": ("measured: mandel_fp32_peak_probe, the 7-op dwell step on 2 independent orbits per "
-                               "thread, 2048 threads/SM, no escape test (T FP32 ops/s, FADD/FMUL = 1 op); "
+                "frac_paper_7op": achieved * PAPER_OPS_PER_ITER / FLOPS_PER_ITER / peak_ops,
+                "peak_basis": ("measured: mandel_fp32_peak_probe, the dwell step (3 FMUL + 2 FADD + 1 FFMA) on 2 "
+                               "independent orbits per thread, 2048 threads/SM, no escape test (T FP32 lane-"
+                               "instructions/s, FMUL/FADD/FFMA = 1 each); "
                                f"nominal {N_SM} SMs x {LANES} lanes x {f_max/1e6:.0f} MHz beside it; "
-                               "7 ops per dwell iteration")}
+                               "6 FP32 instructions per dwell iteration executed (frac_paper_7op: the paper's "
+                               "literal 7-op step count over the same peak)")}
     # border levels: the same algorithmic-ops / measured-peak fraction (all levels together)
     if "b200_border" in kt_all and kt_all["b200_border"] > 0:
         roofline["border_frac"] = FLOPS_PER_ITER * border_iters / (kt_all["b200_border"] / 1e3) / 1e12 / peak_ops

@@ -34,7 +34,7 @@ constexpr int DWELL_K = 8;                 // iterations per escape test (dwell.
 #define MANDEL_RFB_CH 64
 #endif
 #ifndef MANDEL_RFL_K
-#define MANDEL_RFL_K 16
+#define MANDEL_RFL_K 32
 #endif
 #ifndef MANDEL_RFL_T
 #define MANDEL_RFL_T 8

@@ -2,12 +2,16 @@
 //
 // Dwell (Sec. 7): z_{i+1} = z_i^2 + c, z_0 = 0; dwell = first i >= 1 with
 // |z_i|^2 > 4, else maxdwell (R2).  Every float operation is an explicit
-// round-to-nearest intrinsic (__fmul_rn / __fadd_rn / __fsub_rn), so ptxas can never
-// contract a multiply-add into an FFMA and the integer dwell is bit-identical to any IEEE
-// binary32 implementation with the same operation order (R4):
+// round-to-nearest intrinsic (__fmul_rn / __fadd_rn / __fsub_rn / __fmaf_rn), so ptxas can
+// never contract a multiply-add into an FFMA and the integer dwell is bit-identical to any
+// IEEE binary32 implementation of the operation order of DESIGN.md R4:
 //     xy = x*y;  x = (x2 - y2) + cr;  y = (xy + xy) + ci;  x2 = x*x;  y2 = y*y
-// i.e. 3 FMUL + 4 FADD per iteration, the x2/y2 products doubling as the next iteration's
-// squares and the escape test's operands.
+// with one exact rewrite (R4'): (xy + xy) + ci is computed as fma(xy, 2, ci).  2*xy is exact,
+// so the one rounding of the fma is the second addition's; the two differ only if xy + xy
+// overflows and |ci| >= 2^103 pulls the sum back -- an orbit that escaped steps earlier, so
+// no dwell changes (pinned in tests/native/fma2_identity.c).  3 FMUL + 2 FADD + 1 FFMA
+// (immediate form) = 6 FP32 instructions per iteration instead of 7; the x2/y2 products double
+// as the next iteration's squares and the escape test's operands.
 //
 // Iterations run in unrolled chunks of K with ONE escape test per chunk ("!(mag <= 4)",
 // so inf/NaN count as escaped).  On a hit the chunk is replayed one step at a time from
@@ -39,7 +43,7 @@ __device__ __forceinline__ float pix_im(const PixMap &m, int i)
     do {                                                                                       \
         float xy_ = __fmul_rn((x), (y));                                                       \
         (x) = __fadd_rn(__fsub_rn((x2), (y2)), (cr));                                          \
-        (y) = __fadd_rn(__fadd_rn(xy_, xy_), (ci));                                            \
+        (y) = __fmaf_rn(xy_, 2.0f, (ci)); /* == (xy + xy) + ci, R4' */                        \
         (x2) = __fmul_rn((x), (x));                                                            \
         (y2) = __fmul_rn((y), (y));                                                            \
     } while (0)

@@ -673,7 +673,7 @@ int mandel_fp32_peak_probe(int32_t steps, double *tops, void *stream)
             rc = cuda_fail(e, "mandel_fp32_peak_probe");
             break;
         }
-        const double ops = 7.0 * 2 * 8 * (double)steps * blocks * 256;
+        const double ops = 6.0 * 2 * 8 * (double)steps * blocks * 256; // 6 FP32 instructions per step (R4')
         if (rep > 0 && ms > 0.0f && ops / (ms * 1e9) > best) // rep 0 warms up
             best = ops / (ms * 1e9);
     }

@@ -403,6 +403,7 @@ using mandel::f2_unpack;
 using mandel::f2_add;
 using mandel::f2_sub;
 using mandel::f2_mul;
+using mandel::f2_fma2x;
 #ifndef MANDEL3D_PK
 #define MANDEL3D_PK 32 // packed voxel engine: steps per escape test (16: V2 27.95 ms, 32: 27.53 ms)
 #endif

@@ -88,6 +88,12 @@ constexpr int RF_QCAP = 64; // per-warp queue entries (< 32 left over + < 32 new
 // Scalar engine: CKPT sub-chunks per K-step chunk.  The orbit is kept at every sub-chunk
 // boundary, so a parked point's first escape is located to one sub-chunk from the saved
 // points' |z|^2 and the replay bisects K/CKPT steps instead of K (1: plain chunks).
+#ifndef MANDEL_RF_DIRECT
+#define MANDEL_RF_DIRECT 0 // store unescaped maxdwell points at parking time (measured slower)
+#endif
+#ifndef MANDEL_RF2_CKPT
+#define MANDEL_RF2_CKPT 2 // the same for the packed engine
+#endif
 #ifndef MANDEL_RF_CKPT
 #define MANDEL_RF_CKPT 2
 #endif
@@ -154,6 +160,9 @@ __device__ __forceinline__ void replay_batch(const ParkedPoint *q, int cnt, cons
 #ifndef MANDEL_PRE_SLOTS
 #define MANDEL_PRE_SLOTS 0 // prepass raw pixels per free slot (0: a whole grab)
 #endif
+#ifndef MANDEL_PRE_COUNT
+#define MANDEL_PRE_COUNT 0 // prepass: count the steps still inside instead of latching the first escape
+#endif
 #ifndef MANDEL_PRE_MINFRAC
 #define MANDEL_PRE_MINFRAC 25u // keep the prepass while >= this % of its pixels escape in it
 #endif
@@ -194,12 +203,24 @@ __device__ __forceinline__ int rf2_prepass(uint32_t b, uint32_t e, const PixMap 
             const float cr = pix_re(pm, px), ci = pix_im(pm, py);
             if (__fadd_rn(__fmul_rn(cr, cr), __fmul_rn(ci, ci)) <= 3.9f) {
                 float x2 = 0.f, y2 = 0.f;
+#if MANDEL_PRE_COUNT
+                // escape is permanent (|c|^2 <= 3.9): the steps still inside
+                // are exactly the steps before the dwell, so dwell = (their count) + 1
+                int in = 0;
+#pragma unroll
+                for (int k = 1; k <= S; ++k) {
+                    MANDEL_STEP(x, y, x2, y2, cr, ci);
+                    in += __fadd_rn(x2, y2) <= 4.0f ? 1 : 0;
+                }
+                const int dw = in < S ? in + 1 : 0;
+#else
                 int dw = 0;
 #pragma unroll
                 for (int k = 1; k <= S; ++k) {
                     MANDEL_STEP(x, y, x2, y2, cr, ci);
                     dw = (dw == 0 && !(__fadd_rn(x2, y2) <= 4.0f)) ? k : dw;
                 }
+#endif
                 if (dw) {
                     sink(px, py, dw);
                     ++esc;
@@ -223,6 +244,28 @@ __device__ __forceinline__ int rf2_prepass(uint32_t b, uint32_t e, const PixMap 
     n_esc += __reduce_add_sync(FULL, (unsigned)esc);
     __syncwarp();
     return m;
+}
+
+// The replay window of a parked point (CKP sub-chunks of KS steps, chunk start (sx, sy, sit),
+// kept points ck[c] after (c+1)*KS steps): the sub-chunk after the last kept point not yet
+// past the first escape or maxdwell -- P(j) = "escaped by j || sit + j >= md" is monotone.
+template <int CKP, int KS>
+__device__ __forceinline__ void replay_window(float sx, float sy, unsigned sit, const float *ckx, const float *cky,
+                                              unsigned md, float &bx, float &by, unsigned &bit)
+{
+    bx = sx;
+    by = sy;
+    bit = sit;
+#pragma unroll
+    for (int c = 0; c < CKP - 1; ++c) {
+        const unsigned jc = sit + (unsigned)((c + 1) * KS);
+        const float m = __fadd_rn(__fmul_rn(ckx[c], ckx[c]), __fmul_rn(cky[c], cky[c]));
+        if (bit + (unsigned)KS == jc && m <= 4.0f && jc < md) {
+            bx = ckx[c];
+            by = cky[c];
+            bit = jc;
+        }
+    }
 }
 
 // Map: __device__ void operator()(uint32_t t, int &x, int &y) const      (t < 2^32)
@@ -289,28 +332,17 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
         // ---------------------------------------------------------------- park + refill
         const unsigned f = __ballot_sync(FULL, fin);
         if (f) {
-            // a lane that reached maxdwell unescaped (|z|^2 <= 4 at the chunk end, escape is
-            // permanent) has dwell maxdwell: stored at once, no replay
-            const bool direct = fin && endok;
+            // MANDEL_RF_DIRECT: a lane that reached maxdwell unescaped (|z|^2 <= 4 at the
+            // chunk end, escape is permanent) has dwell maxdwell: stored at once, no replay
+            const bool direct = MANDEL_RF_DIRECT && fin && endok;
             if (direct)
                 sink(px, py, (int)md);
             const bool enq = fin && !direct;
-            const unsigned fq = __ballot_sync(FULL, enq);
+            const unsigned fq = MANDEL_RF_DIRECT ? __ballot_sync(FULL, enq) : f;
             if (enq) {
-                // the replay window: the sub-chunk after the last kept point not yet past
-                // the first escape (or maxdwell), P(j) = escaped by j || sit + j >= md
-                float bx = sx, by = sy;
-                unsigned bit = sit;
-#pragma unroll
-                for (int c = 0; c < CKP - 1; ++c) {
-                    const unsigned jc = sit + (unsigned)((c + 1) * KS);
-                    const float m = __fadd_rn(__fmul_rn(ckx[c], ckx[c]), __fmul_rn(cky[c], cky[c]));
-                    if (bit + (unsigned)KS == jc && m <= 4.0f && jc < md) {
-                        bx = ckx[c];
-                        by = cky[c];
-                        bit = jc;
-                    }
-                }
+                float bx, by;
+                unsigned bit;
+                replay_window<CKP, KS>(sx, sy, sit, ckx, cky, md, bx, by, bit);
                 ParkedPoint &e = q[qn + __popc(fq & lt)];
                 e.px = px;
                 e.py = py;
@@ -503,12 +535,21 @@ __device__ __forceinline__ f2_t f2_mul(f2_t a, f2_t b)
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c_f2_negzero));
     return d;
 }
+// (xy + xy) + ci as one fma.rn.f32x2(xy, {2, 2}, ci) on both halves (R4'; the pair
+// of 2.0f from constant memory, like the -0 pair above).
+__constant__ f2_t c_f2_two = 0x4000000040000000ull;
+__device__ __forceinline__ f2_t f2_fma2x(f2_t xy, f2_t c)
+{
+    f2_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(xy), "l"(c_f2_two), "l"(c));
+    return d;
+}
 // The dwell step of dwell.cuh on both halves (same operation order).
 #define MANDEL_STEP2(X, Y, X2, Y2, CR, CI)                                                    \
     do {                                                                                       \
         const f2_t xy_ = f2_mul((X), (Y));                                                     \
         (X) = f2_add(f2_sub((X2), (Y2)), (CR));                                                \
-        (Y) = f2_add(f2_add(xy_, xy_), (CI));                                                  \
+        (Y) = f2_fma2x(xy_, (CI));                                                             \
         (X2) = f2_mul((X), (X));                                                               \
         (Y2) = f2_mul((Y), (Y));                                                               \
     } while (0)
@@ -618,42 +659,69 @@ __device__ __forceinline__ void refill_loop2(const PixMap &pm, int maxdwell, uin
     uint32_t sv_pos = 0, sv_end = 0, pre_tot = 0;
     int pre_esc = 0;
 
-    bool has0 = false, has1 = false, fin0 = false, fin1 = false;
+    constexpr int CKP = MANDEL_RF2_CKPT, KS = K / CKP; // sub-chunks (as the scalar engine's CKPT)
+    static_assert(CKP >= 1 && K % CKP == 0 && (KS & (KS - 1)) == 0, "RF2_CKPT must split K into powers of two");
+    constexpr int NCK = CKP > 1 ? CKP - 1 : 1;
+    bool has0 = false, has1 = false, fin0 = false, fin1 = false, endok0 = false, endok1 = false;
     int px0 = 0, py0 = 0, px1 = 0, py1 = 0;
     unsigned it0 = 0, it1 = 0, sit0 = 0, sit1 = 0;
     float sx0 = 0.f, sy0 = 0.f, sx1 = 0.f, sy1 = 0.f;
+    float ckx0[NCK], cky0[NCK], ckx1[NCK], cky1[NCK];
+#pragma unroll
+    for (int c = 0; c < NCK; ++c)
+        ckx0[c] = cky0[c] = ckx1[c] = cky1[c] = 0.f;
     f2_t X = 0, Y = 0, X2 = 0, Y2 = 0, CR = 0, CI = 0;
 
     while (true) {
         // ---------------------------------------------------------------- park + refill
         const unsigned f0 = __ballot_sync(FULL, fin0), f1 = __ballot_sync(FULL, fin1);
         if (f0 | f1) {
-            const int n0 = __popc(f0);
-            if (fin0) {
-                ParkedPoint &e = q[qn + __popc(f0 & lt)];
+            // MANDEL_RF_DIRECT: slots that reached maxdwell unescaped get dwell maxdwell
+            // without replay
+            const bool d0 = MANDEL_RF_DIRECT && fin0 && endok0, d1 = MANDEL_RF_DIRECT && fin1 && endok1;
+            if (d0)
+                sink(px0, py0, (int)md);
+            if (d1)
+                sink(px1, py1, (int)md);
+            const bool e0 = fin0 && !d0, e1 = fin1 && !d1;
+            const unsigned q0 = MANDEL_RF_DIRECT ? __ballot_sync(FULL, e0) : f0;
+            const unsigned q1 = MANDEL_RF_DIRECT ? __ballot_sync(FULL, e1) : f1;
+            const int n0 = __popc(q0);
+            if (e0) {
+                ParkedPoint &e = q[qn + __popc(q0 & lt)];
+                float bx, by;
+                unsigned bit;
+                replay_window<CKP, KS>(sx0, sy0, sit0, ckx0, cky0, md, bx, by, bit);
                 e.px = px0;
                 e.py = py0;
-                e.x = sx0;
-                e.y = sy0;
-                e.it = sit0;
+                e.x = bx;
+                e.y = by;
+                e.it = bit;
+            }
+            if (e1) {
+                ParkedPoint &e = q[qn + n0 + __popc(q1 & lt)];
+                float bx, by;
+                unsigned bit;
+                replay_window<CKP, KS>(sx1, sy1, sit1, ckx1, cky1, md, bx, by, bit);
+                e.px = px1;
+                e.py = py1;
+                e.x = bx;
+                e.y = by;
+                e.it = bit;
+            }
+            if (fin0) {
                 has0 = false;
                 fin0 = false;
             }
             if (fin1) {
-                ParkedPoint &e = q[qn + n0 + __popc(f1 & lt)];
-                e.px = px1;
-                e.py = py1;
-                e.x = sx1;
-                e.y = sy1;
-                e.it = sit1;
                 has1 = false;
                 fin1 = false;
             }
-            qn += n0 + __popc(f1);
+            qn += n0 + __popc(q1);
             __syncwarp();
             if (qn >= 64) {
                 qn -= 64;
-                replay_batch2<K>(q + qn, 64, pm, md, sink);
+                replay_batch2<KS>(q + qn, 64, pm, md, sink);
             }
         }
         unsigned need0 = __ballot_sync(FULL, !has0), need1 = __ballot_sync(FULL, !has1);
@@ -815,14 +883,29 @@ __device__ __forceinline__ void refill_loop2(const PixMap &pm, int maxdwell, uin
             sy1 = keep1 ? sy1 : yh;
             sit1 = keep1 ? sit1 : it1;
 #pragma unroll
-            for (int k = 0; k < K; ++k)
-                MANDEL_STEP2(X, Y, X2, Y2, CR, CI);
+            for (int c = 0; c < CKP; ++c) {
+#pragma unroll
+                for (int k = 0; k < KS; ++k)
+                    MANDEL_STEP2(X, Y, X2, Y2, CR, CI);
+                if (c < CKP - 1) {
+                    float al, ah, bl, bh;
+                    f2_unpack(X, al, ah);
+                    f2_unpack(Y, bl, bh);
+                    ckx0[c] = keep0 ? ckx0[c] : al;
+                    cky0[c] = keep0 ? cky0[c] : bl;
+                    ckx1[c] = keep1 ? ckx1[c] : ah;
+                    cky1[c] = keep1 ? cky1[c] : bh;
+                }
+            }
             it0 += K;
             it1 += K;
             float m0, m1;
             f2_unpack(f2_add(X2, Y2), m0, m1);
-            fin0 = live0 && (fin0 || !(m0 <= 4.0f) || it0 >= md);
-            fin1 = live1 && (fin1 || !(m1 <= 4.0f) || it1 >= md);
+            const bool in0 = m0 <= 4.0f, in1 = m1 <= 4.0f;
+            endok0 = fin0 ? endok0 : in0;
+            endok1 = fin1 ? endok1 : in1;
+            fin0 = live0 && (fin0 || !in0 || it0 >= md);
+            fin1 = live1 && (fin1 || !in1 || it1 >= md);
             const unsigned g0 = __ballot_sync(FULL, fin0), g1 = __ballot_sync(FULL, fin1);
             if ((g0 == a0m && g1 == a1m) || __popc(g0) + __popc(g1) >= thresh)
                 break;
@@ -831,7 +914,7 @@ __device__ __forceinline__ void refill_loop2(const PixMap &pm, int maxdwell, uin
     while (qn > 0) { // drain the queue
         const int c = qn < 64 ? qn : 64;
         qn -= c;
-        replay_batch2<K>(q + qn, c, pm, md, sink);
+        replay_batch2<KS>(q + qn, c, pm, md, sink);
     }
 #ifdef MANDEL_RF_TRACE
     if (lane == 0 && wrank < 8192 && tslot >= 0 && tslot < 16) {

@@ -63,8 +63,27 @@ def test_sass_is_sm100a():
     assert "sm_100a" in out
 
 
+def check_fma_forms(name: str, f: str):
+    """The only multiply-adds a dwell kernel may contain (R4/R4'): scalar FFMA as
+    fma(xy, 2, ci) -- immediate multiplier 2, unnegated operands -- and packed FFMA2 either as a
+    product fma(a, b, -0) whose addend is the -0 pair from constant memory (a uniform register)
+    or as fma(xy, {2, 2}, ci) whose multiplier is the 2.0 pair from constant memory; never a
+    contracted x*x - y2.  Returns the FFMA2 operand strings."""
+    for ins in re.findall(r"\bFFMA ([^;]*);", f):
+        ops = [o.strip() for o in ins.split(",")]
+        assert len(ops) == 4 and ops[2] == "2" and not any(o.startswith("-") for o in ops), (name, ins)
+    ffma2 = re.findall(r"FFMA2 ([^;]*);", f)
+    for ins in ffma2:
+        ops = [o.strip() for o in ins.split(",")]
+        product = ops[-1].startswith("UR")
+        times2 = ops[2].startswith("UR") and ops[-1].startswith("R")
+        assert (product or times2) and not any(o.startswith("-") for o in ops[1:]), (name, ins)
+    return ffma2
+
+
 def test_no_fma_in_dwell_kernels():
-    """-fmad=false + __f*_rn: the dwell loops must not contain FFMA (R4)."""
+    """-fmad=false + __f*_rn: the dwell loops contain no contracted multiply-add (DESIGN.md R4);
+    their only FFMA/FFMA2 are the exact fma(xy, 2, ci) of R4' and the packed products."""
     build.build_dp()
     sass = os.popen(f"/usr/local/cuda/bin/cuobjdump -sass {_lib.LIB_PATH} 2>&1").read()
     sass += os.popen(f"/usr/local/cuda/bin/cuobjdump -sass {_lib.DP_LIB_PATH} 2>&1").read()
@@ -74,14 +93,7 @@ def test_no_fma_in_dwell_kernels():
         name = f.split("\n", 1)[0]
         if any(k in name for k in ("k_exhaustive", "k_sbr_level", "k_sbr_leaf", "k_b200_border", "k_b200_leaf",
                                    "k_dp")):
-            # no scalar FFMA at all
-            assert re.search(r"\bFFMA\b", f) is None, name
-            # packed engine: every FFMA2 is a product fma(a, b, -0) whose addend is the
-            # -0 pair from constant memory (a uniform register), never a fused x*x - y2
-            ffma2 = re.findall(r"FFMA2 ([^;]*);", f)
-            for ins in ffma2:
-                addend = ins.split(",")[-1].strip()
-                assert addend.startswith("UR") and not addend.startswith("-"), (name, ins)
+            ffma2 = check_fma_forms(name, f)
             assert "FMUL2" not in f, name  # products only through the opaque -0 fma
             assert ("FMUL" in f and "FADD" in f) or (ffma2 and "FADD2" in f), name
             checked += 1
@@ -204,7 +216,5 @@ def test_3d_library_exports_and_validates():
     sass = os.popen(f"/usr/local/cuda/bin/cuobjdump -sass {_lib.LIB3_PATH} 2>&1").read()
     for f in re.split(r"\n\s*Function : ", sass)[1:]:
         if any(k in f.split("\n", 1)[0] for k in ("k3_surface", "k3_leaf", "k3_exhaustive")):  # incl. _rf
-            assert re.search(r"\bFFMA\b", f) is None and "FMUL" in f and "FADD" in f
-            for ins in re.findall(r"FFMA2 ([^;]*);", f):  # packed leaf: products fma(a, b, -0) only
-                addend = ins.split(",")[-1].strip()
-                assert addend.startswith("UR") and not addend.startswith("-"), ins
+            assert "FMUL" in f and "FADD" in f
+            check_fma_forms(f.split("\n", 1)[0], f)
