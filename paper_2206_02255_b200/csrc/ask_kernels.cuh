@@ -778,13 +778,15 @@ __global__ void __launch_bounds__(256) k_b200_classify(LevelArgs a_)
 {
     pdl_entry();
     const LevelArgs a = with_params(a_);
-    // threads per region: half a warp (WPR = 0: small rings, twice the regions in flight per
-    // warp at the deep levels), a warp, or WPR warps
-    constexpr int TPR = WPR == 0 ? 16 : 32 * WPR;
+    // threads per region: a quarter (WPR = -1) or half a warp (WPR = 0: small rings, more
+    // regions in flight per warp at the deep levels), a warp, or WPR warps
+    constexpr int TPR = WPR == 0 ? 16 : WPR < 0 ? 8 : 32 * WPR;
     constexpr int RPB = 256 / TPR; // regions per block round
     __shared__ int s_lo[8], s_hi[8], s_nm[8];
     __shared__ uint32_t s_base[RPB];
-    const unsigned gmask = TPR == 16 ? ((threadIdx.x & 16) ? 0xffff0000u : 0x0000ffffu) : 0xffffffffu;
+    const unsigned gmask = TPR == 8    ? 0xffu << (threadIdx.x & 24)
+                           : TPR == 16 ? ((threadIdx.x & 16) ? 0xffff0000u : 0x0000ffffu)
+                                       : 0xffffffffu;
     const uint32_t count = level_count(a);
     const int d = a.d, ring = 4 * d - 4, s = d / a.r, rr = a.r * a.r;
     const int t = threadIdx.x % TPR, w = threadIdx.x >> 5, slot = threadIdx.x / TPR;

@@ -239,6 +239,10 @@ int resident_grid(K kernel, int tpb, int sms, size_t cap_blocks)
 #ifndef MANDEL_CLASSIFY_HALF_D
 #define MANDEL_CLASSIFY_HALF_D 64
 #endif
+// ... and a quarter of a warp for sides up to this (ring <= 124 pixels; 0: never).
+#ifndef MANDEL_CLASSIFY_QUARTER_D
+#define MANDEL_CLASSIFY_QUARTER_D 32
+#endif
 
 // Launch on `s` with programmatic stream serialization (PDL, see pdl_entry()): under stream
 // capture this becomes a programmatic edge to the previous kernel node on `s`.
@@ -482,6 +486,9 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
             if (d >= 256) {
                 int gsz = resident_grid(k_b200_classify<8>, 256, sms, cap);
                 CK(launch_pdl(k_b200_classify<8>, gsz, 256, s, a));
+            } else if (d <= MANDEL_CLASSIFY_QUARTER_D) { // a quarter of a warp per region
+                int gsz = resident_grid(k_b200_classify<-1>, 256, sms, (cap + 31) / 32);
+                CK(launch_pdl(k_b200_classify<-1>, gsz, 256, s, a));
             } else if (d <= MANDEL_CLASSIFY_HALF_D) { // half a warp per region
                 int gsz = resident_grid(k_b200_classify<0>, 256, sms, (cap + 15) / 16);
                 CK(launch_pdl(k_b200_classify<0>, gsz, 256, s, a));
