@@ -35,7 +35,7 @@ def main():
         ws = mb.workspace(n, g, r, B)
         variants = [dict(scheme=s) for s in ("b200", "sbr", "mbr")] + [
             dict(flat=True), dict(serial=True), dict(groups=3), dict(stats=True), dict(tile_cost=True),
-            dict(timing=True), dict(timing="leaf")]
+            dict(tile_cost="sampled"), dict(timing=True), dict(timing="leaf")]
         for kw in variants:
             out = mb.ask(region, n, md, g, r, B, ws=ws, **kw)
             assert np.array_equal(out.cpu().numpy(), A), kw
@@ -45,6 +45,18 @@ def main():
         mb.ask(region, n, md, g, r, B, out=buf, ws=ws, tiles=tiles)
         At, _ = oracle.ask(region, n, md, g, r, B, tiles=tiles)
         assert np.array_equal(buf.cpu().numpy(), At)
+        n_ok += 1
+        # device tile list chosen by the device deal (mandel_ask_dtiles + mandel_deal_lpt)
+        costs = mb.tile_cost_view(ws, n, g, r, B).clone()
+        dt = torch.full((g * g,), -1, dtype=torch.int32, device="cuda")
+        dn = torch.zeros(1, dtype=torch.int32, device="cuda")
+        mb.deal_lpt(costs, 3, 1, dt, dn)
+        buf.fill_(-1)
+        mb.ask(region, n, md, g, r, B, out=buf, ws=ws, dtiles=(dt, dn), tile_cost="sampled")
+        torch.cuda.synchronize()
+        mine = dt[: int(dn.item())].tolist()
+        Ad, _ = oracle.ask(region, n, md, g, r, B, tiles=mine)
+        assert np.array_equal(buf.cpu().numpy(), Ad)
         n_ok += 1
         if not os.environ.get("SANITIZE_NO_DP"):  # racecheck/synccheck/initcheck cannot follow CDP
             assert np.array_equal(mb.dp(region, n, md, g, r, B).cpu().numpy(), A)
