@@ -41,7 +41,7 @@ def main():
         exact = mb.tile_costs(ws, w.g)
         heavy = max(deal.deal("lpt", w.g, 8, exact), key=lambda p: sum(exact[k] for k in p))
         res = {"w": nm}
-        for G in (1, 2, 4):
+        for G in (1, 2, 3, 4):
             res[f"rank8_G{G}"] = ev(lambda: mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws,
                                                    tiles=heavy, groups=G), flush)
             res[f"full_G{G}"] = ev(lambda: mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws,
