@@ -990,7 +990,7 @@ struct BorderMap {
 // when the low word wraps (exact for any total); flushed once per block.  A 64-bit shared
 // atomicAdd compiles to a CAS spin loop on sm_100 (measured: the counting pass cost 30% more
 // than the plain step with it).
-constexpr int TC_SMEM = 1024;
+constexpr int TC_SMEM = MANDEL_SV_C ? 1008 : 1024; // (SV_C: the leaf kernel stays below 48 KB of static shared memory)
 struct TileCostSmem {
     unsigned lo[TC_SMEM], hi[TC_SMEM];
 };

@@ -161,16 +161,23 @@ __device__ __forceinline__ void replay_batch(const ParkedPoint *q, int cnt, cons
 #define MANDEL_PRE_SLOTS 0 // prepass raw pixels per free slot (0: a whole grab)
 #endif
 #ifndef MANDEL_PRE_COUNT
-#define MANDEL_PRE_COUNT 0 // prepass: count the steps still inside instead of latching the first escape
+#define MANDEL_PRE_COUNT 2 // prepass escape test: 0 latch the first escape, 1 integer count, 2 float count
 #endif
 #ifndef MANDEL_PRE_MINFRAC
 #define MANDEL_PRE_MINFRAC 25u // keep the prepass while >= this % of its pixels escape in it
 #endif
 // A prepass survivor: pixel and its orbit after S steps (x2, y2 are x*x, y*y again).
+#ifndef MANDEL_SV_C
+#define MANDEL_SV_C 1 // prepass survivors keep c, so dealing them does not recompute it
+#endif
 struct SvPoint {
     uint32_t pxy; // x | y << 16
     float x, y;
+#if MANDEL_SV_C
+    float cr, ci; // 20 bytes: the leaf kernel's static shared memory stays below 48 KB
+#else
     uint32_t pad;
+#endif
 };
 
 // Short-pixel prepass (PRE = S > 0): every grab of raw indices is first run
@@ -196,6 +203,9 @@ __device__ __forceinline__ int rf2_prepass(uint32_t b, uint32_t e, const PixMap 
         bool surv = false;
         uint32_t pxy = 0;
         float x = 0.f, y = 0.f;
+#if MANDEL_SV_C
+        float svcr = 0.f, svci = 0.f;
+#endif
         if (t < e) {
             int px, py;
             map(t, px, py);
@@ -203,7 +213,7 @@ __device__ __forceinline__ int rf2_prepass(uint32_t b, uint32_t e, const PixMap 
             const float cr = pix_re(pm, px), ci = pix_im(pm, py);
             if (__fadd_rn(__fmul_rn(cr, cr), __fmul_rn(ci, ci)) <= 3.9f) {
                 float x2 = 0.f, y2 = 0.f;
-#if MANDEL_PRE_COUNT
+#if MANDEL_PRE_COUNT == 1
                 // escape is permanent (|c|^2 <= 3.9): the steps still inside
                 // are exactly the steps before the dwell, so dwell = (their count) + 1
                 int in = 0;
@@ -212,6 +222,16 @@ __device__ __forceinline__ int rf2_prepass(uint32_t b, uint32_t e, const PixMap 
                     MANDEL_STEP(x, y, x2, y2, cr, ci);
                     in += __fadd_rn(x2, y2) <= 4.0f ? 1 : 0;
                 }
+                const int dw = in < S ? in + 1 : 0;
+#elif MANDEL_PRE_COUNT == 2
+                // the same count kept in a float (1.0 / 0.0 per step: exact for S < 2^24)
+                float inf_ = 0.0f;
+#pragma unroll
+                for (int k = 1; k <= S; ++k) {
+                    MANDEL_STEP(x, y, x2, y2, cr, ci);
+                    inf_ = __fadd_rn(inf_, __fadd_rn(x2, y2) <= 4.0f ? 1.0f : 0.0f);
+                }
+                const int in = (int)inf_;
                 const int dw = in < S ? in + 1 : 0;
 #else
                 int dw = 0;
@@ -226,6 +246,10 @@ __device__ __forceinline__ int rf2_prepass(uint32_t b, uint32_t e, const PixMap 
                     ++esc;
                 } else {
                     surv = true;
+#if MANDEL_SV_C
+                    svcr = cr;
+                    svci = ci;
+#endif
                 }
             } else { // per-step loop (escape permanence not guaranteed)
                 sink(px, py, dwell_per_step<S>(cr, ci, maxdwell));
@@ -238,6 +262,10 @@ __device__ __forceinline__ int rf2_prepass(uint32_t b, uint32_t e, const PixMap 
             o.pxy = pxy;
             o.x = x;
             o.y = y;
+#if MANDEL_SV_C
+            o.cr = svcr;
+            o.ci = svci;
+#endif
         }
         m += __popc(sm);
     }
@@ -771,12 +799,17 @@ __device__ __forceinline__ void refill_loop2(const PixMap &pm, int maxdwell, uin
                     const SvPoint p = sv[sv_pos + r0];
                     px0 = (int)(p.pxy & 0xffffu);
                     py0 = (int)(p.pxy >> 16);
+#if MANDEL_SV_C
+                    cr0 = p.cr;
+                    ci0 = p.ci;
+#else
                     cr0 = pix_re(pm, px0);
                     ci0 = pix_im(pm, py0);
-                    xa0 = p.x;
-                    ya0 = p.y;
+#endif
                     qa0 = __fmul_rn(p.x, p.x);
                     wa0 = __fmul_rn(p.y, p.y);
+                    xa0 = p.x;
+                    ya0 = p.y;
                     it0 = (unsigned)PRE;
                     has0 = true;
                 }
@@ -784,12 +817,17 @@ __device__ __forceinline__ void refill_loop2(const PixMap &pm, int maxdwell, uin
                     const SvPoint p = sv[sv_pos + r1];
                     px1 = (int)(p.pxy & 0xffffu);
                     py1 = (int)(p.pxy >> 16);
+#if MANDEL_SV_C
+                    cr1 = p.cr;
+                    ci1 = p.ci;
+#else
                     cr1 = pix_re(pm, px1);
                     ci1 = pix_im(pm, py1);
-                    xa1 = p.x;
-                    ya1 = p.y;
+#endif
                     qa1 = __fmul_rn(p.x, p.x);
                     wa1 = __fmul_rn(p.y, p.y);
+                    xa1 = p.x;
+                    ya1 = p.y;
                     it1 = (unsigned)PRE;
                     has1 = true;
                 }
