@@ -296,6 +296,61 @@ __device__ __forceinline__ void replay_window(float sx, float sy, unsigned sit, 
     }
 }
 
+// Second prepass stage (MANDEL_PRE2 = S2 > 0): the survivors of rf2_prepass<S1> (orbit at
+// iteration S1 in sv[0, m)) run S2 more steps, one per lane, 32 at a time, with the same
+// counted escape test; the ones that escape are stored (dwell S1 + count + 1) and the rest are
+// compacted in place (orbit at iteration S1 + S2).  Returns the new survivor count.
+#ifndef MANDEL_PRE2
+#define MANDEL_PRE2 16
+#endif
+template <int S1, int S2, class Sink>
+__device__ __forceinline__ int rf2_prepass_more(SvPoint *sv, int m, const PixMap &pm, Sink &sink, int &n_esc)
+{
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    int m2 = 0, esc = 0;
+    for (int r0 = 0; r0 < m; r0 += 32) {
+        const bool valid = r0 + lane < m;
+        SvPoint p;
+        p.pxy = 0u;
+        p.x = p.y = 0.0f;
+        if (valid)
+            p = sv[r0 + lane];
+        bool surv = false;
+        if (valid) {
+#if MANDEL_SV_C
+            const float cr = p.cr, ci = p.ci;
+#else
+            const float cr = pix_re(pm, (int)(p.pxy & 0xffffu)), ci = pix_im(pm, (int)(p.pxy >> 16));
+#endif
+            float x = p.x, y = p.y, x2 = __fmul_rn(x, x), y2 = __fmul_rn(y, y);
+            float inf_ = 0.0f;
+#pragma unroll
+            for (int k = 1; k <= S2; ++k) {
+                MANDEL_STEP(x, y, x2, y2, cr, ci);
+                inf_ = __fadd_rn(inf_, __fadd_rn(x2, y2) <= 4.0f ? 1.0f : 0.0f);
+            }
+            const int in = (int)inf_;
+            if (in < S2) {
+                sink((int)(p.pxy & 0xffffu), (int)(p.pxy >> 16), S1 + in + 1);
+                ++esc;
+            } else {
+                surv = true;
+                p.x = x;
+                p.y = y;
+            }
+        }
+        const unsigned sm = __ballot_sync(FULL, surv); // every lane has read its entry
+        if (surv)
+            sv[m2 + __popc(sm & lt)] = p;
+        m2 += __popc(sm);
+    }
+    n_esc += __reduce_add_sync(FULL, (unsigned)esc);
+    __syncwarp();
+    return m2;
+}
+
 // Map: __device__ void operator()(uint32_t t, int &x, int &y) const      (t < 2^32)
 // Sink: __device__ void operator()(int x, int y, int v)                   (store + stats)
 // q: this warp's RF_QCAP-entry queue in shared memory.
@@ -690,6 +745,7 @@ __device__ __forceinline__ void refill_loop2(const PixMap &pm, int maxdwell, uin
     constexpr int CKP = MANDEL_RF2_CKPT, KS = K / CKP; // sub-chunks (as the scalar engine's CKPT)
     static_assert(CKP >= 1 && K % CKP == 0 && (KS & (KS - 1)) == 0, "RF2_CKPT must split K into powers of two");
     constexpr int NCK = CKP > 1 ? CKP - 1 : 1;
+    unsigned sv_it = PRE; // warp-uniform: iteration of the buffered survivors' orbits
     bool has0 = false, has1 = false, fin0 = false, fin1 = false, endok0 = false, endok1 = false;
     int px0 = 0, py0 = 0, px1 = 0, py1 = 0;
     unsigned it0 = 0, it1 = 0, sit0 = 0, sit1 = 0;
@@ -774,6 +830,17 @@ __device__ __forceinline__ void refill_loop2(const PixMap &pm, int maxdwell, uin
                 const uint32_t e = (uint32_t)min(b + (unsigned long long)gpre, (unsigned long long)total);
                 sv_pos = 0;
                 sv_end = (uint32_t)rf2_prepass<PRE>((uint32_t)b, e, pm, maxdwell, map, sink, sv, pre_esc);
+                if constexpr (MANDEL_PRE2 > 0) {
+                    // the second stage on every grab's survivors (measured: C3/C4 leaf -3%, C5
+                    // +1%; gating it by the first stage's or by its own recent escape fraction
+                    // lost most of the C3/C4 gain, profiles/r02_ab_prepass2.jsonl)
+                    sv_it = PRE;
+                    if (maxdwell > PRE + MANDEL_PRE2 && sv_end > 0) {
+                        int esc2 = 0;
+                        sv_end = (uint32_t)rf2_prepass_more<PRE, MANDEL_PRE2>(sv, (int)sv_end, pm, sink, esc2);
+                        sv_it = PRE + MANDEL_PRE2;
+                    }
+                }
                 pre_tot += e - (uint32_t)b;
                 if (pre_tot >= MANDEL_PRE_WINDOW) { // windowed: the list runs hot (long) leaves first
                     use_pre = MANDEL_PRE_MINFRAC * pre_tot <= 100u * (uint32_t)pre_esc;
@@ -810,7 +877,7 @@ __device__ __forceinline__ void refill_loop2(const PixMap &pm, int maxdwell, uin
                     wa0 = __fmul_rn(p.y, p.y);
                     xa0 = p.x;
                     ya0 = p.y;
-                    it0 = (unsigned)PRE;
+                    it0 = sv_it;
                     has0 = true;
                 }
                 if (!has1 && r1 < take) {
@@ -828,7 +895,7 @@ __device__ __forceinline__ void refill_loop2(const PixMap &pm, int maxdwell, uin
                     wa1 = __fmul_rn(p.y, p.y);
                     xa1 = p.x;
                     ya1 = p.y;
-                    it1 = (unsigned)PRE;
+                    it1 = sv_it;
                     has1 = true;
                 }
                 CR = f2_pack(cr0, cr1);
