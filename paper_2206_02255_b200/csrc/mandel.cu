@@ -236,6 +236,9 @@ int resident_grid(K kernel, int tpb, int sms, size_t cap_blocks)
 }
 
 // Classification uses half a warp per region for region sides up to this (ring <= 252 pixels).
+#ifndef MANDEL_CLASSIFY_BLOCK_D // classification: a whole block per region from this side up
+#define MANDEL_CLASSIFY_BLOCK_D 1024 // (256: C3 7.74 ms, 512: 7.71, 1024: 7.69; profiles/r02_ab_classify_block.jsonl)
+#endif
 #ifndef MANDEL_CLASSIFY_HALF_D
 #define MANDEL_CLASSIFY_HALF_D 64
 #endif
@@ -483,7 +486,7 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
             CK(cudaGetLastError());
             TEND(MANDEL_KIND_B200_BORDER, l, s);
             TBEGIN(s);
-            if (d >= 256) {
+            if (d >= MANDEL_CLASSIFY_BLOCK_D) { // a whole block per region
                 int gsz = resident_grid(k_b200_classify<8>, 256, sms, cap);
                 CK(launch_pdl(k_b200_classify<8>, gsz, 256, s, a));
             } else if (d <= MANDEL_CLASSIFY_QUARTER_D) { // a quarter of a warp per region
