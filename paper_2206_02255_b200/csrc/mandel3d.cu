@@ -408,6 +408,12 @@ using mandel::f2_fma2x;
 #define MANDEL3D_PK 32 // packed voxel engine: steps per escape test (16: V2 27.95 ms, 32: 27.53 ms)
 #endif
 constexpr int PK = MANDEL3D_PK, PT = 8, PCH = 128, PPRE = 16, PMINB = 3;
+#ifndef MANDEL3D_PRE_COUNT
+#define MANDEL3D_PRE_COUNT 1 // prepass escape test: 0 latch the first escape, 1 float count
+#endif
+#ifndef MANDEL3D_PRE2
+#define MANDEL3D_PRE2 16 // second prepass stage on the survivors (steps; 0: none)
+#endif
 
 template <class Sink>
 __device__ __forceinline__ void replay3_2(const Args &a, const Park3 *q, int cnt, unsigned md, Sink &sink)
@@ -479,12 +485,25 @@ __device__ __forceinline__ int prepass3(const Args &a, uint32_t b, uint32_t e, c
             if (__fadd_rn(__fmul_rn(cr, cr), __fmul_rn(ci, ci)) <= 3.9f) {
                 x = w;
                 float x2 = __fmul_rn(w, w), y2 = 0.f;
+#if MANDEL3D_PRE_COUNT
+                // the 2-D leaf prepass's counted test (refill.cuh): escape is permanent, so the
+                // steps still inside are the steps before the dwell
+                float inf_ = 0.0f;
+#pragma unroll
+                for (int k = 1; k <= PPRE; ++k) {
+                    MANDEL_STEP(x, y, x2, y2, cr, ci);
+                    inf_ = __fadd_rn(inf_, __fadd_rn(x2, y2) <= 4.0f ? 1.0f : 0.0f);
+                }
+                const int in_ = (int)inf_;
+                const int dw = in_ < PPRE ? in_ + 1 : 0;
+#else
                 int dw = 0;
 #pragma unroll
                 for (int k = 1; k <= PPRE; ++k) {
                     MANDEL_STEP(x, y, x2, y2, cr, ci);
                     dw = (dw == 0 && !(__fadd_rn(x2, y2) <= 4.0f)) ? k : dw;
                 }
+#endif
                 if (dw)
                     sink(o, dw);
                 else
@@ -505,6 +524,54 @@ __device__ __forceinline__ int prepass3(const Args &a, uint32_t b, uint32_t e, c
     }
     __syncwarp();
     return m;
+}
+
+// Second prepass stage (MANDEL3D_PRE2 = S2 > 0, as refill.cuh rf2_prepass_more): the
+// survivors in sv[0, m) run S2 more counted steps, one per lane; escaped voxels are stored,
+// the rest compacted in place with their iteration advanced.  Returns the survivor count.
+template <int S2, class Sink>
+__device__ __forceinline__ int prepass3_more(const Args &a, Park3 *sv, int m, Sink &sink)
+{
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    int m2 = 0;
+    for (int r0 = 0; r0 < m; r0 += 32) {
+        const bool valid = r0 + lane < m;
+        Park3 p;
+        p.o = 0u;
+        p.x = p.y = 0.f;
+        p.it = 0u;
+        if (valid)
+            p = sv[r0 + lane];
+        bool surv = false;
+        if (valid) {
+            float cr, ci, w;
+            voxel_c(a, p.o, cr, ci, w);
+            float x = p.x, y = p.y, x2 = __fmul_rn(x, x), y2 = __fmul_rn(y, y);
+            float inf_ = 0.0f;
+#pragma unroll
+            for (int k = 1; k <= S2; ++k) {
+                MANDEL_STEP(x, y, x2, y2, cr, ci);
+                inf_ = __fadd_rn(inf_, __fadd_rn(x2, y2) <= 4.0f ? 1.0f : 0.0f);
+            }
+            const int in_ = (int)inf_;
+            if (in_ < S2) {
+                sink(p.o, (int)p.it + in_ + 1);
+            } else {
+                surv = true;
+                p.x = x;
+                p.y = y;
+                p.it += (unsigned)S2;
+            }
+        }
+        const unsigned sm = __ballot_sync(FULL, surv); // every lane has read its record
+        if (surv)
+            sv[m2 + __popc(sm & lt)] = p;
+        m2 += __popc(sm);
+    }
+    __syncwarp();
+    return m2;
 }
 
 template <class Map, class Sink>
@@ -578,6 +645,10 @@ __device__ __forceinline__ void refill3_packed(const Args &a, unsigned long long
                 const uint32_t e = (uint32_t)min(b + (unsigned long long)grab, (unsigned long long)total);
                 sv_pos = 0;
                 sv_end = (uint32_t)prepass3(a, (uint32_t)b, e, map, sink, sv);
+                if constexpr (MANDEL3D_PRE2 > 0) {
+                    if (a.maxdwell > PPRE + MANDEL3D_PRE2 && sv_end > 0)
+                        sv_end = (uint32_t)prepass3_more<MANDEL3D_PRE2>(a, sv, (int)sv_end, sink);
+                }
                 continue;
             }
             // slots from the survivor buffer, or (no prepass) straight from the cursor
