@@ -222,6 +222,17 @@ int mandel_ask_to_host(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g
                        int32_t *d_out, int64_t out_pitch, void *d_ws, size_t ws_bytes,
                        int32_t *h_out, void *stream);
 
+/* mandel_ask_to_host with a 16-bit host image: the same call and pipeline, but every finished
+ * band (or tile) is first narrowed on the device into d_stage -- caller-owned DEVICE buffer of
+ * n*n uint16, row pitch n -- and the copy reads d_stage, so the host receives n*n uint16
+ * (h_out, row pitch n; ideally pinned) and PCIe carries half the bytes.  Dwells lie in
+ * [1, maxdwell], so the narrowing is exact; maxdwell > 65535 or a NULL d_stage is
+ * MANDEL_EINVAL.  d_out still receives the int32 image. */
+int mandel_ask_to_host_u16(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, int32_t r,
+                           int32_t B, const int32_t *h_tile_ids, int32_t n_tiles, int32_t scheme,
+                           int32_t *d_out, int64_t out_pitch, void *d_ws, size_t ws_bytes,
+                           uint16_t *d_stage, uint16_t *h_out, void *stream);
+
 /* Per-level statistics of the last call that used d_ws (synchronises `stream`).
  * Writes min(levels, max_levels) entries; returns the number of levels (>= 0) or -code. */
 int mandel_ask_last_stats(const void *d_ws, mandel_level_stats *h_out, int32_t max_levels,

@@ -187,14 +187,34 @@ def ask_stats(ws, stream=None) -> List[dict]:
         return _lib.stats(ws.data_ptr(), _stream_ptr(stream))
 
 
-def ask_to_host(region, n, maxdwell, g, r, B, h_out, out, ws, tiles=None, scheme="b200", stream=None):
-    """ASK through the C ABI into HOST memory h_out (n x n int32, ideally pinned)."""
+def ask_to_host(region, n, maxdwell, g, r, B, h_out, out, ws, tiles=None, scheme="b200", stream=None,
+                stage=None):
+    """ASK through the C ABI into HOST memory h_out (n x n, ideally pinned).  h_out int32:
+    mandel_ask_to_host.  h_out uint16 (or int16 holding the same bits): mandel_ask_to_host_u16,
+    which narrows each finished band on the device into `stage` (n*n 16-bit device tensor,
+    allocated here if None) and copies half the bytes; needs maxdwell <= 65535."""
     torch = _torch()
-    if h_out.dtype != torch.int32 or h_out.is_cuda or not h_out.is_contiguous() or h_out.numel() < n * n:
-        raise ValueError("h_out must be a contiguous host int32 tensor of n*n elements")
-    _check_device(out, ws, stream=stream)
+    u16 = h_out.dtype in (torch.uint16, torch.int16)
+    if (h_out.dtype != torch.int32 and not u16) or h_out.is_cuda or not h_out.is_contiguous() \
+            or h_out.numel() < n * n:
+        raise ValueError("h_out must be a contiguous host int32 or uint16 tensor of n*n elements")
+    _check_device(out, ws, stage, stream=stream)
     t_ptr, t_n, _keep = _lib.tiles_arg(tiles)
     with torch.cuda.device(out.device):
+        if u16:
+            if stage is None:
+                stage = torch.empty(n * n, dtype=torch.int16, device=out.device)
+                if stream is not None and stream != torch.cuda.current_stream():
+                    stage.record_stream(stream)
+            elif stage.dtype not in (torch.uint16, torch.int16) or stage.numel() < n * n \
+                    or not stage.is_contiguous():
+                raise ValueError("stage must be a contiguous 16-bit device tensor of n*n elements")
+            rc = _lib.load().mandel_ask_to_host_u16(_lib.region(region), n, maxdwell, g, r, B, t_ptr, t_n,
+                                                    SCHEMES[scheme], out.data_ptr(), out.stride(0), ws.data_ptr(),
+                                                    ws.numel(), stage.data_ptr(), h_out.data_ptr(),
+                                                    _stream_ptr(stream))
+            _lib.check(rc, "mandel_ask_to_host_u16")
+            return h_out
         rc = _lib.load().mandel_ask_to_host(_lib.region(region), n, maxdwell, g, r, B, t_ptr, t_n,
                                             SCHEMES[scheme], out.data_ptr(), out.stride(0), ws.data_ptr(),
                                             ws.numel(), h_out.data_ptr(), _stream_ptr(stream))

@@ -82,6 +82,9 @@ _SIGS = [
     ("mandel_ask_to_host", ctypes.c_int, [MandelRegion, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                           ctypes.c_int32, ctypes.c_int32, _P, ctypes.c_int32, ctypes.c_int32, _P,
                                           ctypes.c_int64, _P, ctypes.c_size_t, _P, _P]),
+    ("mandel_ask_to_host_u16", ctypes.c_int, [MandelRegion, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                              ctypes.c_int32, ctypes.c_int32, _P, ctypes.c_int32, ctypes.c_int32,
+                                              _P, ctypes.c_int64, _P, ctypes.c_size_t, _P, _P, _P]),
     ("mandel_ask_last_stats", ctypes.c_int, [_P, ctypes.POINTER(MandelLevelStats), ctypes.c_int32, _P]),
     ("mandel_ask_kernel_count", ctypes.c_int32, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                                  ctypes.c_int32]),

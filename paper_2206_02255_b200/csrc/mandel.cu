@@ -985,25 +985,89 @@ int mandel_ask(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, int32_
                             ws_bytes, stream);
 }
 
-int mandel_ask_to_host(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, int32_t r, int32_t B,
-                       const int32_t *h_tile_ids, int32_t n_tiles, int32_t scheme, int32_t *d_out, int64_t out_pitch,
-                       void *d_ws, size_t ws_bytes, int32_t *h_out, void *stream)
+} // extern "C"
+
+namespace {
+
+// u16 host images (mandel_ask_to_host_u16): dst[y][x] = (uint16_t)src[y][x] over the rectangle
+// rows [y0, y0+rows) x columns [x0, x0+cols), both buffers addressed with their own pitch
+// (elements).  Every dwell is in [1, maxdwell] and maxdwell <= 65535 is checked by the caller,
+// so the narrowing is exact.  Four pixels per thread (int4 load, 8-byte store) when the
+// rectangle and both pitches are multiples of 4, else one.
+__global__ void __launch_bounds__(256) k_to_u16(const int32_t *__restrict__ src, int64_t src_pitch,
+                                                uint16_t *__restrict__ dst, int64_t dst_pitch, int64_t y0,
+                                                int64_t rows, int64_t x0, int64_t cols, int vec)
 {
-    if (!h_out)
+    const int64_t per_row = vec ? cols / 4 : cols;
+    const int64_t total = rows * per_row;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t y = y0 + t / per_row, c = t % per_row;
+        if (vec) {
+            const int64_t x = x0 + 4 * c;
+            const int4 v = __ldcs(reinterpret_cast<const int4 *>(src + y * src_pitch + x));
+            uint2 o;
+            o.x = (uint32_t)(v.x & 0xffff) | ((uint32_t)v.y << 16);
+            o.y = (uint32_t)(v.z & 0xffff) | ((uint32_t)v.w << 16);
+            *reinterpret_cast<uint2 *>(dst + y * dst_pitch + x) = o;
+        } else {
+            const int64_t x = x0 + c;
+            dst[y * dst_pitch + x] = (uint16_t)src[y * src_pitch + x];
+        }
+    }
+}
+
+int to_u16(const int32_t *src, int64_t src_pitch, uint16_t *dst, int64_t dst_pitch, int64_t y0, int64_t rows,
+           int64_t x0, int64_t cols, int sms, cudaStream_t s)
+{
+    const int vec = (x0 % 4 == 0 && cols % 4 == 0 && src_pitch % 4 == 0 && dst_pitch % 4 == 0 &&
+                     ((uintptr_t)src & 15) == 0 && ((uintptr_t)dst & 7) == 0);
+    const int64_t work = rows * (vec ? cols / 4 : cols);
+    int64_t grid = (work + 255) / 256;
+    const int64_t cap = (int64_t)sms * 8;
+    grid = grid < 1 ? 1 : (grid > cap ? cap : grid);
+    k_to_u16<<<(unsigned)grid, 256, 0, s>>>(src, src_pitch, dst, dst_pitch, y0, rows, x0, cols, vec);
+    CK(cudaGetLastError());
+    return MANDEL_OK;
+}
+
+// mandel_ask_to_host (T = int32_t: d_stage unused) and mandel_ask_to_host_u16 (T = uint16_t:
+// each finished band or tile is narrowed into d_stage, pitch n, on the copy stream, and the
+// copy reads d_stage -- half the PCIe bytes).
+template <typename T>
+int ask_to_host_impl(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, int32_t r, int32_t B,
+                     const int32_t *h_tile_ids, int32_t n_tiles, int32_t scheme, int32_t *d_out, int64_t out_pitch,
+                     void *d_ws, size_t ws_bytes, uint16_t *d_stage, T *h_out, void *stream)
+{
+    constexpr bool U16 = sizeof(T) == 2;
+    if (!h_out || (U16 && (!d_stage || maxdwell > 65535)))
         return MANDEL_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
+    const size_t E = sizeof(T);
     if (h_tile_ids) { // only the tiles' pixels: one 2-D copy per tile
         int rc = mandel_ask_tiles(reg, n, maxdwell, g, r, B, h_tile_ids, n_tiles, scheme, 0u, d_out, out_pitch, d_ws,
                                   ws_bytes, stream);
         if (rc)
             return rc;
+        int dev = 0, sms = 148;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         const int64_t d0 = n / g;
         for (int32_t i = 0; i < n_tiles; ++i) {
             const int64_t gy = h_tile_ids[i] / g, gx = h_tile_ids[i] % g;
             const size_t off_h = (size_t)(gy * d0) * (size_t)n + (size_t)(gx * d0);
             const size_t off_d = (size_t)(gy * d0) * (size_t)out_pitch + (size_t)(gx * d0);
-            CK(cudaMemcpy2DAsync(h_out + off_h, (size_t)n * 4, d_out + off_d, (size_t)out_pitch * 4,
-                                 (size_t)d0 * 4, (size_t)d0, cudaMemcpyDeviceToHost, st));
+            const void *src = d_out + off_d;
+            size_t spitch = (size_t)out_pitch * 4;
+            if (U16) {
+                rc = to_u16(d_out, out_pitch, d_stage, n, gy * d0, d0, gx * d0, d0, sms, st);
+                if (rc)
+                    return rc;
+                src = d_stage + off_h;
+                spitch = (size_t)n * 2;
+            }
+            CK(cudaMemcpy2DAsync(h_out + off_h, (size_t)n * E, src, spitch, (size_t)d0 * E, (size_t)d0,
+                                 cudaMemcpyDeviceToHost, st));
         }
         CK(cudaStreamSynchronize(st));
         return MANDEL_OK;
@@ -1044,17 +1108,48 @@ int mandel_ask_to_host(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g
             return rc;
         CK(cudaEventRecord(di->band[b], st));
         CK(cudaStreamWaitEvent(di->copy, di->band[b], 0));
-        const int64_t y1 = (int64_t)(b + 1) * rows_per_band * d0;
-        for (int64_t y = (int64_t)b * rows_per_band * d0; y < y1; y += chunk_rows) {
+        const int64_t y0 = (int64_t)b * rows_per_band * d0, y1 = (int64_t)(b + 1) * rows_per_band * d0;
+        if (U16) {
+            rc = to_u16(d_out, out_pitch, d_stage, n, y0, y1 - y0, 0, n, di->sms, di->copy);
+            if (rc)
+                return rc;
+        }
+        for (int64_t y = y0; y < y1; y += chunk_rows) {
             const int64_t rows = y + chunk_rows <= y1 ? chunk_rows : y1 - y;
-            CK(cudaMemcpy2DAsync(h_out + (size_t)y * (size_t)n, (size_t)n * 4, d_out + (size_t)y * (size_t)out_pitch,
-                                 (size_t)out_pitch * 4, (size_t)n * 4, (size_t)rows, cudaMemcpyDeviceToHost, di->copy));
+            if (U16)
+                CK(cudaMemcpyAsync(h_out + (size_t)y * (size_t)n, d_stage + (size_t)y * (size_t)n,
+                                   (size_t)rows * (size_t)n * 2, cudaMemcpyDeviceToHost, di->copy));
+            else
+                CK(cudaMemcpy2DAsync(h_out + (size_t)y * (size_t)n, (size_t)n * 4,
+                                     d_out + (size_t)y * (size_t)out_pitch, (size_t)out_pitch * 4, (size_t)n * 4,
+                                     (size_t)rows, cudaMemcpyDeviceToHost, di->copy));
         }
     }
     CK(cudaEventRecord(di->copied, di->copy));
     CK(cudaStreamWaitEvent(st, di->copied, 0));
     CK(cudaStreamSynchronize(st));
     return MANDEL_OK;
+}
+
+} // namespace
+
+extern "C" {
+
+int mandel_ask_to_host(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, int32_t r, int32_t B,
+                       const int32_t *h_tile_ids, int32_t n_tiles, int32_t scheme, int32_t *d_out, int64_t out_pitch,
+                       void *d_ws, size_t ws_bytes, int32_t *h_out, void *stream)
+{
+    return ask_to_host_impl<int32_t>(reg, n, maxdwell, g, r, B, h_tile_ids, n_tiles, scheme, d_out, out_pitch, d_ws,
+                                     ws_bytes, nullptr, h_out, stream);
+}
+
+int mandel_ask_to_host_u16(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, int32_t r, int32_t B,
+                           const int32_t *h_tile_ids, int32_t n_tiles, int32_t scheme, int32_t *d_out,
+                           int64_t out_pitch, void *d_ws, size_t ws_bytes, uint16_t *d_stage, uint16_t *h_out,
+                           void *stream)
+{
+    return ask_to_host_impl<uint16_t>(reg, n, maxdwell, g, r, B, h_tile_ids, n_tiles, scheme, d_out, out_pitch, d_ws,
+                                      ws_bytes, d_stage, h_out, stream);
 }
 
 int mandel_ask_last_stats(const void *d_ws, mandel_level_stats *h_out, int32_t max_levels, void *stream)

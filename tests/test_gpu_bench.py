@@ -34,7 +34,7 @@ def test_bench_single_gpu_c1():
     assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3
     assert d["value"] > 0 and d["unit"] == "Mpixel/s" and d["gpu_launches"] > 0
     assert d["roofline"]["bound"] == "alu" and 0 < d["roofline"]["frac"] < 1.05
-    assert d["e2e"]["d2h_bytes_per_step"] == 4 * 1024 * 1024
+    assert d["e2e"]["d2h_bytes_per_step"] == 2 * 1024 * 1024  # 16-bit host image
 
 
 def test_bench_two_ranks_gloo_c1():

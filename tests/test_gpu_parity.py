@@ -219,6 +219,44 @@ def test_ask_to_host_banded(mb, n, g, r, B, md):
     assert np.array_equal(h.numpy().reshape(n, n), A)
 
 
+@pytest.mark.parametrize("n,g,r,B,md,pad", [(2048, 16, 2, 16, 700, 4), (1024, 2, 4, 8, 300, 0),
+                                            (512, 8, 8, 4, 900, 3), (256, 4, 2, 8, 65535, 0)])
+def test_ask_to_host_u16(mb, n, g, r, B, md, pad):
+    """The 16-bit host image (mandel_ask_to_host_u16): every pixel equals the oracle's dwell,
+    for the banded whole image and for a tile subset, with pitched device buffers (scalar
+    narrowing path) and unpitched ones (vector path), up to maxdwell 65535."""
+    ws = mb.workspace(n, g, r, B)
+    out = torch.full((n, n + pad), -3, dtype=torch.int32, device="cuda")
+    stage = torch.full((n * n,), -1, dtype=torch.int16, device="cuda")
+    h = torch.full((n * n,), 7, dtype=torch.uint16).pin_memory()
+    mb.ask_to_host(W.SEAHORSE_REGION, n, md, g, r, B, h, out, ws, stage=stage)
+    A, _ = oracle.ask(W.SEAHORSE_REGION, n, md, g, r, B)
+    assert np.array_equal(h.numpy().reshape(n, n).astype(np.int64), A)
+    tiles = _sample_tiles(g, max(1, g * g // 3), seed=5)
+    h2 = torch.zeros((n * n,), dtype=torch.uint16).pin_memory()
+    mb.ask_to_host(W.SEAHORSE_REGION, n, md, g, r, B, h2, out, ws, tiles=tiles)
+    got = h2.numpy().reshape(n, n).astype(np.int64)
+    d0 = n // g
+    for t in range(g * g):
+        ty, tx = divmod(t, g)
+        sl = (slice(ty * d0, (ty + 1) * d0), slice(tx * d0, (tx + 1) * d0))
+        if t in tiles:
+            assert np.array_equal(got[sl], A[sl]), t
+        else:
+            assert not got[sl].any(), t
+
+
+def test_ask_to_host_u16_rejects(mb):
+    """maxdwell > 65535 does not fit the 16-bit image: MANDEL_EINVAL, nothing written."""
+    n, g, r, B = 128, 2, 2, 8
+    ws = mb.workspace(n, g, r, B)
+    out = torch.empty((n, n), dtype=torch.int32, device="cuda")
+    h = torch.zeros((n * n,), dtype=torch.uint16)
+    with pytest.raises(Exception):
+        mb.ask_to_host(W.DEFAULT_REGION, n, 65536, g, r, B, h, out, ws)
+    assert not h.numpy().any()
+
+
 # ----------------------------------------------------------------------------- full sizes
 def _sample_tiles(g, k, seed):
     rng = np.random.default_rng(seed)
