@@ -61,7 +61,7 @@ int main()
 {
     float *out;
     long long *cyc, h;
-    cudaMalloc(&out, 1024 * 4);
+    cudaMalloc(&out, 4096 * 4);
     cudaMalloc(&cyc, 8);
     const char *names[] = {"fadd_chain", "fmul_chain", "dwell_step", "dwell_step_x2_orbits"};
     for (int m = 0; m < 4; ++m) {
@@ -69,7 +69,15 @@ int main()
             k<<<1, 32>>>(m, -0.1f, 0.1f, out, cyc);
             cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
         }
-        printf("{\"mode\": \"%s\", \"cycles_per_iter\": %.2f}\n", names[m], (double)h / N);
+        printf("{\"mode\": \"%s\", \"warps_per_block\": 1, \"cycles_per_iter\": %.2f}\n", names[m], (double)h / N);
+    }
+    // one block of w warps on one SM (w / 4 warps per sub-partition): the dwell step
+    for (int w = 2; w <= 32; w *= 2) {
+        for (int rep = 0; rep < 3; ++rep) {
+            k<<<1, 32 * w>>>(2, -0.1f, 0.1f, out, cyc);
+            cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
+        }
+        printf("{\"mode\": \"dwell_step\", \"warps_per_block\": %d, \"cycles_per_iter\": %.2f}\n", w, (double)h / N);
     }
     return 0;
 }
