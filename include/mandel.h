@@ -119,11 +119,12 @@ enum {
 #define MANDEL_FLAG_FLAT 8u      /* B200 scheme: plain one-thread-per-pixel border and leaf
                                     kernels instead of the lane-refill ones (A/B baseline;
                                     same image)                                            */
-/* Like MANDEL_FLAG_TILE_COST, but estimated: only the pixels on the lattice (x + y) mod 64 == 0
- * are counted, each weighted by 64 (B200 scheme, refill kernels; elsewhere, or together with
- * MANDEL_FLAG_STATS / MANDEL_FLAG_TILE_COST, the call counts exactly).  A ~1-2% estimate of
- * every tile's executed iterations at 1/64 of the counting work: the multi-GPU deal's
- * per-step feedback.                                                          */
+/* Like MANDEL_FLAG_TILE_COST, but estimated, and a time proxy rather than an iteration count:
+ * only the pixels on the lattice (x + y) mod 64 == 0 are counted, each as 64 * (dwell + 64) --
+ * its iterations plus 64 for the engine's per-pixel work (B200 scheme, refill kernels;
+ * elsewhere, or together with MANDEL_FLAG_STATS / MANDEL_FLAG_TILE_COST, the call counts
+ * exact iterations).  At 1/64 of the counting work: the multi-GPU deal's per-step feedback
+ * (DESIGN.md §9).                                                                            */
 #define MANDEL_FLAG_TILE_COST_SAMPLED 32u
 #define MANDEL_FLAG_SERIAL 16u   /* run every fill on the main stream after its level instead
                                     of as a concurrent graph branch (A/B; same image)       */

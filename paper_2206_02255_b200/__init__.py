@@ -131,8 +131,9 @@ def ask(region: Sequence[float], n: int, maxdwell: int, g: int, r: int, B: int, 
     instead of concurrent graph branches (A/B comparisons, same image); groups: independent
     level-synchronous chains over round-robin subsets of the tiles, run as parallel graph
     branches.  tile_cost: True counts every level-0 tile's executed iterations exactly;
-    "sampled" estimates them from the 1/64 pixel lattice (x + y) % 64 == 0 (B200 scheme; the
-    multi-GPU deal's per-step feedback)."""
+    "sampled" estimates a time proxy from the 1/64 pixel lattice (x + y) % 64 == 0, each
+    sampled pixel counted as 64 * (dwell + 64): iterations plus the per-pixel work (B200
+    scheme; the multi-GPU deal's per-step feedback)."""
     out = _image(n, out)
     _check_device(out, ws, stream=stream)
     if ws is None:

@@ -1013,6 +1013,14 @@ struct TcStorage<false> {
 // the C3 step even with the counting itself removed).
 constexpr int CM_NONE = 0, CM_STATS = 1, CM_SAMPLE = 2;
 constexpr int TC_SAMPLE_LOG2 = 6;
+// CM_SAMPLE counts each sampled pixel as its dwell plus TC_PX_COST: the deal balances time,
+// and a computed pixel costs the engine's per-pixel work (fetch, park, replay, store) besides
+// its iterations.  64 balanced the 8-way deal best in time (max/mean 1.023 -> 1.011 at C3,
+// 1.036 -> 1.023 at C4, 1.048 -> 1.007 at C5 against 0; profiles/r02_deal_proxy.jsonl).
+#ifndef MANDEL_TC_PX_COST
+#define MANDEL_TC_PX_COST 64
+#endif
+constexpr int TC_PX_COST = MANDEL_TC_PX_COST;
 
 template <int CM, bool RING>
 struct StoreSink {
@@ -1042,7 +1050,7 @@ struct StoreSink {
             count_tile(x, y, v);
         } else if (CM == CM_SAMPLE) { // 1/64 of the pixels: global reductions (no return value)
             if (((x + y) & ((1 << TC_SAMPLE_LOG2) - 1)) == 0)
-                atomicAdd(&a->tile_cost[tile_of(*a, x, y)], (unsigned long long)v << TC_SAMPLE_LOG2);
+                atomicAdd(&a->tile_cost[tile_of(*a, x, y)], (unsigned long long)(v + TC_PX_COST) << TC_SAMPLE_LOG2);
         }
     }
 };
