@@ -186,6 +186,7 @@ struct LevelArgs {
     uint32_t capP;           // parent slots of one bucket block of an OLT buffer
     uint32_t capL;           // leaf entries of one bucket block of the leaf list
     int ngroups;
+    int pdl_late;            // refill kernels trigger their successor in the tail (device tile list)
 };
 
 // Length-bucket list addressing.  A list (subdivided parents of a level, or
@@ -290,6 +291,16 @@ __device__ __forceinline__ void pdl_entry()
 {
 #if MANDEL_PDL
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+// The lane-refill kernels: wait only; they trigger their successor in the tail (refill.cuh
+// pdl_trigger, MANDEL_PDL_LATE).
+__device__ __forceinline__ void pdl_entry_refill(bool late)
+{
+#if MANDEL_PDL
+    if (!(MANDEL_PDL_LATE && late))
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
 }
@@ -1096,7 +1107,7 @@ __device__ __forceinline__ void sink_flush(const StoreSink<CM, RING> &sk, unsign
 template <int CM>
 __global__ void __launch_bounds__(RF_TPB, RFB_MINB) k_b200_border_rf(LevelArgs a_)
 {
-    pdl_entry();
+    pdl_entry_refill(a_.pdl_late != 0);
     const LevelArgs a = with_params(a_);
     __shared__ ParkedPoint s_q[RF_TPB / 32][MANDEL_RFB_PACK ? RF2_QCAP : RF_QCAP];
 #if MANDEL_RFB_PACK && MANDEL_RFB_PRE > 0
@@ -1133,7 +1144,8 @@ __global__ void __launch_bounds__(RF_TPB, RFB_MINB) k_b200_border_rf(LevelArgs a
         s_sv[threadIdx.x >> 5]);
 #else
     refill_loop<MANDEL_RFB_K, MANDEL_RFB_T, MANDEL_RFB_CH>(a.map, a.maxdwell, total, &a.hdr->cursor[a.level], map,
-                                                           sink, s_q[threadIdx.x >> 5], a.level);
+                                                           sink, s_q[threadIdx.x >> 5], a.level, nullptr,
+                                                           a.pdl_late != 0);
 #endif
 #endif
     if (CM == CM_STATS)
@@ -1144,7 +1156,7 @@ __global__ void __launch_bounds__(RF_TPB, RFB_MINB) k_b200_border_rf(LevelArgs a
 template <int CM>
 __global__ void __launch_bounds__(RF_TPB, RFL_MINB) k_b200_leaf_rf(LevelArgs a_)
 {
-    pdl_entry();
+    pdl_entry_refill(a_.pdl_late != 0);
     const LevelArgs a = with_params(a_);
     __shared__ ParkedPoint s_q[RF_TPB / 32][MANDEL_RFL_PACK ? RF2_QCAP : RF_QCAP];
 #if MANDEL_RFL_PACK && MANDEL_RFL_PRE > 0
@@ -1163,7 +1175,7 @@ __global__ void __launch_bounds__(RF_TPB, RFL_MINB) k_b200_leaf_rf(LevelArgs a_)
 #if MANDEL_RFL_PRE > 0
         refill_loop2<MANDEL_RFL_K, MANDEL_RFL2_T, MANDEL_RFL_CH, LeafMap, StoreSink<CM, false>, MANDEL_RFL_PRE>(
             a.map, a.maxdwell, total, &a.hdr->cursor[MAXL], map, sink, s_q[threadIdx.x >> 5], 15,
-            s_sv[threadIdx.x >> 5]);
+            s_sv[threadIdx.x >> 5], a.pdl_late != 0);
 #else
         refill_loop2<MANDEL_RFL_K, MANDEL_RFL2_T, MANDEL_RFL_CH>(a.map, a.maxdwell, total, &a.hdr->cursor[MAXL],
                                                                  map, sink, s_q[threadIdx.x >> 5], 15);

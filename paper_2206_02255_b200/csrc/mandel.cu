@@ -378,6 +378,7 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
     // refill kernels' count mode (SAMPLED reaches here only for the B200 refill path)
     const int cm = stats ? CM_STATS : (k.flags & MANDEL_FLAG_TILE_COST_SAMPLED) ? CM_SAMPLE : CM_NONE;
     const bool flat = (k.flags & MANDEL_FLAG_FLAT) != 0;
+    a.pdl_late = k.dtiles != nullptr; // refill.cuh pdl_trigger
     if (k.scheme == MANDEL_SCHEME_B200 && lay.colT_bytes) {
         a.colT = (int *)(ws + lay.colT);
         a.u_log2 = lay.u_log2;

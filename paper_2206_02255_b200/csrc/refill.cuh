@@ -65,6 +65,27 @@ __device__ __forceinline__ int dwell_per_step(float cr, float ci, int maxdwell)
     return maxdwell;
 }
 
+// Late programmatic launch (MANDEL_PDL_LATE, calls with a device tile list): a refill kernel
+// waits for its predecessor at entry but lets its successor launch only once its warps find
+// the cursor exhausted, i.e. in the level's tail.  Triggered at entry (pdl_entry), the
+// successor's blocks are scheduled at once and wait in SM slots for the whole kernel, where
+// the overlapped fill kernels would run -- and a device-list call sizes its grids for all g^2
+// tiles, so many of them.  (Full images: the early trigger is 1% faster, the late one hides
+// less launch latency; profiles/r02_ab_pdl_late.jsonl.)
+#ifndef MANDEL_PDL // programmatic dependent launch of the level chain (ask_kernels.cuh)
+#define MANDEL_PDL 1
+#endif
+#ifndef MANDEL_PDL_LATE
+#define MANDEL_PDL_LATE 1
+#endif
+__device__ __forceinline__ void pdl_trigger(bool late)
+{
+#if MANDEL_PDL && MANDEL_PDL_LATE
+    if (late)
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
 // A parked chunk-start point awaiting its exact replay.
 struct ParkedPoint {
     int px, py;
@@ -362,7 +383,8 @@ __device__ __forceinline__ int rf2_prepass_more(SvPoint *sv, int m, const PixMap
 template <int K, int T, int CH, class Map, class Sink, int PRE = 0>
 __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint32_t total,
                                             unsigned long long *cursor, const Map &map, Sink &sink,
-                                            ParkedPoint *q, int tslot = 0, SvPoint *sv = nullptr)
+                                            ParkedPoint *q, int tslot = 0, SvPoint *sv = nullptr,
+                                            bool pdl_late = false)
 {
     // Active warps: a launch with few pixels per lane runs like a thread-per-pixel kernel
     // (every warp waits for its slowest lane and there is nothing to refill from), so only
@@ -455,6 +477,7 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
                     b = __shfl_sync(FULL, b, 0);
                     if (b >= total) {
                         exhausted = true;
+                        pdl_trigger(pdl_late);
                         break;
                     }
                     const uint32_t e = (uint32_t)min(b + (unsigned long long)grab, (unsigned long long)total);
@@ -496,6 +519,7 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
                 b = __shfl_sync(FULL, b, 0);
                 if (b >= total) {
                     exhausted = true;
+                    pdl_trigger(pdl_late);
 #ifdef MANDEL_RF_TRACE
                     tr_ex = rf_now();
 #endif
@@ -713,7 +737,8 @@ __device__ __forceinline__ bool rf2_fetch(uint32_t t, const PixMap &pm, int maxd
 template <int K, int T, int CH, class Map, class Sink, int PRE = 0>
 __device__ __forceinline__ void refill_loop2(const PixMap &pm, int maxdwell, uint32_t total,
                                              unsigned long long *cursor, const Map &map, Sink &sink,
-                                             ParkedPoint *q, int tslot = 0, SvPoint *sv = nullptr)
+                                             ParkedPoint *q, int tslot = 0, SvPoint *sv = nullptr,
+                                             bool pdl_late = false)
 {
     constexpr uint32_t PPL = 8; // pixels per slot before a warp is worth activating
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -825,6 +850,7 @@ __device__ __forceinline__ void refill_loop2(const PixMap &pm, int maxdwell, uin
                 b = __shfl_sync(FULL, b, 0);
                 if (b >= total) {
                     exhausted = true;
+                    pdl_trigger(pdl_late);
                     break;
                 }
                 const uint32_t e = (uint32_t)min(b + (unsigned long long)gpre, (unsigned long long)total);
@@ -920,6 +946,7 @@ __device__ __forceinline__ void refill_loop2(const PixMap &pm, int maxdwell, uin
                 b = __shfl_sync(FULL, b, 0);
                 if (b >= total) {
                     exhausted = true;
+                    pdl_trigger(pdl_late);
 #ifdef MANDEL_RF_TRACE
                     tr_ex = rf_now();
 #endif

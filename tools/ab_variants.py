@@ -55,12 +55,20 @@ def worker(name, workloads, reps, check):
         out = torch.empty((w.n, w.n), dtype=torch.int32, device="cuda")
         ws = mb.workspace(w.n, w.g, w.r, w.B)
         tiles = None
+        dev = share.endswith("d")  # C3r8d: the same rank through mandel_ask_dtiles + sampled costs
+        share = share.rstrip("d")
         if share:
             mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, tile_cost=True)
             exact = mb.tile_costs(ws, w.g)
             parts = deal.deal("lpt", w.g, int(share), exact)
             tiles = max(parts, key=lambda p: sum(exact[k] for k in p))
-        f = lambda: mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, tiles=tiles)  # noqa: E731
+        if dev:
+            dt = torch.tensor(tiles, dtype=torch.int32, device="cuda")
+            dn = torch.tensor([len(tiles)], dtype=torch.int32, device="cuda")
+            f = lambda: mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws,  # noqa: E731
+                               dtiles=(dt, dn), tile_cost="sampled")
+        else:
+            f = lambda: mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, tiles=tiles)  # noqa: E731
         for _ in range(2):
             f()
         torch.cuda.synchronize()
@@ -74,7 +82,11 @@ def worker(name, workloads, reps, check):
             e.synchronize()
             ts.append(s.elapsed_time(e))
         res = {"variant": name, "w": wl, "ms": statistics.median(ts), "ms_min": min(ts)}
-        mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, tiles=tiles, timing=True)
+        if dev:
+            mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, dtiles=(dt, dn), tile_cost="sampled",
+                   timing=True)
+        else:
+            mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, tiles=tiles, timing=True)
         torch.cuda.synchronize()
         kt, lv = {}, {}
         for k in mb.kernel_times():
