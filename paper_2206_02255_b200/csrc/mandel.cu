@@ -197,6 +197,7 @@ std::vector<std::unique_ptr<DevInfo>> g_dev;
 unsigned long long g_clock = 0, g_next_id = 0, g_last_timed = 0;
 long long g_captures = 0; // graphs captured so far (mandel_ask_graph_captures)
 constexpr size_t kMaxGraphs = 64;
+int g_prio_hi = 0, g_prio_lo = 0; // set once by dev_info (cudaDeviceGetStreamPriorityRange)
 
 int dev_info(int dev, DevInfo *&out)
 {
@@ -206,6 +207,7 @@ int dev_info(int dev, DevInfo *&out)
     if (!di.cap) {
         CK(cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev));
         CK(cudaMemcpyToSymbol(c_num_sms, &di.sms, sizeof(int)));
+        CK(cudaDeviceGetStreamPriorityRange(&g_prio_lo, &g_prio_hi));
         CK(cudaStreamCreateWithFlags(&di.cap, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&di.start, cudaEventDisableTiming));
         for (int i = 0; i < MAXG; ++i) {
@@ -247,6 +249,17 @@ int resident_grid(K kernel, int tpb, int sms, size_t cap_blocks)
 #define MANDEL_CLASSIFY_QUARTER_D 32
 #endif
 
+// Block-scheduling priorities (MANDEL_PRIO): the level chain (border, classification, leaf)
+// at the device's greatest priority, the overlapped fills at the least; the graph is
+// instantiated with cudaGraphInstantiateFlagUseNodePriority so the per-node priorities apply
+// (without that flag the captured priorities are ignored).  An overlapped fill grid otherwise
+// takes the SM slots a border kernel frees and the next level's classification waits behind it
+// (refill trace: 67-167 us between C3 levels against 12-87 us of classification):
+// C3 7.71 -> 7.63 ms, C5 21.02 -> 20.86, C4 32.07 -> 31.51 (profiles/r02_ab_prio_fills.jsonl).
+#ifndef MANDEL_PRIO
+#define MANDEL_PRIO 1
+#endif
+
 // Launch on `s` with programmatic stream serialization (PDL, see pdl_entry()): under stream
 // capture this becomes a programmatic edge to the previous kernel node on `s`.
 template <typename... KArgs>
@@ -257,11 +270,30 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, cudaStream
     cfg.blockDim = dim3((unsigned)block);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = s;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = MANDEL_PDL ? 1 : 0;
+    at[1].id = cudaLaunchAttributePriority;
+    at[1].val.priority = g_prio_hi;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = MANDEL_PRIO ? 2 : 1;
+    return cudaLaunchKernelEx(&cfg, kernel, a);
+}
+
+// A fill kernel at the least priority (MANDEL_PRIO), else a plain launch.
+template <typename... KArgs>
+cudaError_t launch_fill(void (*kernel)(KArgs...), int grid, int block, cudaStream_t s, LevelArgs a)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributePriority;
+    at[0].val.priority = g_prio_lo;
+    cfg.attrs = at;
+    cfg.numAttrs = MANDEL_PRIO ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kernel, a);
 }
 
@@ -518,10 +550,10 @@ int enqueue_ask(const Key &k, const Layout &lay, const Group &grp, int ngroups, 
             TBEGIN(sf);
             if (vec) {
                 int gsz = resident_grid(k_fill<true>, 256, sms, blocks);
-                k_fill<true><<<gsz, 256, 0, sf>>>(a);
+                CK(launch_fill(k_fill<true>, gsz, 256, sf, a));
             } else {
                 int gsz = resident_grid(k_fill<false>, 256, sms, blocks);
-                k_fill<false><<<gsz, 256, 0, sf>>>(a);
+                CK(launch_fill(k_fill<false>, gsz, 256, sf, a));
             }
             CK(cudaGetLastError());
             TEND(MANDEL_KIND_FILL, l, sf);
@@ -896,7 +928,7 @@ int ask_launch(mandel_region reg, int64_t n, int32_t maxdwell, int32_t g, int32_
             free_entry(e);
             return erc ? erc : cuda_fail(ce, "cudaStreamEndCapture");
         }
-        ce = cudaGraphInstantiate(&e.exec, graph, 0);
+        ce = cudaGraphInstantiateWithFlags(&e.exec, graph, MANDEL_PRIO ? cudaGraphInstantiateFlagUseNodePriority : 0);
         cudaGraphDestroy(graph);
         if (ce != cudaSuccess) {
             free_entry(e);

@@ -40,6 +40,8 @@ def fetch(lib):
 
 def summarize(buf, label):
     out = []
+    live_all = buf[:, :, 2] > 0
+    g0 = int(buf[:, :, 0][live_all].astype(np.int64).min()) if live_all.any() else 0
     for slot in range(16):
         t = buf[slot]
         live = t[:, 2] > 0
@@ -55,7 +57,8 @@ def summarize(buf, label):
                "end_p50_us": float(np.percentile(ends, 50) / 1e3),
                "end_p90_us": float(np.percentile(ends, 90) / 1e3),
                "end_p99_us": float(np.percentile(ends, 99) / 1e3),
-               "end_max_us": float(ends.max() / 1e3)}
+               "end_max_us": float(ends.max() / 1e3),
+               "abs_start_us": float((t0 - g0) / 1e3), "abs_end_us": float((t[:, 2].max() - g0) / 1e3)}
         out.append(row)
         print(json.dumps(row), flush=True)
     return out
@@ -65,6 +68,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("workload", nargs="?", default="C3")
     ap.add_argument("--P", type=int, default=8)
+    ap.add_argument("--dtiles", action="store_true",
+                    help="the heaviest rank of an LPT deal on exact costs through mandel_ask_dtiles with "
+                         "sampled costs and overlapped fills (bench.py's N > 1 step); abs_* columns give gaps")
     a = ap.parse_args()
     lib = _lib.load()
     lib.mandel_debug_rf_trace.restype = ctypes.c_int
@@ -77,6 +83,19 @@ def main():
     mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, tile_cost=True)
     exact = mb.tile_costs(ws, w.g)
     heavy = max(deal.deal("costrank", w.g, a.P, costs), key=lambda p: sum(exact[k] for k in p))
+    if a.dtiles:
+        heavy = max(deal.deal("lpt", w.g, a.P, exact), key=lambda p: sum(exact[k] for k in p))
+        dt = torch.tensor(heavy, dtype=torch.int32, device="cuda")
+        dn = torch.tensor([len(heavy)], dtype=torch.int32, device="cuda")
+        for label, kw in (("full", {}), (f"rank_of_{a.P}_dtiles", dict(dtiles=(dt, dn), tile_cost="sampled"))):
+            for _ in range(2):
+                mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, **kw)
+            torch.cuda.synchronize()
+            lib.mandel_debug_rf_trace_clear()
+            mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, **kw)
+            torch.cuda.synchronize()
+            summarize(fetch(lib), label)
+        return
     for label, tiles in (("full", None), (f"rank_of_{a.P}", heavy)):
         mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, tiles=tiles, serial=True)
         torch.cuda.synchronize()
