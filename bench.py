@@ -168,11 +168,12 @@ def _config(w: W.Workload, args, world: int):
                         f"ASK g={w.g} r={w.r} B={w.B}",
             "n": w.n, "maxdwell": w.maxdwell, "g": w.g, "r": w.r, "B": w.B, "region": list(w.region),
             "scheme": args.scheme, "deal": "lpt (device)" if world > 1 else "all tiles",
-            "deal_plan": ("inside every timed step: sampled per-tile cost counters of this step's render "
-                          "(1/64 pixel lattice), then on a side stream overlapping the next step's render: NCCL "
-                          "all-reduce of the g*g counters and the device LPT deal (mandel_deal_lpt) of the step "
-                          "after next, which waits for it on the main stream; the first steps are dealt on an "
-                          "n/32, maxdwell/8 preview")
+            "deal_plan": ("inside the timed steps, every 3rd step (multigpu.SAMPLE_EVERY): sampled per-tile "
+                          "cost counters of that step's render (1/64 pixel lattice, dwell + 64 per pixel), then "
+                          "on a side stream overlapping the next step's render: NCCL all-reduce of the g*g "
+                          "counters and the device LPT deal (mandel_deal_lpt) of the step after next, which waits "
+                          "for it on the main stream; the other steps render without counters; the first steps "
+                          "are dealt on an n/32, maxdwell/8 preview")
             if world > 1 else None,
             "parallelism": f"tiles{world}",
             "l2": "output image 4*n^2 B >> 126 MB L2, rewritten every step; plus a 256 MiB L2 flush "
@@ -224,12 +225,13 @@ def main():
     n = w.n
 
     # ---- partition.  N > 1: a device-resident LPT deal of the level-0 tiles
-    # (multigpu.DevicePlan).  Every timed step renders this rank's tiles with sampled per-tile
-    # cost counters (MANDEL_FLAG_TILE_COST_SAMPLED) and hands them to a side stream, which
-    # all-reduces them across ranks and re-deals on the device (mandel_deal_lpt) for the step
-    # after next while the next step renders: the plan is inside the timed region's wall time
-    # (its events sit on the main stream, which waits for the plan a step uses), off the
-    # critical path.  The first steps are dealt on an n/32, maxdwell/8 preview.
+    # (multigpu.DevicePlan).  Every SAMPLE_EVERY-th timed step (3) renders this rank's tiles
+    # with sampled per-tile cost counters (MANDEL_FLAG_TILE_COST_SAMPLED) and hands them to a
+    # side stream, which all-reduces them across ranks and re-deals on the device
+    # (mandel_deal_lpt) for the step after next while the next step renders; the other steps
+    # render without counters.  The plan is inside the timed region's wall time (its events
+    # sit on the main stream, which waits for the plan a step uses), off the critical path.
+    # The first steps are dealt on an n/32, maxdwell/8 preview.
     out = torch.empty((n, n), dtype=torch.int32, device=dev)
     ws = mb.workspace(n, w.g, w.r, w.B, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)

@@ -1023,7 +1023,10 @@ struct TcStorage<false> {
 // __syncthreads gets divergence checks around every ballot of the engine (measured: +4% on
 // the C3 step even with the counting itself removed).
 constexpr int CM_NONE = 0, CM_STATS = 1, CM_SAMPLE = 2;
-constexpr int TC_SAMPLE_LOG2 = 6;
+#ifndef MANDEL_TC_SAMPLE_LOG2
+#define MANDEL_TC_SAMPLE_LOG2 6
+#endif
+constexpr int TC_SAMPLE_LOG2 = MANDEL_TC_SAMPLE_LOG2;
 // CM_SAMPLE counts each sampled pixel as its dwell plus TC_PX_COST: the deal balances time,
 // and a computed pixel costs the engine's per-pixel work (fetch, park, replay, store) besides
 // its iterations.  64 balanced the 8-way deal best in time (max/mean 1.023 -> 1.011 at C3,

@@ -107,6 +107,11 @@ def gather_image(img, parts: Sequence[Sequence[int]], g: int, rank: int, dst: in
 
 
 PREVIEW_SHRINK, PREVIEW_DWELL_SHRINK = 32, 8  # n/32, maxdwell/8 (profiles/r02_preview_study.jsonl)
+# Frames between two sampled (counted) renders: the counters cost ~2.4% of a rank's step
+# (tools/ab_variants.py C4r8d vs C4r8n), so only every third frame counts and re-deals; with
+# two alternating tile lists and an odd period, each list is re-dealt every 2 * SAMPLE_EVERY
+# frames.
+SAMPLE_EVERY = 3
 
 
 class DevicePlan:
@@ -121,7 +126,7 @@ class DevicePlan:
     off the critical path but still inside the timed region's wall time)."""
 
     def __init__(self, w, world: int, rank: int, device, shrink: int = PREVIEW_SHRINK,
-                 dwell_shrink: int = PREVIEW_DWELL_SHRINK):
+                 dwell_shrink: int = PREVIEW_DWELL_SHRINK, sample_every: int = SAMPLE_EVERY):
         import torch
         from . import ask, workspace
         self.w, self.world, self.rank, self.device = w, world, rank, device
@@ -140,6 +145,8 @@ class DevicePlan:
         self.pws = workspace(self.pn, w.g, w.r, self.pB, device=device)
         self.pout = torch.empty((self.pn, self.pn), dtype=torch.int32, device=device)
         self._ask = ask
+        self.sample_every = max(1, int(sample_every))
+        self.n_steps = 0
 
     @property
     def tiles(self):
@@ -171,15 +178,23 @@ class DevicePlan:
                          dtiles=(self.tiles, self.count), tile_cost=tile_cost, timing=timing)
 
     def step(self, out, ws, allreduce, timing=False):
-        """One frame: wait for the plan that chose this step's tiles, render them, hand the
-        sampled counters to the side stream, which all-reduces them (`allreduce(t)`: in place,
-        sum over ranks) and deals the step after next into the list this step just used."""
+        """One frame: wait for the plan that chose this step's tiles and render them.  Every
+        `sample_every`-th frame renders with the sampled counters and hands them to the side
+        stream, which all-reduces them (`allreduce(t)`: in place, sum over ranks) and deals the
+        step after next into the list this step just used; the other frames render without
+        counters and keep their list.  Every rank calls allreduce on the same frames."""
         import torch
         from . import deal_lpt, tile_cost_view
         w, k = self.w, self.cur
         main = torch.cuda.current_stream(self.device)
         if self.ev_plan[k] is not None:
             main.wait_event(self.ev_plan[k])
+        sample = self.n_steps % self.sample_every == 0
+        self.n_steps += 1
+        if not sample:
+            self.render(out, ws, tile_cost=False, timing=timing)
+            self.cur = 1 - k
+            return
         self.render(out, ws, timing=timing)
         cb = self.cbuf2[k]
         cb.copy_(tile_cost_view(ws, w.n, w.g, w.r, w.B))

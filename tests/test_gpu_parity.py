@@ -476,7 +476,7 @@ def test_device_plan_frame_loop(mb):
     w = W.Workload("fl", W.DEFAULT_REGION, 1024, 1000, 16, 2, 16)
     A, _ = oracle.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B)
     P = 4
-    plans = [multigpu.DevicePlan(w, P, r, torch.device("cuda")) for r in range(P)]
+    plans = [multigpu.DevicePlan(w, P, r, torch.device("cuda"), sample_every=1) for r in range(P)]
     c0 = torch.zeros(w.g * w.g, dtype=torch.int64, device="cuda")
     plans[0].preview_costs(c0)
     for p in plans:
@@ -505,6 +505,46 @@ def test_device_plan_frame_loop(mb):
         for p in plans:
             k = 1 - p.cur
             assert p.tiles2[k][: int(p.count2[k].item())].tolist() == want[p.rank]
+
+
+def test_device_plan_sampling_period(mb):
+    """The default frame loop counts and re-deals only every SAMPLE_EVERY-th frame (odd, so
+    both alternating lists are re-dealt): every frame's image is the oracle's, the partition is
+    complete every frame, the counters are all-reduced on the same frames on every rank, and
+    both lists end up dealt on the sampled costs."""
+    from paper_2206_02255_b200 import deal, multigpu
+    w = W.Workload("fs", W.SEAHORSE_REGION, 1024, 900, 16, 2, 16)
+    A, _ = oracle.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B)
+    P, E = 3, multigpu.SAMPLE_EVERY
+    assert E % 2 == 1
+    plans = [multigpu.DevicePlan(w, P, r, torch.device("cuda")) for r in range(P)]
+    c0 = torch.zeros(w.g * w.g, dtype=torch.int64, device="cuda")
+    plans[0].preview_costs(c0)
+    for p in plans:
+        p.deal(c0, both=True)
+    wss = [mb.workspace(w.n, w.g, w.r, w.B) for _ in range(P)]
+    out = torch.full((w.n, w.n), -1, dtype=torch.int32, device="cuda")
+    calls = []
+    for frame in range(2 * E + 1):
+        out.fill_(-1)
+        lists = [p.host_tiles() for p in plans]
+        assert sorted(k for l in lists for k in l) == list(range(w.g * w.g)), frame
+        views = []
+        for p, ws in zip(plans, wss):
+            p.step(out, ws, lambda t: views.append(t))
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), A), frame
+        assert len(views) in (0, P), frame
+        calls.append(len(views) > 0)
+        if views:  # what the all-reduce would leave: re-deal both ranks' lists on the sum
+            total = sum(views)
+            for v in views:
+                v.copy_(total)
+            for p in plans:
+                k = 1 - p.cur
+                mb.deal_lpt(p.cbuf2[k], P, p.rank, p.tiles2[k], p.count2[k])
+            torch.cuda.synchronize()
+    assert calls == [f % E == 0 for f in range(2 * E + 1)]
 
 
 def test_timing_modes(mb):

@@ -55,8 +55,9 @@ def worker(name, workloads, reps, check):
         out = torch.empty((w.n, w.n), dtype=torch.int32, device="cuda")
         ws = mb.workspace(w.n, w.g, w.r, w.B)
         tiles = None
-        dev = share.endswith("d")  # C3r8d: the same rank through mandel_ask_dtiles + sampled costs
-        share = share.rstrip("d")
+        dev = share.endswith("d") or share.endswith("n")  # C3r8d: the same rank through mandel_ask_dtiles
+        tcm = "sampled" if share.endswith("d") else False  # + sampled costs; C3r8n: without counters
+        share = share.rstrip("dn")
         if share:
             mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, tile_cost=True)
             exact = mb.tile_costs(ws, w.g)
@@ -66,7 +67,7 @@ def worker(name, workloads, reps, check):
             dt = torch.tensor(tiles, dtype=torch.int32, device="cuda")
             dn = torch.tensor([len(tiles)], dtype=torch.int32, device="cuda")
             f = lambda: mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws,  # noqa: E731
-                               dtiles=(dt, dn), tile_cost="sampled")
+                               dtiles=(dt, dn), tile_cost=tcm)
         else:
             f = lambda: mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, tiles=tiles)  # noqa: E731
         for _ in range(2):
@@ -83,7 +84,7 @@ def worker(name, workloads, reps, check):
             ts.append(s.elapsed_time(e))
         res = {"variant": name, "w": wl, "ms": statistics.median(ts), "ms_min": min(ts)}
         if dev:
-            mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, dtiles=(dt, dn), tile_cost="sampled",
+            mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, dtiles=(dt, dn), tile_cost=tcm,
                    timing=True)
         else:
             mb.ask(w.region, w.n, w.maxdwell, w.g, w.r, w.B, out=out, ws=ws, tiles=tiles, timing=True)
