@@ -277,7 +277,8 @@ def main():
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
-    kernels_per_step = mb.kernel_count(n, w.g, w.r, w.B, args.scheme) + (1 if plan is not None else 0)
+    kernels_per_step = mb.kernel_count(n, w.g, w.r, w.B, args.scheme)
+    plan_steps0 = plan.n_steps if plan is not None else 0
 
     stream = torch.cuda.current_stream()
     step_ms, ktime = [], {}
@@ -298,6 +299,11 @@ def main():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+    # kernels launched in the timed region: every step's graph, plus the device deal
+    # (mandel_deal_lpt) of each sampled step of the N > 1 frame loop
+    gpu_launches = kernels_per_step * args.steps
+    if plan is not None:
+        gpu_launches += sum(1 for k in range(plan_steps0, plan_steps0 + args.steps) if k % plan.sample_every == 0)
     # per-kernel breakdown (informational; outside the timed region): every kernel timed
     kall = {}
     for _ in range(3):
@@ -477,7 +483,7 @@ def main():
             "verify_gather": gather,
             "kernel_ms_per_step": kt_all,
             "clocks": clocks, "e2e": e2e,
-            "gpu_launches": kernels_per_step * args.steps,
+            "gpu_launches": gpu_launches,
             "roofline": roofline, "cpu_baseline": cpu}
     print(json.dumps(line), flush=True)
     if world > 1:
