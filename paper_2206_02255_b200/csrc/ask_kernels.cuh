@@ -856,7 +856,7 @@ __global__ void __launch_bounds__(256) k_b200_classify(LevelArgs a_)
             // atomics on a handful of counters serialise in L2).  Same outcomes and slot
             // addressing as decide(): subdivided parents and leaves by length bucket.
             __shared__ int s_cat[RPB];
-            __shared__ uint32_t s_cb[10];
+            __shared__ uint32_t s_cb[10], s_rank[RPB];
             if (t == 0) {
                 int cat = 0; // 0 none, 1 fill, 2+b subdivide (bucket b), 6+b leaf (bucket b)
                 if (valid)
@@ -864,32 +864,43 @@ __global__ void __launch_bounds__(256) k_b200_classify(LevelArgs a_)
                 s_cat[slot] = cat;
             }
             __syncthreads();
-            if (threadIdx.x == 0) {
-                uint32_t c[10];
+            if (threadIdx.x < 32) { // warp 0: per-category counts and ranks by ballot (RPB <= 32)
+                const int k = threadIdx.x;
+                const int cat = k < RPB ? s_cat[k] : 0;
+                const unsigned lt = (1u << k) - 1u;
+                uint32_t n_mine = 0u; // lane c (1..9): the block's count of category c
+                uint32_t rank = 0u;
 #pragma unroll
-                for (int k = 0; k < 10; ++k)
-                    c[k] = 0u;
-                for (int k = 0; k < RPB; ++k)
-                    ++c[s_cat[k]];
-                s_cb[1] = c[1] ? atomicAdd(&a.hdr->n_fill[a.level], c[1]) : 0u;
-                const uint32_t ns = c[2] + c[3] + c[4] + c[5], nl = c[6] + c[7] + c[8] + c[9];
-                if (ns)
-                    atomicAdd(&a.hdr->n_subdiv[a.level], ns);
-                if (nl)
-                    atomicAdd(&a.hdr->n_leaf, nl);
-#pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    s_cb[2 + b] = c[2 + b] ? atomicAdd(&a.hdr->n_sub_b[a.level][b], c[2 + b]) : 0u;
-                    s_cb[6 + b] = c[6 + b] ? atomicAdd(&a.hdr->n_leaf_b[b], c[6 + b]) : 0u;
+                for (int c = 1; c < 10; ++c) {
+                    const unsigned m = __ballot_sync(0xffffffffu, cat == c);
+                    if (cat == c)
+                        rank = (uint32_t)__popc(m & lt);
+                    if (k == c)
+                        n_mine = (uint32_t)__popc(m);
                 }
+                const uint32_t ns = (uint32_t)__popc(__ballot_sync(0xffffffffu, cat >= 2 && cat < 6));
+                const uint32_t nl = (uint32_t)__popc(__ballot_sync(0xffffffffu, cat >= 6));
+                // every append counter of the round at once, one lane each (all in flight)
+                uint32_t b0 = 0u;
+                if (n_mine) {
+                    unsigned *ctr = k == 1 ? &a.hdr->n_fill[a.level]
+                                  : k < 6  ? &a.hdr->n_sub_b[a.level][k - 2]
+                                           : &a.hdr->n_leaf_b[k - 6];
+                    b0 = atomicAdd(ctr, n_mine);
+                }
+                if (k == 10 && ns)
+                    atomicAdd(&a.hdr->n_subdiv[a.level], ns);
+                if (k == 11 && nl)
+                    atomicAdd(&a.hdr->n_leaf, nl);
+                if (k >= 1 && k < 10)
+                    s_cb[k] = b0;
+                if (k < RPB)
+                    s_rank[k] = rank;
             }
             __syncthreads();
             if (t == 0) {
                 const int cat = s_cat[slot];
-                uint32_t rank = 0;
-                for (int k = 0; k < slot; ++k)
-                    rank += s_cat[k] == cat ? 1u : 0u;
-                const uint32_t e = s_cb[cat] + rank;
+                const uint32_t e = s_cb[cat] + s_rank[slot];
                 uint32_t base = UINT_MAX;
                 if (cat == 1)
                     a.fill[e] = make_uint2(off, (uint32_t)lo);
