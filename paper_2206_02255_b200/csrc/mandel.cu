@@ -248,7 +248,10 @@ int resident_grid(K kernel, int tpb, int sms, size_t cap_blocks)
 
 // Classification uses half a warp per region for region sides up to this (ring <= 252 pixels).
 #ifndef MANDEL_CLASSIFY_BLOCK_D // classification: a whole block per region from this side up
-#define MANDEL_CLASSIFY_BLOCK_D 1024 // (256: C3 7.74 ms, 512: 7.71, 1024: 7.69; profiles/r02_ab_classify_block.jsonl)
+#define MANDEL_CLASSIFY_BLOCK_D 512 // (round 2, before the ballot appends: 256: C3 7.74 ms, 512: 7.71, 1024: 7.69,
+                                    // profiles/r02_ab_classify_block.jsonl; with them 512 is 0.2-0.7% faster
+                                    // at C3, C5, C3r8d and C4r8d, 0.15% slower at C4;
+                                    // profiles/r02_ab_classify_block_d_final.jsonl)
 #endif
 #ifndef MANDEL_CLASSIFY_HALF_D
 #define MANDEL_CLASSIFY_HALF_D 64
