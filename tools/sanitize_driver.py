@@ -24,7 +24,8 @@ from paper_2206_02255_b200 import mandel3d as m3  # noqa: E402
 
 def main():
     cases = [(W.SEAHORSE_REGION, 256, 700, 4, 2, 8), (W.NONDYADIC_REGIONS[0], 512, 1500, 8, 4, 4),
-             (W.DEFAULT_REGION, 256, 300, 2, 2, 16)]
+             (W.DEFAULT_REGION, 256, 300, 2, 2, 16),
+             (W.SEAHORSE_REGION, 1024, 600, 2, 2, 32)]  # side-512 regions: block-per-region classify
     n_ok = 0
     for region, n, md, g, r, B in cases:
         A, _ = oracle.ask(region, n, md, g, r, B)
@@ -58,6 +59,18 @@ def main():
         Ad, _ = oracle.ask(region, n, md, g, r, B, tiles=mine)
         assert np.array_equal(buf.cpu().numpy(), Ad)
         n_ok += 1
+        # end to end into host memory: int32 and 16-bit images, whole (banded) and a tile subset
+        h32 = torch.zeros(n * n, dtype=torch.int32).pin_memory()
+        mb.ask_to_host(region, n, md, g, r, B, h32, buf, ws)
+        assert np.array_equal(h32.numpy().reshape(n, n), A)
+        h16 = torch.zeros(n * n, dtype=torch.uint16).pin_memory()
+        mb.ask_to_host(region, n, md, g, r, B, h16, buf, ws)
+        assert np.array_equal(h16.numpy().reshape(n, n).astype(np.int64), A)
+        h16.zero_()
+        mb.ask_to_host(region, n, md, g, r, B, h16, buf, ws, tiles=tiles)
+        got = h16.numpy().reshape(n, n).astype(np.int64)
+        assert np.array_equal(got[At != -1], At[At != -1])
+        n_ok += 3
         if not os.environ.get("SANITIZE_NO_DP"):  # racecheck/synccheck/initcheck cannot follow CDP
             assert np.array_equal(mb.dp(region, n, md, g, r, B).cpu().numpy(), A)
             n_ok += 1
