@@ -166,6 +166,13 @@ def test_validation_before_any_launch(lib):
     assert lib.mandel_ask_tiles(*args, None, 0, 1, 8 << 8, fake, 64, fake, ws_need, None) == 1
     assert _lib.flag_groups(1) == 0 and _lib.flag_groups(8) == 7 << 8
     assert lib.mandel_strerror(2) == b"workspace too small"
+    # end-to-end calls: NULL host buffer; 16-bit image without a stage buffer or with
+    # maxdwell > 65535 (does not fit) -> EINVAL before anything is launched
+    assert lib.mandel_ask_to_host(*args, None, 0, 1, fake, 64, fake, ws_need, None, None) == 1
+    assert lib.mandel_ask_to_host_u16(*args, None, 0, 1, fake, 64, fake, ws_need, None, fake, None) == 1
+    assert lib.mandel_ask_to_host_u16(*args, None, 0, 1, fake, 64, fake, ws_need, fake, None, None) == 1
+    assert lib.mandel_ask_to_host_u16(reg, 64, 65536, 4, 2, 4, None, 0, 1, fake, 64, fake, ws_need, fake, fake,
+                                      None) == 1
 
 
 def test_product_has_no_oracle_dependency():
