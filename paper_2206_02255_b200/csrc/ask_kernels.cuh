@@ -30,8 +30,8 @@ constexpr int DWELL_K = 8;                 // iterations per escape test (dwell.
 #ifndef MANDEL_RFB_T
 #define MANDEL_RFB_T 8
 #endif
-#ifndef MANDEL_RFB_CH
-#define MANDEL_RFB_CH 64
+#ifndef MANDEL_RFB_CH // border grab cap (128: C4 -0.9%, C5 -0.3%, C3 -0.25%, ranks equal against 64;
+#define MANDEL_RFB_CH 128 // profiles/r02_ab_border_ch_t.jsonl)
 #endif
 #ifndef MANDEL_RFL_K
 #define MANDEL_RFL_K 32
