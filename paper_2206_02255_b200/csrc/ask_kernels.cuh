@@ -30,8 +30,11 @@ constexpr int DWELL_K = 8;                 // iterations per escape test (dwell.
 #ifndef MANDEL_RFB_T
 #define MANDEL_RFB_T 8
 #endif
-#ifndef MANDEL_RFB_CH // border grab cap (128: C4 -0.9%, C5 -0.3%, C3 -0.25%, ranks equal against 64;
+#ifndef MANDEL_RFB_CH // border grab cap (128: C4 -0.9%, C5 -0.3%, C3 -0.25% against 64;
 #define MANDEL_RFB_CH 128 // profiles/r02_ab_border_ch_t.jsonl)
+#endif
+#ifndef MANDEL_RFB_CH_DEV // ... and for device-tile-list calls (one rank's share of the N > 1 step),
+#define MANDEL_RFB_CH_DEV 64 // where 128 unbalanced the 8-way C4 deal (6.85x vs 7.07x emulated)
 #endif
 #ifndef MANDEL_RFL_K
 #define MANDEL_RFL_K 32
@@ -1159,7 +1162,7 @@ __global__ void __launch_bounds__(RF_TPB, RFB_MINB) k_b200_border_rf(LevelArgs a
 #else
     refill_loop<MANDEL_RFB_K, MANDEL_RFB_T, MANDEL_RFB_CH>(a.map, a.maxdwell, total, &a.hdr->cursor[a.level], map,
                                                            sink, s_q[threadIdx.x >> 5], a.level, nullptr,
-                                                           a.pdl_late != 0);
+                                                           a.pdl_late != 0, a.pdl_late ? MANDEL_RFB_CH_DEV : 0u);
 #endif
 #endif
     if (CM == CM_STATS)

@@ -384,7 +384,7 @@ template <int K, int T, int CH, class Map, class Sink, int PRE = 0>
 __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint32_t total,
                                             unsigned long long *cursor, const Map &map, Sink &sink,
                                             ParkedPoint *q, int tslot = 0, SvPoint *sv = nullptr,
-                                            bool pdl_late = false)
+                                            bool pdl_late = false, uint32_t ch_cap = 0)
 {
     // Active warps: a launch with few pixels per lane runs like a thread-per-pixel kernel
     // (every warp waits for its slowest lane and there is nothing to refill from), so only
@@ -405,7 +405,8 @@ __device__ __forceinline__ void refill_loop(const PixMap &pm, int maxdwell, uint
     unsigned long long tr_start = rf_now(), tr_ex = 0, tr_px = 0;
 #endif
     uint32_t grab = total / (4u * active);
-    grab = grab < 8u ? 8u : (grab > (uint32_t)CH ? (uint32_t)CH : grab);
+    const uint32_t chx = (ch_cap && ch_cap < (uint32_t)CH) ? ch_cap : (uint32_t)CH; // runtime cap <= CH
+    grab = grab < 8u ? 8u : (grab > chx ? chx : grab);
     // exact grabs (below) only for launches with few pixels per warp: there a window of long
     // pixels held by one warp is the level's tail; in big launches the extra cursor atomics
     // cost more than the windows (C3's deep border levels)
