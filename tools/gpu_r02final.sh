@@ -1,7 +1,7 @@
 # Closing evidence of round 2 (final kernels): bench lines C3 (default), C5, C4; ncu launch list
 # of the bench command; ncu --set full of one C3 step + Ex (tools/gpu_prof.sh); GPU tests; smoke.
 mkdir -p gpurun_out
-TAG=${TAG:-r02k}
+TAG=${TAG:-r02l}
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail gpurun_out/build.log; exit 1; }
 timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu_${TAG}.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/pytest_gpu_${TAG}.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()"; echo smoke=$?
